@@ -1,0 +1,132 @@
+/*
+ * psa.h — C ABI of the B200-native Pyramid Sparse Attention (PSA) forward path.
+ *
+ * One shared library (libpsa.so, sm_100a) exports these entry points. Each one replaces a
+ * function of the reference package `pyrattn` (mounted at /root/reference/pkg); the cited
+ * file:line is the reference interface whose semantics it reproduces. The Python layer
+ * `paper_2512_04025_b200` binds them with ctypes and keeps the reference names.
+ *
+ * Conventions (all entry points):
+ *   - return PSA_OK (0) on success; PSA_EINVAL (-2) maps to ValidationError,
+ *     PSA_ENUMERIC (-4) to NumericError, PSA_ECUDA (-5) to RuntimeError; psa_last_error()
+ *     returns a thread-local message for the last failure.
+ *   - tensor arguments are DEVICE pointers to contiguous row-major arrays; bf16 tensors are
+ *     passed as `const void*` (raw 16-bit payloads). The caller allocates every output and
+ *     workspace; the library never calls cudaMalloc.
+ *   - `stream` is a cudaStream_t; every call is asynchronous and stream-ordered, no host
+ *     synchronisation happens inside. Small host arrays (thresholds, counts) are copied into
+ *     kernel parameters before the call returns.
+ *   - Re-entrant: no mutable global state besides the thread-local error string and a cached
+ *     driver entry point.
+ *   - Shapes: `bh` = batch*heads; Q is [batch, hq, n, d], K/V are [batch, hkv, n, d]
+ *     (hq % hkv == 0; q head h reads kv head h / (hq/hkv)).
+ */
+#ifndef PSA_H_
+#define PSA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PSA_OK 0
+#define PSA_EINVAL (-2)
+#define PSA_ENUMERIC (-4)
+#define PSA_ECUDA (-5)
+
+/* Last error message of the calling thread ("" if none). */
+const char* psa_last_error(void);
+
+/* Library/ABI version (major*100 + minor). */
+int psa_version(void);
+
+/*
+ * K1 — pyramid build.  Replaces build_pyramid / _pool_stack / mean_pool_rows
+ * (pkg/src/pyrattn/blocks.py:86-109, pkg/src/pyrattn/linalg.py:46-58).
+ * k, v      : bf16 [bh, n, d]
+ * k_pyr/v_pyr: bf16 buffers holding levels 2..levels back to back; level h occupies
+ *             [bh, n >> (h-1), d] starting at element offset d * sum_{h'=2}^{h-1} bh*(n >> (h'-1)).
+ *             Level 1 is the raw K/V (not copied).
+ * Each level is the fp64 dyadic mean of raw rows rounded once to bf16 (RNE).
+ * nonfinite : optional device int32 flag, OR-ed with 1 if any K/V entry is NaN/Inf.
+ */
+int psa_pyramid_build(const void* k, const void* v, int64_t bh, int64_t n, int d, int b_k,
+                      int levels, void* k_pyr, void* v_pyr, int32_t* nonfinite, void* stream);
+
+/*
+ * Similarity cap (Alg. 3).  Replaces level_cap_from_similarity / _strided_block_similarity
+ * (pkg/src/pyrattn/mask.py:347-399).  sim_taus: HOST array of levels-1 thresholds.
+ * caps: int8 [bh, n/b_k], each in 1..levels.
+ */
+int psa_similarity_caps(const void* k, int64_t bh, int64_t n, int d, int b_k, int levels,
+                        const double* sim_taus, int8_t* caps, void* stream);
+
+/*
+ * K2 — sampled importance.  Replaces importance_sampled (pkg/src/pyrattn/importance.py:52-85).
+ * q_rows/k_rows: DEVICE int32 tables of sampled row indices inside a head, in the order the
+ *   reference's single seeded generator produces them (n_q*s_q and n_k*s_k entries).
+ * reducer: 0 = max, 1 = mean.  scores: fp64 [batch*hq, n_q, n_k].
+ * Logits are formed in fp64 (exact for bf16 inputs) and divided by sqrt(d) as the reference
+ * does; the row softmax over all n_k*s_k sampled keys is fp64.
+ * workspace: psa_importance_workspace_bytes(...) bytes of device memory.
+ */
+size_t psa_importance_workspace_bytes(int64_t bhq, int n_q, int s_q, int n_k);
+int psa_importance_sampled(const void* q, const void* k, int64_t batch, int hq, int hkv,
+                           int64_t n, int d, int b_q, int b_k, const int32_t* q_rows,
+                           const int32_t* k_rows, int s_q, int s_k, int reducer,
+                           double* scores, void* workspace, void* stream);
+
+/*
+ * K3 — level assignment + compact plan.  Replaces assign_threshold / binary_mask /
+ * assign_quantile (pkg/src/pyrattn/mask.py:293-344), combine_mask (mask.py:402-412) and
+ * causal_premask (mask.py:489-514), and emits the selected-block lists the attention
+ * kernel walks.
+ * mode 0 (threshold): taus = HOST array of n_cuts thresholds (Alg. 2: stable descending sort,
+ *   exactly-rounded row total, sequential Neumaier cumulative sum, searchsorted 'left').
+ * mode 1 (quantile) : counts = HOST array of n_cuts cumulative rank counts
+ *   (mask.py:326-329 computed on the host exactly as the reference does).
+ * caps: optional int8 [batch*hkv, n_k]; causal: apply the causal pre-pass.
+ * Outputs: level_map int8 [batch*hq, n_q, n_k];
+ *   plan_csr uint16 [batch*hq*n_q, n_k]: per (head, query block) the selected blocks as
+ *     (j | (level << 12)), level-major (level 1 first), ascending j within a level;
+ *   plan_info int32 [batch*hq*n_q, 2]: (number of entries, number of 128-row KV tiles);
+ *   level_counts uint64 [levels+1] (accumulated: caller zeroes it).
+ */
+int psa_assign_levels(const double* scores, int64_t batch, int hq, int hkv, int n_q, int n_k,
+                      int mode, const double* taus, const int32_t* counts, int n_cuts,
+                      const int8_t* caps, int causal, int b_q, int b_k, int levels,
+                      int8_t* level_map, uint16_t* plan_csr, int32_t* plan_info,
+                      unsigned long long* level_counts, void* stream);
+
+/*
+ * Plan from an explicit mask (int8 or int64 [units, n_k], units = batch*hq*n_q), used by the
+ * psa_streaming drop-in (pkg/src/pyrattn/attention.py:171-218) when the caller supplies M.
+ * Entries outside 0..levels, or pooled levels on causally straddling pairs, set *bad_flag.
+ */
+int psa_mask_to_plan(const void* mask, int mask_is_int64, int64_t units, int n_q, int n_k,
+                     int causal, int b_q, int b_k, int levels, uint16_t* plan_csr,
+                     int32_t* plan_info, unsigned long long* level_counts, int32_t* bad_flag,
+                     void* stream);
+
+/*
+ * K4 — multi-level block-sparse attention forward (tcgen05/TMEM/TMA).  Replaces
+ * psa_streaming (pkg/src/pyrattn/attention.py:171-218), level_bias (attention.py:39-44) and
+ * the decoupled block-tile executor execute_schedule (pkg/src/pyrattn/scheduler.py:203-269).
+ * q: bf16 [batch, hq, n, d]; k, v: bf16 [batch, hkv, n, d]; k_pyr/v_pyr: as produced by
+ * psa_pyramid_build. Constraints of the sm_100a kernel: d in {64,128}, b_q <= 128,
+ * b_k <= 128.
+ * out: bf16 [batch, hq, n, d]; lse: fp32 [batch, hq, n] (natural log; -inf for rows with no
+ * key); skipped_rows: device int32 counter (accumulated: caller zeroes it).
+ */
+int psa_attn_fwd(const void* q, const void* k, const void* v, const void* k_pyr,
+                 const void* v_pyr, int64_t batch, int hq, int hkv, int64_t n, int d, int b_q,
+                 int b_k, int levels, const uint16_t* plan_csr, const int32_t* plan_info,
+                 int causal, void* out, float* lse, int32_t* skipped_rows, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PSA_H_ */

@@ -1,0 +1,31 @@
+"""B200-native Pyramid Sparse Attention (PSA, arXiv 2512.04025) forward.
+
+Drop-in for the hot path of the reference package ``pyrattn`` (pkg/src/pyrattn/__init__.py):
+same entry-point names, argument meaning and error classes, but every tensor operation runs in
+hand-written sm_100a CUDA (libpsa.so, C ABI in include/psa.h) on torch CUDA tensors. There is
+no CPU fallback: calling with CPU tensors or without the built library raises.
+"""
+
+from .attention import (LN2, AttentionOutput, causal_full_attention, full_attention,
+                        level_bias, psa_streaming)
+from .errors import NumericError, TensorFileError, ValidationError
+from .importance import importance_sampled, sample_tables
+from .layout import (PRESET_CUTPOINTS, BlockLayout, LevelThresholds, QuantileCutpoints,
+                     SamplerConfig, SimThresholds, make_layout)
+from .mask import (MaskPlan, SparsityReport, assign_quantile, assign_threshold, binary_mask,
+                   causal_premask, combine_mask, report_from_counts, sparsity_report)
+from .pipeline import PSAResult, RunConfig, psa_attention, psa_forward_4d
+from .pyramid import PyramidKV, build_pyramid, level_cap_from_similarity
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "AttentionOutput", "BlockLayout", "LN2", "LevelThresholds", "MaskPlan", "NumericError",
+    "PRESET_CUTPOINTS", "PSAResult", "PyramidKV", "QuantileCutpoints", "RunConfig",
+    "SamplerConfig", "SimThresholds", "SparsityReport", "TensorFileError", "ValidationError",
+    "assign_quantile", "assign_threshold", "binary_mask", "build_pyramid",
+    "causal_full_attention", "causal_premask", "combine_mask", "full_attention",
+    "importance_sampled", "level_bias", "level_cap_from_similarity", "make_layout",
+    "psa_attention", "psa_forward_4d", "psa_streaming", "report_from_counts", "sample_tables",
+    "sparsity_report",
+]

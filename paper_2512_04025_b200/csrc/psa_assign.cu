@@ -1,0 +1,357 @@
+// K3: multi-level mask assignment + compact per-query-block plan.
+//
+// Reference semantics (pkg/src/pyrattn/mask.py):
+//   _descending_order      :272-274  stable argsort of -s (ties -> ascending block index)
+//   _compensated_cumsum    :277-290  sequential Neumaier, out[i] = total + comp
+//   assign_threshold       :293-316  row/fsum(row) (uniform 1/n_k if the total is 0), clip 1.0,
+//                                    searchsorted(taus, cum, 'left') -> level t+1, 0 past tau_H
+//   binary_mask            :319-323  threshold with a single tau
+//   assign_quantile        :332-344  rank levels via searchsorted(counts, rank, 'right')
+//   combine_mask           :402-412  min(M, caps[j])
+//   causal_premask         :489-514  future -> 0, straddling -> 1, visible -> keep
+//
+// One CTA (128 threads) per (head, query block) row. The sort is a bitonic network in shared
+// memory; the row total is computed EXACTLY (a 256-bit fixed-point superaccumulator reduced
+// across a warp, then rounded half-to-even), which is what CPython's math.fsum returns; the
+// Neumaier recurrence is inherently sequential and runs on one thread with the same IEEE ops
+// in the same order, so identical scores give identical levels.
+#include "common.cuh"
+#include "psa_internal.h"
+
+namespace psa {
+
+struct AssignParams {
+  LevelRule rule;
+  int n_q, n_k, hq, hkv, b_q, b_k, levels, causal, n_pad;
+};
+
+PSA_DEV bool sorts_before(double ka, int ia, double kb, int ib) {
+  return ka > kb || (ka == kb && ia < ib);
+}
+
+// Bitonic sort of (key, idx) pairs in shared memory into "descending key, ascending idx".
+PSA_DEV void bitonic_sort_desc(double* keys, int* idx, int n_pad) {
+  for (int k = 2; k <= n_pad; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = threadIdx.x; t < (n_pad >> 1); t += blockDim.x) {
+        const int i = 2 * j * (t / j) + (t % j);
+        const int l = i + j;
+        const double ki = keys[i], kl = keys[l];
+        const int ii = idx[i], il = idx[l];
+        const bool asc = (i & k) == 0;  // this run must end up in "sorts_before" order
+        const bool sw = asc ? sorts_before(kl, il, ki, ii) : sorts_before(ki, ii, kl, il);
+        if (sw) {
+          keys[i] = kl;
+          keys[l] = ki;
+          idx[i] = il;
+          idx[l] = ii;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Extract `cnt` (<= 53) bits starting at bit `lo` of a 256-bit little-endian limb array.
+PSA_DEV uint64_t bits256(const uint32_t (&w)[8], int lo, int cnt) {
+  uint64_t r = 0;
+  for (int b = 0; b < cnt; ++b) {
+    const int pos = lo + b;
+    if (pos >= 0 && pos < 256) r |= static_cast<uint64_t>((w[pos >> 5] >> (pos & 31)) & 1u) << b;
+  }
+  return r;
+}
+
+// Correctly rounded (half-to-even) sum of n non-negative finite doubles, sorted descending
+// (v[0] is the maximum). Executed by one full warp; the result is returned on every lane.
+// Equivalent to CPython math.fsum for this input class.
+PSA_DEV double exact_sum_sorted_nonneg(const double* v, int n) {
+  const int lane = threadIdx.x & 31;
+  const double vmax = v[0];
+  if (!(vmax > 0.0)) return 0.0;
+  const int emax = ilogb(vmax);
+  const int lsb = emax - 243;  // window bit 0 weight 2^lsb; sum < 2^(emax+13) <= 2^(lsb+256)
+  uint64_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  bool sticky = false;
+  for (int i = lane; i < n; i += 32) {
+    const uint64_t bits = __double_as_longlong(v[i]);
+    const int e = static_cast<int>((bits >> 52) & 0x7FF);
+    uint64_t m = bits & 0xFFFFFFFFFFFFFull;
+    if (e != 0) m |= 1ull << 52;
+    if (m == 0) continue;
+    int pos = (e != 0 ? e : 1) - 1075 - lsb;
+    if (pos < 0) {
+      const int sh = -pos;
+      if (sh >= 64) {
+        sticky = true;
+        continue;
+      }
+      if (m & ((1ull << sh) - 1ull)) sticky = true;
+      m >>= sh;
+      pos = 0;
+    }
+    const int li = pos >> 5, s = pos & 31;
+    const uint64_t lo = (m & 0xFFFFFFFFull) << s;
+    const uint64_t hi = (m >> 32) << s;
+    const uint64_t p0 = lo & 0xFFFFFFFFull;
+    const uint64_t p1 = (lo >> 32) + (hi & 0xFFFFFFFFull);
+    const uint64_t p2 = hi >> 32;
+#pragma unroll
+    for (int L = 0; L < 8; ++L)
+      acc[L] += (L == li) ? p0 : (L == li + 1) ? p1 : (L == li + 2) ? p2 : 0ull;
+  }
+#pragma unroll
+  for (int L = 0; L < 8; ++L)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[L] += __shfl_xor_sync(0xffffffffu, acc[L], o);
+  sticky = __any_sync(0xffffffffu, sticky);
+  uint32_t w[8];
+  uint64_t carry = 0;
+#pragma unroll
+  for (int L = 0; L < 8; ++L) {
+    const uint64_t t = acc[L] + carry;
+    w[L] = static_cast<uint32_t>(t);
+    carry = t >> 32;
+  }
+  int p = -1;
+  for (int L = 7; L >= 0 && p < 0; --L)
+    if (w[L]) p = L * 32 + 31 - __clz(w[L]);
+  int r = p - 52;
+  if (lsb + p < -1022) r = max(r, -1074 - lsb);  // subnormal result
+  uint64_t mant = bits256(w, r, p - r + 1);
+  const bool rbit = bits256(w, r - 1, 1) != 0;
+  bool st = sticky;
+  for (int b = 0; b < r - 1 && !st; ++b) st = ((w[b >> 5] >> (b & 31)) & 1u) != 0;
+  if (rbit && (st || (mant & 1ull))) mant += 1;
+  return ldexp(static_cast<double>(mant), lsb + r);
+}
+
+PSA_DEV int slot_rows(int pooled) {  // power-of-two slot >= 8 rows (TMA/UMMA atom alignment)
+  int s = 8;
+  while (s < pooled) s <<= 1;
+  return s;
+}
+
+// Level-major compaction of lvl[0..n_k) into the plan row; returns per-level counts in cnt.
+PSA_DEV void emit_plan_row(const int8_t* lvl, int n_k, int levels, int b_k, int64_t unit,
+                           uint16_t* __restrict__ csr, int32_t* __restrict__ info,
+                           unsigned long long* __restrict__ level_counts, int* warp_tot) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  int base = 0;
+  int64_t rows_total = 0;
+  for (int h = 1; h <= levels; ++h) {
+    const int start_h = base;
+    for (int j0 = 0; j0 < n_k; j0 += blockDim.x) {
+      const int j = j0 + threadIdx.x;
+      const bool f = j < n_k && lvl[j] == h;
+      const unsigned bal = __ballot_sync(0xffffffffu, f);
+      if (lane == 0) warp_tot[warp] = __popc(bal);
+      __syncthreads();
+      int off = base;
+      int tot = 0;
+      for (int w = 0; w < nwarps; ++w) {
+        if (w < warp) off += warp_tot[w];
+        tot += warp_tot[w];
+      }
+      if (f)
+        csr[unit * n_k + off + __popc(bal & ((1u << lane) - 1u))] =
+            static_cast<uint16_t>(j | (h << 12));
+      __syncthreads();
+      base += tot;
+    }
+    const int cnt = base - start_h;
+    if (threadIdx.x == 0) {
+      rows_total += static_cast<int64_t>(cnt) * slot_rows(b_k >> (h - 1));
+      if (level_counts && cnt) atomicAdd(level_counts + h, static_cast<unsigned long long>(cnt));
+    }
+  }
+  if (threadIdx.x == 0) {
+    info[unit * 2 + 0] = base;
+    info[unit * 2 + 1] = static_cast<int32_t>((rows_total + 127) / 128);
+    if (level_counts && n_k - base)
+      atomicAdd(level_counts, static_cast<unsigned long long>(n_k - base));
+  }
+}
+
+__global__ void __launch_bounds__(128) assign_levels_kernel(
+    const double* __restrict__ S, const int8_t* __restrict__ caps, AssignParams p,
+    int8_t* __restrict__ level_map, uint16_t* __restrict__ csr, int32_t* __restrict__ info,
+    unsigned long long* __restrict__ level_counts) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* keys = reinterpret_cast<double*>(smem_raw);
+  int* idx = reinterpret_cast<int*>(keys + p.n_pad);
+  int8_t* lsorted = reinterpret_cast<int8_t*>(idx + p.n_pad);
+  int8_t* lvl = lsorted + p.n_pad;
+  __shared__ double total_s;
+  __shared__ int warp_tot[4];
+
+  const int i = blockIdx.x;
+  const int64_t bhq = blockIdx.y;
+  const int64_t unit = bhq * p.n_q + i;
+  const double* row = S + unit * p.n_k;
+  for (int t = threadIdx.x; t < p.n_pad; t += blockDim.x) {
+    keys[t] = t < p.n_k ? row[t] : -1.0;  // scores are >= 0: pads sort last
+    idx[t] = t;
+  }
+  __syncthreads();
+  bitonic_sort_desc(keys, idx, p.n_pad);
+
+  if (p.rule.mode == 0) {
+    if (threadIdx.x < 32) {
+      const double tot = exact_sum_sorted_nonneg(keys, p.n_k);  // math.fsum(row)
+      if (threadIdx.x == 0) total_s = tot;
+    }
+    __syncthreads();
+    const double tot = total_s;
+    const double uni = 1.0 / static_cast<double>(p.n_k);
+    for (int t = threadIdx.x; t < p.n_k; t += blockDim.x)
+      keys[t] = tot > 0.0 ? __ddiv_rn(keys[t], tot) : uni;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double total = 0.0, comp = 0.0;
+      for (int t = 0; t < p.n_k; ++t) {
+        const double x = keys[t];
+        const double tt = __dadd_rn(total, x);
+        if (fabs(total) >= fabs(x))
+          comp = __dadd_rn(comp, __dadd_rn(__dsub_rn(total, tt), x));
+        else
+          comp = __dadd_rn(comp, __dadd_rn(__dsub_rn(x, tt), total));
+        total = tt;
+        const double cum = fmin(__dadd_rn(total, comp), 1.0);
+        int c = 0;
+        while (c < p.rule.n_cuts && p.rule.taus[c] < cum) ++c;  // searchsorted 'left'
+        lsorted[t] = static_cast<int8_t>(c < p.rule.n_cuts ? c + 1 : 0);
+      }
+    }
+  } else {
+    for (int t = threadIdx.x; t < p.n_k; t += blockDim.x) {
+      int c = 0;
+      while (c < p.rule.n_cuts && p.rule.counts[c] <= t) ++c;  // searchsorted 'right'
+      lsorted[t] = static_cast<int8_t>(c < p.rule.n_cuts ? c + 1 : 0);
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < p.n_k; t += blockDim.x) lvl[idx[t]] = lsorted[t];
+  __syncthreads();
+
+  const int b = static_cast<int>(bhq / p.hq), h = static_cast<int>(bhq % p.hq);
+  const int64_t bhkv = static_cast<int64_t>(b) * p.hkv + h / (p.hq / p.hkv);
+  const int64_t q_lo = static_cast<int64_t>(i) * p.b_q, q_hi = q_lo + p.b_q - 1;
+  for (int j = threadIdx.x; j < p.n_k; j += blockDim.x) {
+    int L = lvl[j];
+    if (caps) L = min(L, static_cast<int>(caps[bhkv * p.n_k + j]));
+    if (p.causal) {
+      const int64_t k_lo = static_cast<int64_t>(j) * p.b_k, k_hi = k_lo + p.b_k - 1;
+      if (k_lo > q_hi) L = 0;
+      else if (!(k_hi <= q_lo)) L = 1;
+    }
+    lvl[j] = static_cast<int8_t>(L);
+    level_map[unit * p.n_k + j] = static_cast<int8_t>(L);
+  }
+  __syncthreads();
+  emit_plan_row(lvl, p.n_k, p.levels, p.b_k, unit, csr, info, level_counts, warp_tot);
+}
+
+// Plan from a caller-supplied mask (psa_streaming drop-in). Validates like
+// attention.py:66-75 (_check_mask) and attention.py:88-108 (_causal_key_mask).
+template <typename T>
+__global__ void __launch_bounds__(128) mask_to_plan_kernel(
+    const T* __restrict__ mask, int n_q, int n_k, int causal, int b_q, int b_k, int levels,
+    uint16_t* __restrict__ csr, int32_t* __restrict__ info,
+    unsigned long long* __restrict__ level_counts, int32_t* __restrict__ bad) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  int8_t* lvl = reinterpret_cast<int8_t*>(smem_raw);
+  __shared__ int warp_tot[4];
+  const int64_t unit = blockIdx.x;
+  const int i = static_cast<int>(unit % n_q);
+  const int64_t q_lo = static_cast<int64_t>(i) * b_q;
+  for (int j = threadIdx.x; j < n_k; j += blockDim.x) {
+    const long long L = static_cast<long long>(mask[unit * n_k + j]);
+    int8_t v = 0;
+    if (L < 0 || L > levels) {
+      atomicOr(bad, 1);
+    } else {
+      v = static_cast<int8_t>(L);
+      if (causal && L > 1) {
+        const int64_t k_hi = static_cast<int64_t>(j + 1) * b_k - 1;
+        if (!(k_hi <= q_lo)) atomicOr(bad, 2);  // pooled level on a straddling pair
+      }
+    }
+    lvl[j] = v;
+  }
+  __syncthreads();
+  emit_plan_row(lvl, n_k, levels, b_k, unit, csr, info, level_counts, warp_tot);
+}
+
+}  // namespace psa
+
+using namespace psa;
+
+extern "C" int psa_assign_levels(const double* scores, int64_t batch, int hq, int hkv, int n_q,
+                                 int n_k, int mode, const double* taus, const int32_t* counts,
+                                 int n_cuts, const int8_t* caps, int causal, int b_q, int b_k,
+                                 int levels, int8_t* level_map, uint16_t* plan_csr,
+                                 int32_t* plan_info, unsigned long long* level_counts,
+                                 void* stream) {
+  PSA_CHECK_ARG(scores && level_map && plan_csr && plan_info, "null pointer argument");
+  PSA_CHECK_ARG(mode == 0 || mode == 1, "mode must be 0 (threshold) or 1 (quantile)");
+  PSA_CHECK_ARG(n_cuts >= 1 && n_cuts <= kMaxCuts, "need 1..16 thresholds/cutpoints");
+  PSA_CHECK_ARG(n_cuts <= levels, "more thresholds than pyramid levels");
+  PSA_CHECK_ARG(levels >= 1 && levels <= 15, "levels must lie in 1..15");
+  PSA_CHECK_ARG(n_k >= 1 && n_k <= 4096, "n_k must lie in 1..4096");
+  PSA_CHECK_ARG(n_q >= 1, "n_q must be positive");
+  PSA_CHECK_ARG(hq >= 1 && hkv >= 1 && hq % hkv == 0, "query heads must be a multiple of kv heads");
+  AssignParams p{};
+  p.rule.mode = mode;
+  p.rule.n_cuts = n_cuts;
+  for (int c = 0; c < n_cuts; ++c) {
+    if (mode == 0) {
+      PSA_CHECK_ARG(taus != nullptr, "threshold mode needs taus");
+      p.rule.taus[c] = taus[c];
+    } else {
+      PSA_CHECK_ARG(counts != nullptr, "quantile mode needs counts");
+      p.rule.counts[c] = counts[c];
+    }
+  }
+  p.n_q = n_q;
+  p.n_k = n_k;
+  p.hq = hq;
+  p.hkv = hkv;
+  p.b_q = b_q;
+  p.b_k = b_k;
+  p.levels = levels;
+  p.causal = causal;
+  int n_pad = 32;
+  while (n_pad < n_k) n_pad <<= 1;
+  p.n_pad = n_pad;
+  const size_t smem = static_cast<size_t>(n_pad) * (8 + 4 + 1) + n_k + 16;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(assign_levels_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+  dim3 grid(n_q, static_cast<unsigned>(batch * hq));
+  assign_levels_kernel<<<grid, 128, smem, static_cast<cudaStream_t>(stream)>>>(
+      scores, caps, p, level_map, plan_csr, plan_info, level_counts);
+  return psa_check_launch("assign_levels_kernel");
+}
+
+extern "C" int psa_mask_to_plan(const void* mask, int mask_is_int64, int64_t units, int n_q,
+                                int n_k, int causal, int b_q, int b_k, int levels,
+                                uint16_t* plan_csr, int32_t* plan_info,
+                                unsigned long long* level_counts, int32_t* bad_flag,
+                                void* stream) {
+  PSA_CHECK_ARG(mask && plan_csr && plan_info && bad_flag, "null pointer argument");
+  PSA_CHECK_ARG(n_k >= 1 && n_k <= 4096, "n_k must lie in 1..4096");
+  PSA_CHECK_ARG(levels >= 1 && levels <= 15, "levels must lie in 1..15");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t smem = static_cast<size_t>(n_k) + 16;
+  if (mask_is_int64)
+    mask_to_plan_kernel<long long><<<static_cast<unsigned>(units), 128, smem, s>>>(
+        static_cast<const long long*>(mask), n_q, n_k, causal, b_q, b_k, levels, plan_csr,
+        plan_info, level_counts, bad_flag);
+  else
+    mask_to_plan_kernel<int8_t><<<static_cast<unsigned>(units), 128, smem, s>>>(
+        static_cast<const int8_t*>(mask), n_q, n_k, causal, b_q, b_k, levels, plan_csr,
+        plan_info, level_counts, bad_flag);
+  return psa_check_launch("mask_to_plan_kernel");
+}

@@ -1,0 +1,469 @@
+// K4: multi-level block-sparse attention forward on sm_100a (tcgen05 + TMEM + TMA).
+//
+// Reference semantics:
+//   psa_streaming        pkg/src/pyrattn/attention.py:171-218  (online softmax over the selected
+//                        (j, h) pairs; logits q.k*scale + (h-1)*ln2; empty rows -> 0, lse -inf)
+//   level_bias           pkg/src/pyrattn/attention.py:39-44
+//   _causal_key_mask     pkg/src/pyrattn/attention.py:88-108 (k_pos <= q_pos on straddling pairs)
+//   execute_schedule     pkg/src/pyrattn/scheduler.py:203-269 (decoupled block tiles: pooled
+//                        segments of several KV blocks packed into one fixed-size tile)
+//
+// One CTA per (head, query block) work unit; 8 warps:
+//   warp 0  TMA producer: walks the unit's level-major plan and packs pooled segments into
+//           128-row KV tiles. Segment sizes are padded to power-of-two slots (>= 8 rows) and
+//           emitted largest-first, so every slot starts on a 1024-byte (8-row) swizzle atom and
+//           the packing is perfect except for the last tile. Per 8-column chunk it records
+//           (valid rows, level bias, causal flag, key position) for the softmax warps.
+//   warp 1  MMA issuer (one thread): S[sb] = Q K^T into TMEM (double-buffered), then
+//           O += P V with P from shared memory; commits signal the other roles.
+//   warp 2  TMEM allocator (512 columns: S0 | S1 | O).
+//   warps 4-7  softmax + epilogue, one thread per query row (TMEM lane). log2-domain online
+//           softmax with the level bias exactly (h-1) in log2 units, lazy O rescaling
+//           (only when the running max grows by more than 2^8), P written as bf16 into a
+//           128B-swizzled K-major tile, final 1/l normalisation and lse.
+#include "common.cuh"
+#include "psa_internal.h"
+
+namespace psa {
+
+constexpr int kTileRows = 128;  // query rows per tile (MMA M) and KV rows per tile (MMA N)
+constexpr int kStages = 2;
+constexpr int kChunks = kTileRows / 8;
+constexpr int kAttnThreads = 256;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units
+
+struct AttnMaps {
+  CUtensorMap q;
+  CUtensorMap k[kMaxLevels];
+  CUtensorMap v[kMaxLevels];
+};
+
+struct AttnParams {
+  int64_t n;
+  int hq, hkv, b_q, b_k, levels, n_q, n_k, causal;
+  float scale_log2;
+  int rows_lvl[kMaxLevels];
+  int slot_lvl[kMaxLevels];
+  int64_t nh_lvl[kMaxLevels];
+};
+
+template <int D>
+struct AttnSmem {
+  alignas(1024) uint8_t q[kTileRows * D * 2];            // [D/64][128 rows][128 B]
+  alignas(1024) uint8_t p[kTileRows * kTileRows * 2];    // [2][128 rows][128 B]
+  alignas(1024) uint8_t k[kStages][kTileRows * D * 2];   // [D/64][128 rows][128 B]
+  alignas(1024) uint8_t v[kStages][kTileRows * D * 2];
+  uint32_t meta[kStages][kChunks];
+  uint64_t q_full, kv_full[kStages], kv_empty[kStages], s_full[2], s_free[2], p_full, o_done;
+  uint32_t tmem_base;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kAttnThreads, 1)
+    psa_attn_fwd_kernel(const __grid_constant__ AttnMaps maps, const AttnParams p,
+                        const uint16_t* __restrict__ csr, const int32_t* __restrict__ info,
+                        uint16_t* __restrict__ out, float* __restrict__ lse,
+                        int32_t* __restrict__ skipped) {
+  extern __shared__ unsigned char smem_raw[];
+  auto& sm = *reinterpret_cast<AttnSmem<D>*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t unit = blockIdx.x;
+  const int bhq = static_cast<int>(unit / p.n_q);
+  const int i = static_cast<int>(unit % p.n_q);
+  const int b = bhq / p.hq, hh = bhq % p.hq;
+  const int64_t bhkv = static_cast<int64_t>(b) * p.hkv + hh / (p.hq / p.hkv);
+  const int n_ent = info[unit * 2 + 0];
+  const int T = info[unit * 2 + 1];
+  const int64_t q_row0 = static_cast<int64_t>(bhq) * p.n + static_cast<int64_t>(i) * p.b_q;
+
+  // ---------------------------------------------------------------- setup
+  if (threadIdx.x == 0) {
+    mbar_init(&sm.q_full, 1);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&sm.kv_full[s], 1);
+      mbar_init(&sm.kv_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&sm.s_full[s], 1);
+      mbar_init(&sm.s_free[s], 128);
+    }
+    mbar_init(&sm.p_full, 4);
+    mbar_init(&sm.o_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&maps.q);
+    for (int h = 0; h < p.levels; ++h) {
+      tma_prefetch_desc(&maps.k[h]);
+      tma_prefetch_desc(&maps.v[h]);
+    }
+  }
+  if (warp == 2) {
+    tmem_alloc(&sm.tmem_base, 512);
+    tmem_relinquish();
+  }
+  {  // V tiles may be read past the last filled slot of a tile: keep them finite (zero)
+    uint4* vz = reinterpret_cast<uint4*>(&sm.v[0][0]);
+    const int nvec = kStages * kTileRows * D * 2 / 16;
+    for (int t = threadIdx.x; t < nvec; t += kAttnThreads) vz[t] = make_uint4(0, 0, 0, 0);
+    fence_proxy_async_smem();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp == 0) {
+    // ================================================================ TMA producer
+    if (lane == 0 && T > 0) {
+      mbar_arrive_expect_tx(&sm.q_full, kTileRows * D * 2);
+      for (int c = 0; c < D / 64; ++c)
+        tma_load_2d(&maps.q, &sm.q_full, sm.q + c * kTileRows * 128, c * 64,
+                    static_cast<int>(q_row0));
+      const uint16_t* plan = csr + unit * p.n_k;
+      const int64_t q_lo = static_cast<int64_t>(i) * p.b_q;
+      int e = 0;
+      for (int t = 0; t < T; ++t) {
+        const int st = t % kStages;
+        if (t >= kStages) mbar_wait(&sm.kv_empty[st], ((t / kStages) - 1) & 1);
+        int seg_h[kChunks], seg_row[kChunks], seg_off[kChunks];
+        int nseg = 0, off = 0;
+        uint32_t meta[kChunks];
+#pragma unroll
+        for (int c = 0; c < kChunks; ++c) meta[c] = 0;
+        while (e < n_ent) {
+          const uint32_t ent = plan[e];
+          const int j = static_cast<int>(ent & 0xFFFu), h = static_cast<int>(ent >> 12);
+          const int sz = p.slot_lvl[h - 1];
+          if (off + sz > kTileRows) break;
+          const int L = p.rows_lvl[h - 1];
+          const bool straddle =
+              p.causal && (static_cast<int64_t>(j + 1) * p.b_k - 1 > q_lo);
+          for (int c = off / 8; c < (off + sz) / 8; ++c) {
+            const int first = c * 8 - off;
+            const int nv = min(max(L - first, 0), 8);
+            const uint32_t kpos = static_cast<uint32_t>(j * p.b_k + first);
+            meta[c] = static_cast<uint32_t>(nv) | (static_cast<uint32_t>(h - 1) << 4) |
+                      ((straddle ? 1u : 0u) << 8) | (kpos << 9);
+          }
+          seg_h[nseg] = h;
+          seg_row[nseg] = static_cast<int>(bhkv * p.nh_lvl[h - 1] + static_cast<int64_t>(j) * L);
+          seg_off[nseg] = off;
+          ++nseg;
+          off += sz;
+          ++e;
+        }
+        for (int c = 0; c < kChunks; ++c) sm.meta[st][c] = meta[c];
+        mbar_arrive_expect_tx(&sm.kv_full[st], static_cast<uint32_t>(off) * D * 2 * 2);
+        for (int g = 0; g < nseg; ++g) {
+          const int h = seg_h[g];
+          for (int c = 0; c < D / 64; ++c) {
+            tma_load_2d(&maps.k[h - 1], &sm.kv_full[st],
+                        sm.k[st] + c * kTileRows * 128 + seg_off[g] * 128, c * 64, seg_row[g]);
+            tma_load_2d(&maps.v[h - 1], &sm.kv_full[st],
+                        sm.v[st] + c * kTileRows * 128 + seg_off[g] * 128, c * 64, seg_row[g]);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================================================================ MMA issuer
+    if (lane == 0 && T > 0) {
+      constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128, false, false);
+      constexpr uint32_t idesc_o = umma_idesc_bf16(128, D, false, true);
+      const uint32_t q_base = smem_u32(sm.q), p_base = smem_u32(sm.p);
+      auto issue_pv = [&](int u) {
+        const int st = u % kStages;
+        mbar_wait(&sm.p_full, u & 1);
+        tc_fence_after();
+        const uint32_t v_base = smem_u32(sm.v[st]);
+#pragma unroll
+        for (int kk = 0; kk < kTileRows / 16; ++kk) {
+          const uint64_t a = umma_desc_sw128(p_base + (kk >> 2) * kTileRows * 128 + (kk & 3) * 32, 16, 1024);
+          const uint64_t bdesc = umma_desc_sw128(v_base + kk * 16 * 128, kTileRows * 128, 1024);
+          mma_bf16_ss(tmem + 256, a, bdesc, idesc_o, (u > 0 || kk > 0) ? 1u : 0u);
+        }
+        mma_commit(&sm.kv_empty[st]);
+        mma_commit(&sm.o_done);
+      };
+      mbar_wait(&sm.q_full, 0);
+      tc_fence_after();
+      for (int t = 0; t < T; ++t) {
+        const int st = t % kStages, sb = t & 1;
+        mbar_wait(&sm.kv_full[st], (t / kStages) & 1);
+        if (t >= 2) mbar_wait(&sm.s_free[sb], ((t >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t k_base = smem_u32(sm.k[st]);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t koff = (kk >> 2) * kTileRows * 128 + (kk & 3) * 32;
+          const uint64_t a = umma_desc_sw128(q_base + koff, 16, 1024);
+          const uint64_t bdesc = umma_desc_sw128(k_base + koff, 16, 1024);
+          mma_bf16_ss(tmem + sb * 128, a, bdesc, idesc_s, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(&sm.s_full[sb]);
+        if (t >= 1) issue_pv(t - 1);
+      }
+      issue_pv(T - 1);
+    }
+  } else if (warp >= 4) {
+    // ================================================================ softmax + epilogue
+    const int wq = warp & 3;
+    const int row = wq * 32 + lane;
+    const uint32_t t_lane = tmem + (static_cast<uint32_t>(wq * 32) << 16);
+    const int qpos = i * p.b_q + row;
+    const float scale = p.scale_log2;
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int t = 0; t < T; ++t) {
+      const int st = t % kStages, sb = t & 1;
+      mbar_wait(&sm.s_full[sb], (t >> 1) & 1);
+      tc_fence_after();
+      uint32_t s[4][32];
+#pragma unroll
+      for (int c4 = 0; c4 < 4; ++c4) tmem_ld32(t_lane + sb * 128 + c4 * 32, s[c4]);
+#pragma unroll
+      for (int c4 = 0; c4 < 4; ++c4) tmem_ld_wait(s[c4]);
+      tc_fence_before();
+      mbar_arrive(&sm.s_free[sb]);
+
+      uint32_t mw[kChunks];
+#pragma unroll
+      for (int c = 0; c < kChunks; c += 4) {
+        const uint4 w4 = *reinterpret_cast<const uint4*>(&sm.meta[st][c]);
+        mw[c] = w4.x;
+        mw[c + 1] = w4.y;
+        mw[c + 2] = w4.z;
+        mw[c + 3] = w4.w;
+      }
+      int nvc[kChunks];
+      float mt = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < kChunks; ++c) {
+        const uint32_t w = mw[c];
+        int nv = static_cast<int>(w & 15u);
+        if ((w >> 8) & 1u) nv = min(nv, max(qpos - static_cast<int>(w >> 9) + 1, 0));
+        nvc[c] = nv;
+        float mx = -INFINITY;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float x = __uint_as_float(s[c >> 2][(c & 3) * 8 + e]);
+          mx = (e < nv) ? fmaxf(mx, x) : mx;
+        }
+        mt = fmaxf(mt, fmaf(mx, scale, static_cast<float>((w >> 4) & 15u)));
+      }
+      const float m_new = fmaxf(m_run, mt);
+      const bool resc = m_new > m_run + kRescaleThreshold;
+      float alpha = 1.f;
+      if (resc) {
+        alpha = ex2_approx(m_run - m_new);
+        m_run = m_new;
+      }
+      const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
+      float lsum = 0.f;
+      uint32_t pk[kChunks * 4];
+#pragma unroll
+      for (int c = 0; c < kChunks; ++c) {
+        const float off = static_cast<float>((mw[c] >> 4) & 15u) - m_use;
+        const int nv = nvc[c];
+#pragma unroll
+        for (int e = 0; e < 8; e += 2) {
+          const float x0 = __uint_as_float(s[c >> 2][(c & 3) * 8 + e]);
+          const float x1 = __uint_as_float(s[c >> 2][(c & 3) * 8 + e + 1]);
+          const float p0 = (e < nv) ? ex2_approx(fmaf(x0, scale, off)) : 0.f;
+          const float p1 = (e + 1 < nv) ? ex2_approx(fmaf(x1, scale, off)) : 0.f;
+          lsum += p0 + p1;
+          __nv_bfloat162 pb = __floats2bfloat162_rn(p0, p1);
+          pk[c * 4 + e / 2] = *reinterpret_cast<uint32_t*>(&pb);
+        }
+      }
+      l_run = l_run * alpha + lsum;
+
+      const bool need = (t > 0) && __any_sync(0xffffffffu, resc);
+      if (t > 0) mbar_wait(&sm.o_done, (t - 1) & 1);  // PV(t-1) done: P tile free, O stable
+      if (need) {
+        tc_fence_after();
+#pragma unroll
+        for (int c4 = 0; c4 < D / 32; ++c4) {
+          uint32_t o[32];
+          tmem_ld32(t_lane + 256 + c4 * 32, o);
+          tmem_ld_wait(o);
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+          tmem_st32(t_lane + 256 + c4 * 32, o);
+        }
+        tmem_st_wait();
+      }
+      uint8_t* prow = sm.p + row * 128;
+#pragma unroll
+      for (int cc = 0; cc < 16; ++cc) {
+        const int half = cc >> 3, within = cc & 7;
+        uint8_t* dst = prow + half * kTileRows * 128 + ((within ^ (row & 7)) << 4);
+        *reinterpret_cast<uint4*>(dst) =
+            make_uint4(pk[cc * 4], pk[cc * 4 + 1], pk[cc * 4 + 2], pk[cc * 4 + 3]);
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.p_full);
+    }
+
+    // ---------------------------------------------------------------- epilogue
+    if (T > 0) {
+      mbar_wait(&sm.o_done, (T - 1) & 1);
+      tc_fence_after();
+    }
+    const bool valid = row < p.b_q;
+    const bool alive = l_run > 0.f;
+    const float inv = alive ? 1.f / l_run : 0.f;
+    uint16_t* orow = out + (q_row0 + row) * D;
+#pragma unroll
+    for (int c4 = 0; c4 < D / 32; ++c4) {
+      uint32_t o[32];
+      if (T > 0) {
+        tmem_ld32(t_lane + 256 + c4 * 32, o);
+        tmem_ld_wait(o);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) o[e] = 0u;
+      }
+      uint32_t pkd[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        __nv_bfloat162 v2 = __floats2bfloat162_rn(__uint_as_float(o[2 * e]) * inv,
+                                                  __uint_as_float(o[2 * e + 1]) * inv);
+        pkd[e] = *reinterpret_cast<uint32_t*>(&v2);
+      }
+      if (valid) {
+#pragma unroll
+        for (int v4 = 0; v4 < 4; ++v4)
+          *reinterpret_cast<uint4*>(orow + c4 * 32 + v4 * 8) =
+              make_uint4(pkd[v4 * 4], pkd[v4 * 4 + 1], pkd[v4 * 4 + 2], pkd[v4 * 4 + 3]);
+      }
+    }
+    if (valid)
+      lse[q_row0 + row] = alive ? (m_run + log2f(l_run)) * 0.69314718055994530942f : -INFINITY;
+    const unsigned dead = __ballot_sync(0xffffffffu, valid && !alive);
+    if (lane == 0 && dead) atomicAdd(skipped, __popc(dead));
+  }
+
+  // ---------------------------------------------------------------- teardown
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (fn == nullptr) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  }
+  return fn;
+}
+
+// 2D bf16 [rows, cols] row-major, box = [box_rows, 64 cols], 128-byte swizzle.
+static int encode_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols,
+                     uint32_t box_rows) {
+  EncodeTiledFn fn = get_encode_fn();
+  if (fn == nullptr) return psa_fail(PSA_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return psa_fail(PSA_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return PSA_OK;
+}
+
+template <int D>
+static int launch_attn(const void* q, const void* k, const void* v, const void* k_pyr,
+                       const void* v_pyr, int64_t batch, int hq, int hkv, int64_t n, int b_q,
+                       int b_k, int levels, const uint16_t* csr, const int32_t* info, int causal,
+                       void* out, float* lse, int32_t* skipped, cudaStream_t s) {
+  AttnMaps maps;
+  memset(&maps, 0, sizeof(maps));
+  AttnParams p{};
+  p.n = n;
+  p.hq = hq;
+  p.hkv = hkv;
+  p.b_q = b_q;
+  p.b_k = b_k;
+  p.levels = levels;
+  p.n_q = static_cast<int>(n / b_q);
+  p.n_k = static_cast<int>(n / b_k);
+  p.causal = causal;
+  p.scale_log2 = static_cast<float>(1.4426950408889634 / sqrt(static_cast<double>(D)));
+  const int64_t bhkv = batch * hkv;
+  int rc = encode_2d(&maps.q, q, static_cast<uint64_t>(batch * hq * n), D, kTileRows);
+  if (rc) return rc;
+  int64_t off_elems = 0;
+  for (int h = 1; h <= levels; ++h) {
+    const int L = b_k >> (h - 1);
+    int sz = 8;
+    while (sz < L) sz <<= 1;
+    p.rows_lvl[h - 1] = L;
+    p.slot_lvl[h - 1] = sz;
+    p.nh_lvl[h - 1] = n >> (h - 1);
+    const uint64_t rows = static_cast<uint64_t>(bhkv * (n >> (h - 1)));
+    const void* kb = h == 1 ? k : static_cast<const void*>(static_cast<const uint16_t*>(k_pyr) + off_elems);
+    const void* vb = h == 1 ? v : static_cast<const void*>(static_cast<const uint16_t*>(v_pyr) + off_elems);
+    if (h > 1) off_elems += static_cast<int64_t>(rows) * D;
+    rc = encode_2d(&maps.k[h - 1], kb, rows, D, sz);
+    if (rc) return rc;
+    rc = encode_2d(&maps.v[h - 1], vb, rows, D, sz);
+    if (rc) return rc;
+  }
+  const size_t smem = sizeof(AttnSmem<D>) + 1024;
+  cudaFuncSetAttribute(psa_attn_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(smem));
+  const int64_t units = batch * hq * p.n_q;
+  psa_attn_fwd_kernel<D><<<static_cast<unsigned>(units), kAttnThreads, smem, s>>>(
+      maps, p, csr, info, static_cast<uint16_t*>(out), lse, skipped);
+  return psa_check_launch("psa_attn_fwd_kernel");
+}
+
+}  // namespace psa
+
+using namespace psa;
+
+extern "C" int psa_attn_fwd(const void* q, const void* k, const void* v, const void* k_pyr,
+                            const void* v_pyr, int64_t batch, int hq, int hkv, int64_t n, int d,
+                            int b_q, int b_k, int levels, const uint16_t* plan_csr,
+                            const int32_t* plan_info, int causal, void* out, float* lse,
+                            int32_t* skipped_rows, void* stream) {
+  PSA_CHECK_ARG(q && k && v && plan_csr && plan_info && out && lse && skipped_rows,
+                "null pointer argument");
+  PSA_CHECK_ARG(d == 64 || d == 128, "head_dim must be 64 or 128 for the sm_100a path");
+  PSA_CHECK_ARG(b_q >= 1 && b_q <= kTileRows, "q_block must lie in 1..128 for the sm_100a kernel");
+  PSA_CHECK_ARG(b_k >= 1 && b_k <= kTileRows, "k_block must lie in 1..128 for the sm_100a kernel");
+  PSA_CHECK_ARG(n % b_q == 0 && n % b_k == 0, "layout does not divide seq_len");
+  PSA_CHECK_ARG(levels >= 1 && levels <= kMaxLevels, "levels must lie in 1..8");
+  PSA_CHECK_ARG(levels == 1 || (k_pyr && v_pyr), "pyramid pointers required for levels > 1");
+  PSA_CHECK_ARG(hq >= 1 && hkv >= 1 && hq % hkv == 0, "query heads must be a multiple of kv heads");
+  PSA_CHECK_ARG(n / b_k <= 4096, "n_k must be <= 4096");
+  PSA_CHECK_ARG(batch * hq * n < (int64_t(1) << 31), "too many rows for 32-bit TMA coordinates");
+  PSA_CHECK_ARG(n < (int64_t(1) << 23), "seq_len must be < 2^23");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (d == 128)
+    return launch_attn<128>(q, k, v, k_pyr, v_pyr, batch, hq, hkv, n, b_q, b_k, levels, plan_csr,
+                            plan_info, causal, out, lse, skipped_rows, s);
+  return launch_attn<64>(q, k, v, k_pyr, v_pyr, batch, hq, hkv, n, b_q, b_k, levels, plan_csr,
+                         plan_info, causal, out, lse, skipped_rows, s);
+}

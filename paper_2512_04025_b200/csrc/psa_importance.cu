@@ -1,0 +1,295 @@
+// K2: sampled block importance (pkg/src/pyrattn/importance.py:52-85).
+//
+// Reference: q_s = Q[q_rows], k_s = K[k_rows] (rows drawn by one seeded generator,
+// importance.py:68-79); probs = row_softmax(q_s @ k_s.T / sqrt(d)) over ALL n_k*s_k sampled
+// keys (importance.py:80, linalg.py:38-43); S = max (or mean) over each s_q x s_k block.
+//
+// GPU formulation (no n_q*s_q x n_k*s_k probability matrix is ever materialised):
+//   pass A (this file, stats kernel): per sampled query row a, stream the sampled keys in
+//     chunks of whole KV blocks; logits X = dot(q_a, k_b) / sqrt(d) in fp64 on the DMMA pipe
+//     (products and sums of bf16 values are exact in fp64, so the summation order is free);
+//     keep the per-(a, block) max logit M_aj plus an online (max, sum-exp) pair (m_a, l_a).
+//   pass B (finalize kernel): S_ij = max_{a in block i} exp(M_aj - m_a) / l_a. Because exp
+//     and the division are monotone, this equals the reference's max over the block of the
+//     individually normalised probabilities (same subtraction, exp and division per element).
+//   The mean reducer re-runs pass A with the final (m_a, l_a) and accumulates block sums of
+//   exp(x - m_a) / l_a.
+#include "common.cuh"
+#include "psa_internal.h"
+
+namespace psa {
+
+constexpr int kImpRows = 64;   // sampled query rows per CTA
+constexpr int kImpCols = 64;   // sampled key rows per chunk (upper bound)
+constexpr int kImpThreads = 256;
+
+PSA_DEV void dmma_m8n8k4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int D>
+struct ImpSmem {
+  static constexpr int kLd = D + 4;  // padded fp64 row (bank spread for fragment loads)
+  double qs[kImpRows * kLd];
+  double ks[kImpCols * kLd];
+  double x[kImpRows * (kImpCols + 1)];
+};
+
+// Load `count` gathered bf16 rows of length D into registers (16 B per vector).
+template <int D>
+PSA_DEV void gather_rows_regs(const uint16_t* __restrict__ base, const int32_t* __restrict__ rows,
+                              int first, int count, uint4 (&buf)[kImpCols * D / 8 / kImpThreads]) {
+  constexpr int kVecPerRow = D / 8;
+  constexpr int kPer = kImpCols * D / 8 / kImpThreads;
+#pragma unroll
+  for (int p = 0; p < kPer; ++p) {
+    const int idx = threadIdx.x + p * kImpThreads;
+    const int r = idx / kVecPerRow, c = idx % kVecPerRow;
+    if (r < count) {
+      const int64_t row = rows[first + r];
+      buf[p] = __ldg(reinterpret_cast<const uint4*>(base + row * D) + c);
+    } else {
+      buf[p] = make_uint4(0, 0, 0, 0);
+    }
+  }
+}
+
+template <int D>
+PSA_DEV void store_rows_f64(double* dst, const uint4 (&buf)[kImpCols * D / 8 / kImpThreads]) {
+  constexpr int kVecPerRow = D / 8;
+  constexpr int kPer = kImpCols * D / 8 / kImpThreads;
+  constexpr int kLd = D + 4;
+#pragma unroll
+  for (int p = 0; p < kPer; ++p) {
+    const int idx = threadIdx.x + p * kImpThreads;
+    const int r = idx / kVecPerRow, c = idx % kVecPerRow;
+    const uint32_t w[4] = {buf[p].x, buf[p].y, buf[p].z, buf[p].w};
+    double* o = dst + r * kLd + c * 8;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      o[2 * e] = bf16_bits_to_dbl(static_cast<uint16_t>(w[e] & 0xFFFFu));
+      o[2 * e + 1] = bf16_bits_to_dbl(static_cast<uint16_t>(w[e] >> 16));
+    }
+  }
+}
+
+template <int D, bool MEAN>
+__global__ void __launch_bounds__(kImpThreads, 1)
+    importance_stats_kernel(const uint16_t* __restrict__ q, const uint16_t* __restrict__ k,
+                            int hq, int hkv, int64_t n, const int32_t* __restrict__ q_rows,
+                            const int32_t* __restrict__ k_rows, int R, int s_k, int n_k,
+                            double sqrt_d, double* __restrict__ M, double* __restrict__ mstat,
+                            double* __restrict__ lstat) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  auto& sm = *reinterpret_cast<ImpSmem<D>*>(smem_raw);
+  constexpr int kLd = ImpSmem<D>::kLd;
+  constexpr int kXld = kImpCols + 1;
+  constexpr int kPer = kImpCols * D / 8 / kImpThreads;
+
+  const int bhq = blockIdx.y;
+  const int b = bhq / hq, h = bhq % hq;
+  const int hk = h / (hq / hkv);
+  const uint16_t* qh = q + static_cast<int64_t>(bhq) * n * D;
+  const uint16_t* kh = k + (static_cast<int64_t>(b) * hkv + hk) * n * D;
+  const int a0 = blockIdx.x * kImpRows;
+  const int rows_here = min(kImpRows, R - a0);
+
+  // sampled query rows -> fp64 smem (reuse the chunk register buffer for the gather)
+  {
+    uint4 buf[kPer];
+    gather_rows_regs<D>(qh, q_rows, a0, rows_here, buf);
+    store_rows_f64<D>(sm.qs, buf);
+  }
+
+  const int blocks_per_chunk = kImpCols / s_k;  // s_k <= 64 checked on the host
+  const int cw = blocks_per_chunk * s_k;
+  const int C = n_k * s_k;
+  const int n_chunks = (C + cw - 1) / cw;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wr = warp >> 2, wc = warp & 3;  // 2 x 4 warp grid over the 64 x 64 logit tile
+  const int a_loc = threadIdx.x >> 2, quad = threadIdx.x & 3;
+  const int a_glob = a0 + a_loc;
+  const bool row_ok = a_loc < rows_here;
+
+  double m_run = -INFINITY, l_run = 0.0;
+  double m_fin = 0.0, l_fin = 1.0;
+  if (MEAN && row_ok) {
+    m_fin = mstat[static_cast<int64_t>(bhq) * R + a_glob];
+    l_fin = lstat[static_cast<int64_t>(bhq) * R + a_glob];
+  }
+
+  uint4 pref[kPer];
+  gather_rows_regs<D>(kh, k_rows, 0, min(cw, C), pref);
+
+  for (int ch = 0; ch < n_chunks; ++ch) {
+    const int b0 = ch * cw;
+    const int cols = min(cw, C - b0);
+    __syncthreads();  // previous chunk's X/K consumers are done
+    store_rows_f64<D>(sm.ks, pref);
+    if (ch + 1 < n_chunks) gather_rows_regs<D>(kh, k_rows, b0 + cw, min(cw, C - b0 - cw), pref);
+    __syncthreads();
+
+    // ---- 64 x 64 fp64 logit tile on the DMMA pipe: warp tile 32 x 16 (4 x 2 m8n8 tiles)
+    double acc[4][2][2];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+    const double* qa = sm.qs + (wr * 32 + (lane >> 2)) * kLd + (lane & 3);
+    const double* kb = sm.ks + (wc * 16 + (lane >> 2)) * kLd + (lane & 3);
+#pragma unroll 4
+    for (int k4 = 0; k4 < D / 4; ++k4) {
+      double af[4], bf[2];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) af[mt] = qa[mt * 8 * kLd + k4 * 4];
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) bf[nt] = kb[nt * 8 * kLd + k4 * 4];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) dmma_m8n8k4(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
+    }
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = wr * 32 + mt * 8 + (lane >> 2);
+          const int c = wc * 16 + nt * 8 + (lane & 3) * 2 + e;
+          sm.x[r * kXld + c] = __ddiv_rn(acc[mt][nt][e], sqrt_d);  // importance.py:80
+        }
+    __syncthreads();
+
+    // ---- per-row statistics; 4 threads per row, blocks interleaved over the quad
+    const double* xr = sm.x + a_loc * kXld;
+    const int nb = cols / s_k;
+    const int j0 = b0 / s_k;
+    if (!MEAN) {
+      double lmax = -INFINITY;
+      for (int bb = quad; bb < nb; bb += 4) {
+        double bm = -INFINITY;
+        for (int t = 0; t < s_k; ++t) bm = fmax(bm, xr[bb * s_k + t]);
+        lmax = fmax(lmax, bm);
+        if (row_ok) M[(static_cast<int64_t>(bhq) * R + a_glob) * n_k + j0 + bb] = bm;
+      }
+      lmax = fmax(lmax, __shfl_xor_sync(0xffffffffu, lmax, 1));
+      lmax = fmax(lmax, __shfl_xor_sync(0xffffffffu, lmax, 2));
+      const double m_new = fmax(m_run, lmax);
+      double part = 0.0;
+      for (int bb = quad; bb < nb; bb += 4)
+        for (int t = 0; t < s_k; ++t) part = __dadd_rn(part, exp(__dsub_rn(xr[bb * s_k + t], m_new)));
+      part = __dadd_rn(part, __shfl_xor_sync(0xffffffffu, part, 1));
+      part = __dadd_rn(part, __shfl_xor_sync(0xffffffffu, part, 2));
+      l_run = __dadd_rn(__dmul_rn(l_run, exp(__dsub_rn(m_run, m_new))), part);
+      m_run = m_new;
+    } else {
+      for (int bb = quad; bb < nb; bb += 4) {
+        double s = 0.0;
+        for (int t = 0; t < s_k; ++t)
+          s = __dadd_rn(s, __ddiv_rn(exp(__dsub_rn(xr[bb * s_k + t], m_fin)), l_fin));
+        if (row_ok) M[(static_cast<int64_t>(bhq) * R + a_glob) * n_k + j0 + bb] = s;
+      }
+    }
+  }
+  if (!MEAN && row_ok && quad == 0) {
+    mstat[static_cast<int64_t>(bhq) * R + a_glob] = m_run;
+    lstat[static_cast<int64_t>(bhq) * R + a_glob] = l_run;
+  }
+}
+
+// S_ij = max_a exp(M_aj - m_a) / l_a   (or mean: sum_a M_aj / (s_q*s_k))
+template <bool MEAN>
+__global__ void __launch_bounds__(128) importance_finalize_kernel(
+    const double* __restrict__ M, const double* __restrict__ mstat,
+    const double* __restrict__ lstat, int R, int s_q, int s_k, int n_q, int n_k,
+    double* __restrict__ S) {
+  const int i = blockIdx.x;
+  const int64_t bhq = blockIdx.y;
+  for (int j = threadIdx.x; j < n_k; j += blockDim.x) {
+    double acc = MEAN ? 0.0 : -INFINITY;
+    for (int t = 0; t < s_q; ++t) {
+      const int64_t a = bhq * R + static_cast<int64_t>(i) * s_q + t;
+      const double mv = M[a * n_k + j];
+      if (MEAN) {
+        acc = __dadd_rn(acc, mv);
+      } else {
+        const double p = __ddiv_rn(exp(__dsub_rn(mv, mstat[a])), lstat[a]);
+        acc = fmax(acc, p);
+      }
+    }
+    if (MEAN) acc = __ddiv_rn(acc, static_cast<double>(s_q) * static_cast<double>(s_k));
+    S[(bhq * n_q + i) * n_k + j] = acc;
+  }
+}
+
+}  // namespace psa
+
+using namespace psa;
+
+extern "C" size_t psa_importance_workspace_bytes(int64_t bhq, int n_q, int s_q, int n_k) {
+  const int64_t R = static_cast<int64_t>(n_q) * s_q;
+  return static_cast<size_t>(bhq * R * n_k + 2 * bhq * R) * sizeof(double);
+}
+
+template <int D>
+static int launch_importance(const void* q, const void* k, int64_t batch, int hq, int hkv,
+                             int64_t n, const int32_t* q_rows, const int32_t* k_rows, int R,
+                             int s_q, int s_k, int n_q, int n_k, int reducer, double* scores,
+                             void* ws, cudaStream_t s) {
+  const int64_t bhq = batch * hq;
+  double* M = static_cast<double*>(ws);
+  double* mstat = M + bhq * R * n_k;
+  double* lstat = mstat + bhq * R;
+  const size_t smem = sizeof(ImpSmem<D>);
+  cudaFuncSetAttribute(importance_stats_kernel<D, false>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  cudaFuncSetAttribute(importance_stats_kernel<D, true>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  dim3 grid((R + kImpRows - 1) / kImpRows, static_cast<unsigned>(bhq));
+  const double sqrt_d = sqrt(static_cast<double>(D));
+  auto* qq = static_cast<const uint16_t*>(q);
+  auto* kk = static_cast<const uint16_t*>(k);
+  importance_stats_kernel<D, false><<<grid, kImpThreads, smem, s>>>(
+      qq, kk, hq, hkv, n, q_rows, k_rows, R, s_k, n_k, sqrt_d, M, mstat, lstat);
+  int rc = psa_check_launch("importance_stats_kernel");
+  if (rc) return rc;
+  if (reducer == 1) {
+    importance_stats_kernel<D, true><<<grid, kImpThreads, smem, s>>>(
+        qq, kk, hq, hkv, n, q_rows, k_rows, R, s_k, n_k, sqrt_d, M, mstat, lstat);
+    rc = psa_check_launch("importance_stats_kernel<mean>");
+    if (rc) return rc;
+    importance_finalize_kernel<true><<<dim3(n_q, bhq), 128, 0, s>>>(M, mstat, lstat, R, s_q, s_k,
+                                                                     n_q, n_k, scores);
+  } else {
+    importance_finalize_kernel<false><<<dim3(n_q, bhq), 128, 0, s>>>(M, mstat, lstat, R, s_q,
+                                                                      s_k, n_q, n_k, scores);
+  }
+  return psa_check_launch("importance_finalize_kernel");
+}
+
+extern "C" int psa_importance_sampled(const void* q, const void* k, int64_t batch, int hq,
+                                      int hkv, int64_t n, int d, int b_q, int b_k,
+                                      const int32_t* q_rows, const int32_t* k_rows, int s_q,
+                                      int s_k, int reducer, double* scores, void* workspace,
+                                      void* stream) {
+  PSA_CHECK_ARG(q && k && q_rows && k_rows && scores && workspace, "null pointer argument");
+  PSA_CHECK_ARG(d == 64 || d == 128, "head_dim must be 64 or 128 for the sm_100a path");
+  PSA_CHECK_ARG(hq >= 1 && hkv >= 1 && hq % hkv == 0, "query heads must be a multiple of kv heads");
+  PSA_CHECK_ARG(b_q >= 1 && b_k >= 1 && n % b_q == 0 && n % b_k == 0, "layout does not divide seq_len");
+  PSA_CHECK_ARG(s_q >= 1 && s_q <= b_q, "s_q outside 1..q_block");
+  PSA_CHECK_ARG(s_k >= 1 && s_k <= b_k, "s_k outside 1..k_block");
+  PSA_CHECK_ARG(s_k <= kImpCols, "s_k > 64 is not supported by the sm_100a importance kernel");
+  PSA_CHECK_ARG(reducer == 0 || reducer == 1, "reducer must be 0 (max) or 1 (mean)");
+  const int n_q = static_cast<int>(n / b_q), n_k = static_cast<int>(n / b_k);
+  const int R = n_q * s_q;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (d == 128)
+    return launch_importance<128>(q, k, batch, hq, hkv, n, q_rows, k_rows, R, s_q, s_k, n_q, n_k,
+                                  reducer, scores, workspace, s);
+  return launch_importance<64>(q, k, batch, hq, hkv, n, q_rows, k_rows, R, s_q, s_k, n_q, n_k,
+                               reducer, scores, workspace, s);
+}

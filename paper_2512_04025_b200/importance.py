@@ -1,0 +1,83 @@
+"""Block-importance estimation (K2) on the GPU.
+
+Drop-in for importance_sampled (pkg/src/pyrattn/importance.py:52-85). The sampled row
+indices come from the same single seeded numpy generator in the same order as the reference
+(importance.py:68-76: every query block ascending, then every KV block ascending); they
+depend only on (seed, layout, s_q, s_k), are shared by all heads, and are cached on the
+device. All tensor arithmetic (fp64 logits, softmax statistics, block max) runs in libpsa.
+"""
+
+from __future__ import annotations
+
+import functools
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._tensors import as_bhnd, stream_handle
+from .errors import ValidationError
+from .layout import BlockLayout, SamplerConfig
+
+
+@functools.lru_cache(maxsize=64)
+def _sample_tables_host(seed: int, n_q: int, b_q: int, s_q: int, n_k: int, b_k: int, s_k: int):
+    rng = np.random.default_rng(seed)
+    q_rows = np.concatenate([i * b_q + rng.permutation(b_q)[:s_q] for i in range(n_q)])
+    k_rows = np.concatenate([j * b_k + rng.permutation(b_k)[:s_k] for j in range(n_k)])
+    return q_rows.astype(np.int32), k_rows.astype(np.int32)
+
+
+_device_tables: dict = {}
+
+
+def sample_tables(layout: BlockLayout, cfg: SamplerConfig, device) -> tuple:
+    """(q_rows, k_rows) int32 device tensors of sampled row indices inside a head."""
+    key = (cfg.seed, layout.n_q, layout.q_block, cfg.s_q, layout.n_k, layout.k_block, cfg.s_k,
+           str(device))
+    hit = _device_tables.get(key)
+    if hit is None:
+        qr, kr = _sample_tables_host(*key[:-1])
+        hit = (torch.from_numpy(qr).to(device), torch.from_numpy(kr).to(device))
+        _device_tables[key] = hit
+    return hit
+
+
+def importance_scores(q4: torch.Tensor, k4: torch.Tensor, layout: BlockLayout,
+                      cfg: SamplerConfig, reducer: str = "max") -> torch.Tensor:
+    """fp64 scores [B, Hq, n_q, n_k] from bf16 [B, H, N, d] device tensors."""
+    if reducer not in ("max", "mean"):
+        raise ValidationError(f"reducer must be 'max' or 'mean', got {reducer!r}")
+    cfg.validate(layout)
+    if cfg.s_k > 64:
+        raise ValidationError("s_k > 64 is not supported by the sm_100a importance kernel")
+    B, Hq, n, d = q4.shape
+    Hkv = k4.shape[1]
+    if Hq % Hkv:
+        raise ValidationError(f"query heads {Hq} not a multiple of kv heads {Hkv}")
+    dev = q4.device
+    q_rows, k_rows = sample_tables(layout, cfg, dev)
+    lib = _lib.load()
+    ws_bytes = lib.psa_importance_workspace_bytes(B * Hq, layout.n_q, cfg.s_q, layout.n_k)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    scores = torch.empty(B, Hq, layout.n_q, layout.n_k, dtype=torch.float64, device=dev)
+    rc = lib.psa_importance_sampled(q4.data_ptr(), k4.data_ptr(), B, Hq, Hkv, n, d,
+                                    layout.q_block, layout.k_block, q_rows.data_ptr(),
+                                    k_rows.data_ptr(), cfg.s_q, cfg.s_k,
+                                    0 if reducer == "max" else 1, scores.data_ptr(),
+                                    ws.data_ptr(), stream_handle(dev))
+    _lib.check(rc, "psa_importance_sampled")
+    return scores
+
+
+def importance_sampled(q, k, layout: BlockLayout, cfg: SamplerConfig,
+                       reducer: str = "max") -> torch.Tensor:
+    """Sampled-token importance scores (importance.py:52-85), float64.
+
+    Shape (n_q, n_k) for (n, d) inputs, else [..., n_q, n_k] following q's leading dims.
+    """
+    layout.check_gpu()
+    q4, lead = as_bhnd(q, "Q", layout.seq_len, layout.head_dim)
+    k4, _ = as_bhnd(k, "K", layout.seq_len, layout.head_dim)
+    s = importance_scores(q4, k4, layout, cfg, reducer)
+    return s.reshape(lead + (layout.n_q, layout.n_k))

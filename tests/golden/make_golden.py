@@ -1,0 +1,106 @@
+"""Generate the golden fixtures from the REAL reference implementation.
+
+Run in the build container (the reference is importable only here):
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+It imports `pyrattn` read-only, feeds it bf16-rounded seeded inputs, and stores inputs plus the
+reference's outputs as small .npz files next to this script. tests/test_oracle_golden.py (CPU)
+pins the oracle to these files; tests/test_gpu_golden.py (GPU) checks the kernels against them.
+Nothing at GPU-test time reads /root/reference.
+"""
+
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+HERE = Path(__file__).resolve().parent
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import pyrattn as ref  # noqa: E402
+
+
+def bf16(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(torch.bfloat16) \
+        .to(torch.float64).numpy()
+
+
+def bits(x):
+    """bf16 payload (uint16) of bf16-representable float64 values."""
+    return torch.from_numpy(np.ascontiguousarray(x)).to(torch.bfloat16).view(torch.int16) \
+        .numpy().view(np.uint16)
+
+
+def qkv(seed, n, d, kind="gaussian"):
+    if kind == "gaussian":
+        rng = np.random.default_rng(seed)
+        return [bf16(rng.standard_normal((n, d), dtype=np.float32)) for _ in range(3)]
+    g = 1 << ((n.bit_length() - 1) // 2)
+    data = ref.synthesize("correlated", n, d, seed, grid=(g, n // g))
+    return [bf16(data[x]) for x in ("q", "k", "v")]
+
+
+def case(name, n, d, bq, bk, H, *, seed, kind="gaussian", estimator="sampled-max", s_q=8,
+         s_k=8, mask="threshold", thresholds=None, cutpoints=None, tau=None, sim=None,
+         causal=False, stride=None, keep_pyramid=False):
+    q, k, v = qkv(seed, n, d, kind)
+    lay = ref.make_layout(n, d, bq, bk, H)
+    pyr = ref.build_pyramid(k, v, lay)
+    if estimator == "antidiagonal":
+        scores = ref.importance_antidiagonal(q, k, lay, stride)
+    else:
+        scores = ref.importance_sampled(q, k, lay, ref.SamplerConfig(s_q, s_k, 0),
+                                        reducer="max" if estimator == "sampled-max" else "mean")
+    if mask == "threshold":
+        m = ref.assign_threshold(scores, ref.LevelThresholds(thresholds))
+    elif mask == "binary":
+        m = ref.binary_mask(scores, tau)
+    else:
+        pts = ref.QuantileCutpoints(cutpoints) if mask == "quantile" else ref.PRESET_CUTPOINTS[mask]
+        m = ref.assign_quantile(scores, pts)
+    caps = None
+    if sim is not None:
+        caps = ref.level_cap_from_similarity(pyr, ref.SimThresholds(sim))
+        m = ref.combine_mask(m, caps)
+    if causal:
+        m = ref.causal_premask(m, lay)
+    att = ref.psa_streaming(q, pyr, m, causal=causal)
+    rep = ref.sparsity_report(m, levels=H)
+    levels_k = [np.concatenate([pyr.k(j, h) for j in range(lay.n_k)]) for h in range(1, H + 1)]
+    levels_v = [np.concatenate([pyr.v(j, h) for j in range(lay.n_k)]) for h in range(1, H + 1)]
+    payload = dict(
+        q=bits(q), k=bits(k), v=bits(v),
+        layout=np.array([n, d, bq, bk, H]), scores=scores, mask=m,
+        caps=caps if caps is not None else np.zeros(0, np.int64),
+        out=att.out, lse=att.row_log_normalizers, skipped=np.array(att.skipped_rows),
+        level_counts=np.array(rep.level_counts), rho_bar=np.array(rep.rho_bar),
+        kv_coverage=np.array(rep.kv_coverage),
+        config=np.array(repr(dict(estimator=estimator, s_q=s_q, s_k=s_k, seed=0, mask=mask,
+                                  thresholds=thresholds, cutpoints=cutpoints, tau=tau,
+                                  sim_thresholds=sim, causal=causal, stride=stride))),
+    )
+    for h in range(2, H + 1 if keep_pyramid else 2):
+        payload[f"k_level{h}"] = levels_k[h - 1]
+        payload[f"v_level{h}"] = levels_v[h - 1]
+    np.savez_compressed(HERE / f"{name}.npz", **payload)
+    print(name, "rho", rep.rho_bar, "skipped", att.skipped_rows)
+
+
+TAUS = (0.164713, 0.282366, 0.376488, 0.95)
+
+if __name__ == "__main__":
+    case("cfg1_small", 1024, 64, 64, 64, 4, seed=1, thresholds=TAUS, keep_pyramid=True)
+    case("wan_b120", 960, 128, 120, 120, 4, seed=2, thresholds=(0.1634, 0.2803, 0.3738, 0.95),
+         keep_pyramid=True)
+    case("quantile_psa3", 512, 128, 64, 64, 4, seed=3, mask="psa-3")
+    case("binary", 1024, 64, 64, 64, 1, seed=4, mask="binary", tau=0.6)
+    case("simcap_corr", 1024, 64, 64, 64, 4, seed=5, kind="correlated", thresholds=TAUS,
+         sim=(0.7, 0.65, 0.6))
+    case("causal", 512, 128, 64, 64, 4, seed=6, thresholds=TAUS, causal=True)
+    case("mean_reducer", 1024, 64, 64, 32, 3, seed=7, estimator="sampled-mean", s_q=5, s_k=7,
+         thresholds=(0.3, 0.6, 0.9))
+    case("antidiag", 1024, 64, 64, 64, 4, seed=8, estimator="antidiagonal", stride=8,
+         thresholds=TAUS)
+    case("dropped_rows", 512, 64, 64, 64, 2, seed=9, thresholds=(0.02, 0.05))
