@@ -62,7 +62,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
@@ -90,7 +90,7 @@ class ClockSampler:
         sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if "Active" in r[5 + i]})
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].strip() == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
                 "power_w_max": max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit())
@@ -133,7 +133,6 @@ def flops_from_counts(counts, cfg):
 def _cpu_worker(args):
     """Time the oracle port of the reference path on a bounded sample of one head."""
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
-    import numpy as np
     from oracle import psa_oracle as orc
     q, k, v, lay_t, taus, n_blocks, causal = args
     lay = orc.Layout(*lay_t)
@@ -144,14 +143,8 @@ def _cpu_worker(args):
     if causal:
         m = orc.causal_premask(m, lay)
     t1 = time.perf_counter()
-    # psa_streaming restricted to the first n_blocks query blocks (same per-block loop)
-    sub = orc.Layout(n_blocks * lay.q_block, lay.head_dim, lay.q_block, lay.k_block, lay.levels)
-    sub.n_k = lay.n_k
-    sub.seq_len = lay.seq_len
-    qs = np.zeros_like(q)
-    qs[: n_blocks * lay.q_block] = q[: n_blocks * lay.q_block]
-    mm = m[:n_blocks]
-    _stream_blocks(orc, q, kl, vl, mm, lay, n_blocks, causal)
+    # psa_streaming's per-query-block loop restricted to the first n_blocks query blocks
+    _stream_blocks(orc, q, kl, vl, m[:n_blocks], lay, n_blocks, causal)
     t2 = time.perf_counter()
     return t1 - t0, t2 - t1
 
@@ -210,10 +203,20 @@ def cpu_baseline(cfg, q_dev, k_dev, v_dev, flops_total, n_blocks=None, max_worke
                      v_dev[0, hk].to(torch.float64).cpu().numpy(), lay_t, cfg["taus"],
                      n_blocks, cfg["causal"]))
     ctx = mp.get_context("spawn")
-    t0 = time.perf_counter()
-    with ctx.Pool(workers) as pool:
-        res = pool.map(_cpu_worker, jobs)
-    wall = time.perf_counter() - t0
+    saved = {k_: os.environ.get(k_) for k_ in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS")}
+    for k_ in saved:  # children inherit: one BLAS thread per worker process
+        os.environ[k_] = "1"
+    try:
+        t0 = time.perf_counter()
+        with ctx.Pool(workers) as pool:
+            res = pool.map(_cpu_worker, jobs)
+        wall = time.perf_counter() - t0
+    finally:
+        for k_, v_ in saved.items():
+            if v_ is None:
+                os.environ.pop(k_, None)
+            else:
+                os.environ[k_] = v_
     pre = statistics.mean(r[0] for r in res)
     att = statistics.mean(r[1] for r in res)
     per_head = pre + att * (n_q / n_blocks)
@@ -267,11 +270,9 @@ def main():
 
     _lib.load()
     # strong scaling: the workload's query heads are split evenly; KV heads follow (GQA groups)
+    from paper_2512_04025_b200.parallel import shard_heads
     Hq, Hkv = cfg["Hq"], cfg["Hkv"]
-    group = Hq // Hkv
-    per = math.ceil(Hkv / world)
-    kv_heads = list(range(rank * per, min(Hkv, (rank + 1) * per)))
-    heads = [h for hk in kv_heads for h in range(hk * group, (hk + 1) * group)]
+    heads, kv_heads = shard_heads(Hq, Hkv, world, rank)
     if not heads:
         raise SystemExit("more ranks than kv heads")
     q, k, v = make_inputs(cfg, heads, kv_heads, device)

@@ -209,20 +209,26 @@ __global__ void __launch_bounds__(128) assign_levels_kernel(
       keys[t] = tot > 0.0 ? __ddiv_rn(keys[t], tot) : uni;
     __syncthreads();
     if (threadIdx.x == 0) {
+      // The recurrence is inherently sequential; keep only it on one thread and store
+      // cum_t in place of e_t (read just before it is overwritten).
       double total = 0.0, comp = 0.0;
+#pragma unroll 4
       for (int t = 0; t < p.n_k; ++t) {
         const double x = keys[t];
         const double tt = __dadd_rn(total, x);
-        if (fabs(total) >= fabs(x))
-          comp = __dadd_rn(comp, __dadd_rn(__dsub_rn(total, tt), x));
-        else
-          comp = __dadd_rn(comp, __dadd_rn(__dsub_rn(x, tt), total));
+        const double d = fabs(total) >= fabs(x) ? __dadd_rn(__dsub_rn(total, tt), x)
+                                                : __dadd_rn(__dsub_rn(x, tt), total);
+        comp = __dadd_rn(comp, d);
         total = tt;
-        const double cum = fmin(__dadd_rn(total, comp), 1.0);
-        int c = 0;
-        while (c < p.rule.n_cuts && p.rule.taus[c] < cum) ++c;  // searchsorted 'left'
-        lsorted[t] = static_cast<int8_t>(c < p.rule.n_cuts ? c + 1 : 0);
+        keys[t] = fmin(__dadd_rn(total, comp), 1.0);
       }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < p.n_k; t += blockDim.x) {
+      const double cum = keys[t];
+      int c = 0;
+      while (c < p.rule.n_cuts && p.rule.taus[c] < cum) ++c;  // searchsorted 'left'
+      lsorted[t] = static_cast<int8_t>(c < p.rule.n_cuts ? c + 1 : 0);
     }
   } else {
     for (int t = threadIdx.x; t < p.n_k; t += blockDim.x) {

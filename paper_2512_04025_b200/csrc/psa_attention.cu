@@ -8,29 +8,43 @@
 //   execute_schedule     pkg/src/pyrattn/scheduler.py:203-269 (decoupled block tiles: pooled
 //                        segments of several KV blocks packed into one fixed-size tile)
 //
-// One CTA per (head, query block) work unit; 8 warps:
+// One CTA per (head, query block) work unit; 12 warps:
 //   warp 0  TMA producer: walks the unit's level-major plan and packs pooled segments into
 //           128-row KV tiles. Segment sizes are padded to power-of-two slots (>= 8 rows) and
 //           emitted largest-first, so every slot starts on a 1024-byte (8-row) swizzle atom and
-//           the packing is perfect except for the last tile. Per 8-column chunk it records
-//           (valid rows, level bias, causal flag, key position) for the softmax warps.
+//           the packing is perfect except for the last tile. Per 8-column chunk it publishes
+//           (valid rows, level bias, causal flag, key position) through a 4-deep meta ring.
+//           K and V have separate rings (K: 3 stages, freed when S = QK^T completes;
+//           V: 2 stages, freed when O += PV completes).
 //   warp 1  MMA issuer (one thread): S[sb] = Q K^T into TMEM (double-buffered), then
 //           O += P V with P from shared memory; commits signal the other roles.
 //   warp 2  TMEM allocator (512 columns: S0 | S1 | O).
-//   warps 4-7  softmax + epilogue, one thread per query row (TMEM lane). log2-domain online
-//           softmax with the level bias exactly (h-1) in log2 units, lazy O rescaling
-//           (only when the running max grows by more than 2^8), P written as bf16 into a
-//           128B-swizzled K-major tile, final 1/l normalisation and lse.
+//   warps 4-11  softmax + epilogue: two warpgroups, one TMEM lane (query row) per thread;
+//           warpgroup g owns S columns [64g, 64g+64) and O columns [D/2 g, D/2 (g+1)), so every
+//           SM sub-partition runs two softmax warps. Per tile the two halves exchange their row
+//           max through shared memory (one named barrier). log2-domain online softmax with the
+//           level bias exactly (h-1) in log2 units, packed f32x2 FMA/ADD, lazy O rescaling (only
+//           when the running max grows by more than 2^8), P written as bf16 into a 128B-swizzled
+//           K-major tile, final 1/l normalisation and lse.
 #include "common.cuh"
 #include "psa_internal.h"
 
 namespace psa {
 
 constexpr int kTileRows = 128;  // query rows per tile (MMA M) and KV rows per tile (MMA N)
-constexpr int kStages = 2;
 constexpr int kChunks = kTileRows / 8;
-constexpr int kAttnThreads = 256;
+constexpr int kMetaRing = 4;
+constexpr int kSoftmaxWarps = 8;
+constexpr int kSoftmaxThreads = kSoftmaxWarps * 32;
+constexpr int kAttnThreads = 4 * 32 + kSoftmaxThreads;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+
+template <int D>
+struct AttnCfg {
+  static constexpr int kKStages = D == 128 ? 3 : 4;
+  static constexpr int kVStages = D == 128 ? 2 : 3;
+  static constexpr int kTileBytes = kTileRows * D * 2;  // one K or V tile
+};
 
 struct AttnMaps {
   CUtensorMap q;
@@ -49,12 +63,18 @@ struct AttnParams {
 
 template <int D>
 struct AttnSmem {
-  alignas(1024) uint8_t q[kTileRows * D * 2];            // [D/64][128 rows][128 B]
-  alignas(1024) uint8_t p[kTileRows * kTileRows * 2];    // [2][128 rows][128 B]
-  alignas(1024) uint8_t k[kStages][kTileRows * D * 2];   // [D/64][128 rows][128 B]
-  alignas(1024) uint8_t v[kStages][kTileRows * D * 2];
-  uint32_t meta[kStages][kChunks];
-  uint64_t q_full, kv_full[kStages], kv_empty[kStages], s_full[2], s_free[2], p_full, o_done;
+  using C = AttnCfg<D>;
+  uint8_t q[kTileRows * D * 2];                   // [D/64][128 rows][128 B]
+  uint8_t p[kTileRows * kTileRows * 2];           // [2][128 rows][128 B]
+  uint8_t k[C::kKStages][C::kTileBytes];          // [D/64][128 rows][128 B]
+  uint8_t v[C::kVStages][C::kTileBytes];
+  uint32_t meta[kMetaRing][kChunks];
+  float red[2][2][kTileRows];                     // [tile parity][warpgroup][row]
+  uint64_t q_full;
+  uint64_t k_full[C::kKStages], k_empty[C::kKStages];
+  uint64_t v_full[C::kVStages], v_empty[C::kVStages];
+  uint64_t meta_full[kMetaRing], meta_empty[kMetaRing];
+  uint64_t s_full[2], s_free[2], p_full, o_done;
   uint32_t tmem_base;
 };
 
@@ -64,9 +84,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                         const uint16_t* __restrict__ csr, const int32_t* __restrict__ info,
                         uint16_t* __restrict__ out, float* __restrict__ lse,
                         int32_t* __restrict__ skipped) {
-  extern __shared__ unsigned char smem_raw[];
-  auto& sm = *reinterpret_cast<AttnSmem<D>*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  using C = AttnCfg<D>;
+  constexpr int KST = C::kKStages, VST = C::kVStages;
+  constexpr int OC = D / 2;  // O columns per softmax warpgroup
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  auto& sm = *reinterpret_cast<AttnSmem<D>*>(smem_raw);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t unit = blockIdx.x;
@@ -80,16 +102,25 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 
   // ---------------------------------------------------------------- setup
   if (threadIdx.x == 0) {
+    if (smem_u32(smem_raw) & 1023u) __trap();  // 128B-swizzle atoms need 1024-B alignment
     mbar_init(&sm.q_full, 1);
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&sm.kv_full[s], 1);
-      mbar_init(&sm.kv_empty[s], 1);
+    for (int s = 0; s < KST; ++s) {
+      mbar_init(&sm.k_full[s], 1);
+      mbar_init(&sm.k_empty[s], 1);
+    }
+    for (int s = 0; s < VST; ++s) {
+      mbar_init(&sm.v_full[s], 1);
+      mbar_init(&sm.v_empty[s], 1);
+    }
+    for (int s = 0; s < kMetaRing; ++s) {
+      mbar_init(&sm.meta_full[s], 1);
+      mbar_init(&sm.meta_empty[s], kSoftmaxThreads);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&sm.s_full[s], 1);
-      mbar_init(&sm.s_free[s], 128);
+      mbar_init(&sm.s_free[s], kSoftmaxThreads);
     }
-    mbar_init(&sm.p_full, 4);
+    mbar_init(&sm.p_full, kSoftmaxWarps);
     mbar_init(&sm.o_done, 1);
     fence_barrier_init();
   }
@@ -106,7 +137,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   }
   {  // V tiles may be read past the last filled slot of a tile: keep them finite (zero)
     uint4* vz = reinterpret_cast<uint4*>(&sm.v[0][0]);
-    const int nvec = kStages * kTileRows * D * 2 / 16;
+    const int nvec = VST * C::kTileBytes / 16;
     for (int t = threadIdx.x; t < nvec; t += kAttnThreads) vz[t] = make_uint4(0, 0, 0, 0);
     fence_proxy_async_smem();
   }
@@ -117,54 +148,86 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 
   if (warp == 0) {
     // ================================================================ TMA producer
-    if (lane == 0 && T > 0) {
-      mbar_arrive_expect_tx(&sm.q_full, kTileRows * D * 2);
-      for (int c = 0; c < D / 64; ++c)
-        tma_load_2d(&maps.q, &sm.q_full, sm.q + c * kTileRows * 128, c * 64,
-                    static_cast<int>(q_row0));
+    // Lane-parallel tile packing: lane l owns plan entry e+l (l < 16; a tile holds at most
+    // 128/8 segments). A warp inclusive scan of the slot sizes yields every segment's row
+    // offset; the segments whose running total fits in 128 rows form tile t. Each such lane
+    // issues its own K/V TMA boxes and writes the meta words of its 8-column chunks.
+    if (T > 0) {
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&sm.q_full, kTileRows * D * 2);
+        for (int c = 0; c < D / 64; ++c)
+          tma_load_2d(&maps.q, &sm.q_full, sm.q + c * kTileRows * 128, c * 64,
+                      static_cast<int>(q_row0));
+      }
       const uint16_t* plan = csr + unit * p.n_k;
       const int64_t q_lo = static_cast<int64_t>(i) * p.b_q;
+      uint32_t cur = lane < n_ent ? plan[lane] : 0u;
+      uint32_t nxt = 32 + lane < n_ent ? plan[32 + lane] : 0u;
+      int base = 0;  // plan index held by lane 0 of `cur`
       int e = 0;
       for (int t = 0; t < T; ++t) {
-        const int st = t % kStages;
-        if (t >= kStages) mbar_wait(&sm.kv_empty[st], ((t / kStages) - 1) & 1);
-        int seg_h[kChunks], seg_row[kChunks], seg_off[kChunks];
-        int nseg = 0, off = 0;
-        uint32_t meta[kChunks];
+        const int ks = t % KST, vs = t % VST, ms = t % kMetaRing;
+        // entry e + lane from the two-window register cache
+        const int rel = e - base + lane;
+        const uint32_t a = __shfl_sync(0xffffffffu, cur, rel & 31);
+        const uint32_t bb = __shfl_sync(0xffffffffu, nxt, rel & 31);
+        const uint32_t ent = rel < 32 ? a : bb;
+        const bool valid = lane < kChunks && e + lane < n_ent;
+        const int j = static_cast<int>(ent & 0xFFFu);
+        const int h = valid ? static_cast<int>(ent >> 12) : 1;
+        const int L = valid ? (p.b_k >> (h - 1)) : 0;
+        int sz = 256;  // never fits: keeps the fitting lanes a prefix
+        if (valid) sz = L <= 8 ? 8 : (1 << (32 - __clz(L - 1)));
+        int incl = sz;
 #pragma unroll
-        for (int c = 0; c < kChunks; ++c) meta[c] = 0;
-        while (e < n_ent) {
-          const uint32_t ent = plan[e];
-          const int j = static_cast<int>(ent & 0xFFFu), h = static_cast<int>(ent >> 12);
-          const int sz = p.slot_lvl[h - 1];
-          if (off + sz > kTileRows) break;
-          const int L = p.rows_lvl[h - 1];
-          const bool straddle =
-              p.causal && (static_cast<int64_t>(j + 1) * p.b_k - 1 > q_lo);
-          for (int c = off / 8; c < (off + sz) / 8; ++c) {
-            const int first = c * 8 - off;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const bool fits = incl <= kTileRows;
+        const int nseg = __popc(__ballot_sync(0xffffffffu, fits));
+        const int total = __shfl_sync(0xffffffffu, incl, nseg - 1);
+        const int off = incl - sz;
+        const int row = static_cast<int>(bhkv * (p.n >> (h - 1)) + static_cast<int64_t>(j) * L);
+        const uint32_t bytes = static_cast<uint32_t>(total) * D * 2;
+
+        if (t >= KST) mbar_wait(&sm.k_empty[ks], ((t / KST) - 1) & 1);
+        if (lane == 0) mbar_arrive_expect_tx(&sm.k_full[ks], bytes);
+        __syncwarp();
+        if (fits)
+          for (int c = 0; c < D / 64; ++c)
+            tma_load_2d(&maps.k[h - 1], &sm.k_full[ks], sm.k[ks] + c * kTileRows * 128 + off * 128,
+                        c * 64, row);
+
+        if (t >= kMetaRing) mbar_wait(&sm.meta_empty[ms], ((t / kMetaRing) - 1) & 1);
+        if (fits) {
+          const bool straddle = p.causal && (static_cast<int64_t>(j + 1) * p.b_k - 1 > q_lo);
+          for (int c = 0; c < sz / 8; ++c) {
+            const int first = c * 8;
             const int nv = min(max(L - first, 0), 8);
             const uint32_t kpos = static_cast<uint32_t>(j * p.b_k + first);
-            meta[c] = static_cast<uint32_t>(nv) | (static_cast<uint32_t>(h - 1) << 4) |
-                      ((straddle ? 1u : 0u) << 8) | (kpos << 9);
+            sm.meta[ms][off / 8 + c] = static_cast<uint32_t>(nv) |
+                                       (static_cast<uint32_t>(h - 1) << 4) |
+                                       ((straddle ? 1u : 0u) << 8) | (kpos << 9);
           }
-          seg_h[nseg] = h;
-          seg_row[nseg] = static_cast<int>(bhkv * p.nh_lvl[h - 1] + static_cast<int64_t>(j) * L);
-          seg_off[nseg] = off;
-          ++nseg;
-          off += sz;
-          ++e;
         }
-        for (int c = 0; c < kChunks; ++c) sm.meta[st][c] = meta[c];
-        mbar_arrive_expect_tx(&sm.kv_full[st], static_cast<uint32_t>(off) * D * 2 * 2);
-        for (int g = 0; g < nseg; ++g) {
-          const int h = seg_h[g];
-          for (int c = 0; c < D / 64; ++c) {
-            tma_load_2d(&maps.k[h - 1], &sm.kv_full[st],
-                        sm.k[st] + c * kTileRows * 128 + seg_off[g] * 128, c * 64, seg_row[g]);
-            tma_load_2d(&maps.v[h - 1], &sm.kv_full[st],
-                        sm.v[st] + c * kTileRows * 128 + seg_off[g] * 128, c * 64, seg_row[g]);
-          }
+        if (lane < kChunks && lane >= total / 8) sm.meta[ms][lane] = 0u;  // unused tail chunks
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.meta_full[ms]);
+
+        if (t >= VST) mbar_wait(&sm.v_empty[vs], ((t / VST) - 1) & 1);
+        if (lane == 0) mbar_arrive_expect_tx(&sm.v_full[vs], bytes);
+        __syncwarp();
+        if (fits)
+          for (int c = 0; c < D / 64; ++c)
+            tma_load_2d(&maps.v[h - 1], &sm.v_full[vs], sm.v[vs] + c * kTileRows * 128 + off * 128,
+                        c * 64, row);
+
+        e += nseg;
+        if (e - base >= 32) {  // advance the window (warp-uniform)
+          base += 32;
+          cur = nxt;
+          nxt = base + 32 + lane < n_ent ? plan[base + 32 + lane] : 0u;
         }
       }
     }
@@ -175,27 +238,28 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       constexpr uint32_t idesc_o = umma_idesc_bf16(128, D, false, true);
       const uint32_t q_base = smem_u32(sm.q), p_base = smem_u32(sm.p);
       auto issue_pv = [&](int u) {
-        const int st = u % kStages;
+        const int vs = u % VST;
+        mbar_wait(&sm.v_full[vs], (u / VST) & 1);
         mbar_wait(&sm.p_full, u & 1);
         tc_fence_after();
-        const uint32_t v_base = smem_u32(sm.v[st]);
+        const uint32_t v_base = smem_u32(sm.v[vs]);
 #pragma unroll
         for (int kk = 0; kk < kTileRows / 16; ++kk) {
           const uint64_t a = umma_desc_sw128(p_base + (kk >> 2) * kTileRows * 128 + (kk & 3) * 32, 16, 1024);
           const uint64_t bdesc = umma_desc_sw128(v_base + kk * 16 * 128, kTileRows * 128, 1024);
           mma_bf16_ss(tmem + 256, a, bdesc, idesc_o, (u > 0 || kk > 0) ? 1u : 0u);
         }
-        mma_commit(&sm.kv_empty[st]);
+        mma_commit(&sm.v_empty[vs]);
         mma_commit(&sm.o_done);
       };
       mbar_wait(&sm.q_full, 0);
       tc_fence_after();
       for (int t = 0; t < T; ++t) {
-        const int st = t % kStages, sb = t & 1;
-        mbar_wait(&sm.kv_full[st], (t / kStages) & 1);
+        const int ks = t % KST, sb = t & 1;
+        mbar_wait(&sm.k_full[ks], (t / KST) & 1);
         if (t >= 2) mbar_wait(&sm.s_free[sb], ((t >> 1) - 1) & 1);
         tc_fence_after();
-        const uint32_t k_base = smem_u32(sm.k[st]);
+        const uint32_t k_base = smem_u32(sm.k[ks]);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t koff = (kk >> 2) * kTileRows * 128 + (kk & 3) * 32;
@@ -203,6 +267,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           const uint64_t bdesc = umma_desc_sw128(k_base + koff, 16, 1024);
           mma_bf16_ss(tmem + sb * 128, a, bdesc, idesc_s, kk > 0 ? 1u : 0u);
         }
+        mma_commit(&sm.k_empty[ks]);
         mma_commit(&sm.s_full[sb]);
         if (t >= 1) issue_pv(t - 1);
       }
@@ -210,49 +275,60 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     }
   } else if (warp >= 4) {
     // ================================================================ softmax + epilogue
-    const int wq = warp & 3;
+    const int wg = (warp - 4) >> 2;  // warpgroup: S columns [64 wg, 64 wg + 64)
+    const int wq = warp & 3;         // TMEM lane quarter
     const int row = wq * 32 + lane;
     const uint32_t t_lane = tmem + (static_cast<uint32_t>(wq * 32) << 16);
     const int qpos = i * p.b_q + row;
     const float scale = p.scale_log2;
+    const float2 scale2 = make_float2(scale, scale);
     float m_run = -INFINITY, l_run = 0.f;
     for (int t = 0; t < T; ++t) {
-      const int st = t % kStages, sb = t & 1;
+      const int sb = t & 1, ms = t % kMetaRing;
       mbar_wait(&sm.s_full[sb], (t >> 1) & 1);
       tc_fence_after();
-      uint32_t s[4][32];
-#pragma unroll
-      for (int c4 = 0; c4 < 4; ++c4) tmem_ld32(t_lane + sb * 128 + c4 * 32, s[c4]);
-#pragma unroll
-      for (int c4 = 0; c4 < 4; ++c4) tmem_ld_wait(s[c4]);
+      uint32_t s[2][32];
+      tmem_ld32(t_lane + sb * 128 + wg * 64, s[0]);
+      tmem_ld32(t_lane + sb * 128 + wg * 64 + 32, s[1]);
+      tmem_ld_wait(s[0]);
+      tmem_ld_wait(s[1]);
       tc_fence_before();
       mbar_arrive(&sm.s_free[sb]);
 
-      uint32_t mw[kChunks];
-#pragma unroll
-      for (int c = 0; c < kChunks; c += 4) {
-        const uint4 w4 = *reinterpret_cast<const uint4*>(&sm.meta[st][c]);
-        mw[c] = w4.x;
-        mw[c + 1] = w4.y;
-        mw[c + 2] = w4.z;
-        mw[c + 3] = w4.w;
+      mbar_wait(&sm.meta_full[ms], (t / kMetaRing) & 1);
+      uint32_t mw[8];
+      {
+        const uint4 w0 = *reinterpret_cast<const uint4*>(&sm.meta[ms][wg * 8]);
+        const uint4 w1 = *reinterpret_cast<const uint4*>(&sm.meta[ms][wg * 8 + 4]);
+        mw[0] = w0.x; mw[1] = w0.y; mw[2] = w0.z; mw[3] = w0.w;
+        mw[4] = w1.x; mw[5] = w1.y; mw[6] = w1.z; mw[7] = w1.w;
       }
-      int nvc[kChunks];
+      mbar_arrive(&sm.meta_empty[ms]);
+
+      // ---- row max over this half (chunk-wise; warp-uniform fast path for full chunks)
+      int nvc[8];
       float mt = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < kChunks; ++c) {
+      for (int c = 0; c < 8; ++c) {
         const uint32_t w = mw[c];
+        const float* x = reinterpret_cast<const float*>(&s[c >> 2][(c & 3) * 8]);
         int nv = static_cast<int>(w & 15u);
-        if ((w >> 8) & 1u) nv = min(nv, max(qpos - static_cast<int>(w >> 9) + 1, 0));
-        nvc[c] = nv;
-        float mx = -INFINITY;
+        float mx;
+        if (nv == 8 && !(w & 256u)) {
+          mx = fmax3(fmax3(x[0], x[1], x[2]), fmax3(x[3], x[4], x[5]), fmaxf(x[6], x[7]));
+        } else {
+          if (w & 256u) nv = min(nv, max(qpos - static_cast<int>(w >> 9) + 1, 0));
+          mx = -INFINITY;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float x = __uint_as_float(s[c >> 2][(c & 3) * 8 + e]);
-          mx = (e < nv) ? fmaxf(mx, x) : mx;
+          for (int e = 0; e < 8; ++e) mx = (e < nv) ? fmaxf(mx, x[e]) : mx;
         }
+        nvc[c] = nv;
         mt = fmaxf(mt, fmaf(mx, scale, static_cast<float>((w >> 4) & 15u)));
       }
+      sm.red[t & 1][wg][row] = mt;
+      named_bar_sync(1, kSoftmaxThreads);
+      mt = fmaxf(sm.red[t & 1][0][row], sm.red[t & 1][1][row]);
+
       const float m_new = fmaxf(m_run, mt);
       const bool resc = m_new > m_run + kRescaleThreshold;
       float alpha = 1.f;
@@ -261,48 +337,57 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         m_run = m_new;
       }
       const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
-      float lsum = 0.f;
-      uint32_t pk[kChunks * 4];
+      float2 lsum = make_float2(0.f, 0.f);
+      uint32_t pk[32];
 #pragma unroll
-      for (int c = 0; c < kChunks; ++c) {
-        const float off = static_cast<float>((mw[c] >> 4) & 15u) - m_use;
+      for (int c = 0; c < 8; ++c) {
+        const uint32_t w = mw[c];
+        const float off = static_cast<float>((w >> 4) & 15u) - m_use;
+        const float2 off2 = make_float2(off, off);
+        const float* x = reinterpret_cast<const float*>(&s[c >> 2][(c & 3) * 8]);
         const int nv = nvc[c];
+        if (nv == 8) {
 #pragma unroll
-        for (int e = 0; e < 8; e += 2) {
-          const float x0 = __uint_as_float(s[c >> 2][(c & 3) * 8 + e]);
-          const float x1 = __uint_as_float(s[c >> 2][(c & 3) * 8 + e + 1]);
-          const float p0 = (e < nv) ? ex2_approx(fmaf(x0, scale, off)) : 0.f;
-          const float p1 = (e + 1 < nv) ? ex2_approx(fmaf(x1, scale, off)) : 0.f;
-          lsum += p0 + p1;
-          __nv_bfloat162 pb = __floats2bfloat162_rn(p0, p1);
-          pk[c * 4 + e / 2] = *reinterpret_cast<uint32_t*>(&pb);
+          for (int e = 0; e < 8; e += 2) {
+            float2 y = ffma2(make_float2(x[e], x[e + 1]), scale2, off2);
+            y.x = ex2_approx(y.x);
+            y.y = ex2_approx(y.y);
+            lsum = fadd2(lsum, y);
+            pk[c * 4 + e / 2] = pack_bf16x2(y.x, y.y);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; e += 2) {
+            float2 y = ffma2(make_float2(x[e], x[e + 1]), scale2, off2);
+            y.x = (e < nv) ? ex2_approx(y.x) : 0.f;
+            y.y = (e + 1 < nv) ? ex2_approx(y.y) : 0.f;
+            lsum = fadd2(lsum, y);
+            pk[c * 4 + e / 2] = pack_bf16x2(y.x, y.y);
+          }
         }
       }
-      l_run = l_run * alpha + lsum;
+      l_run = l_run * alpha + (lsum.x + lsum.y);
 
       const bool need = (t > 0) && __any_sync(0xffffffffu, resc);
       if (t > 0) mbar_wait(&sm.o_done, (t - 1) & 1);  // PV(t-1) done: P tile free, O stable
       if (need) {
         tc_fence_after();
 #pragma unroll
-        for (int c4 = 0; c4 < D / 32; ++c4) {
+        for (int c4 = 0; c4 < OC / 32; ++c4) {
           uint32_t o[32];
-          tmem_ld32(t_lane + 256 + c4 * 32, o);
+          tmem_ld32(t_lane + 256 + wg * OC + c4 * 32, o);
           tmem_ld_wait(o);
 #pragma unroll
           for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-          tmem_st32(t_lane + 256 + c4 * 32, o);
+          tmem_st32(t_lane + 256 + wg * OC + c4 * 32, o);
         }
         tmem_st_wait();
       }
-      uint8_t* prow = sm.p + row * 128;
+      uint8_t* prow = sm.p + wg * kTileRows * 128 + row * 128;
 #pragma unroll
-      for (int cc = 0; cc < 16; ++cc) {
-        const int half = cc >> 3, within = cc & 7;
-        uint8_t* dst = prow + half * kTileRows * 128 + ((within ^ (row & 7)) << 4);
-        *reinterpret_cast<uint4*>(dst) =
+      for (int cc = 0; cc < 8; ++cc)
+        *reinterpret_cast<uint4*>(prow + ((cc ^ (row & 7)) << 4)) =
             make_uint4(pk[cc * 4], pk[cc * 4 + 1], pk[cc * 4 + 2], pk[cc * 4 + 3]);
-      }
       fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();
@@ -310,19 +395,23 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     }
 
     // ---------------------------------------------------------------- epilogue
+    named_bar_sync(1, kSoftmaxThreads);  // both halves finished reading red[]
+    sm.red[0][wg][row] = l_run;
+    named_bar_sync(1, kSoftmaxThreads);
+    const float l_tot = sm.red[0][0][row] + sm.red[0][1][row];
     if (T > 0) {
       mbar_wait(&sm.o_done, (T - 1) & 1);
       tc_fence_after();
     }
     const bool valid = row < p.b_q;
-    const bool alive = l_run > 0.f;
-    const float inv = alive ? 1.f / l_run : 0.f;
-    uint16_t* orow = out + (q_row0 + row) * D;
+    const bool alive = l_tot > 0.f;
+    const float inv = alive ? 1.f / l_tot : 0.f;
+    uint16_t* orow = out + (q_row0 + row) * D + wg * OC;
 #pragma unroll
-    for (int c4 = 0; c4 < D / 32; ++c4) {
+    for (int c4 = 0; c4 < OC / 32; ++c4) {
       uint32_t o[32];
       if (T > 0) {
-        tmem_ld32(t_lane + 256 + c4 * 32, o);
+        tmem_ld32(t_lane + 256 + wg * OC + c4 * 32, o);
         tmem_ld_wait(o);
       } else {
 #pragma unroll
@@ -330,11 +419,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       }
       uint32_t pkd[16];
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        __nv_bfloat162 v2 = __floats2bfloat162_rn(__uint_as_float(o[2 * e]) * inv,
-                                                  __uint_as_float(o[2 * e + 1]) * inv);
-        pkd[e] = *reinterpret_cast<uint32_t*>(&v2);
-      }
+      for (int e = 0; e < 16; ++e)
+        pkd[e] = pack_bf16x2(__uint_as_float(o[2 * e]) * inv, __uint_as_float(o[2 * e + 1]) * inv);
       if (valid) {
 #pragma unroll
         for (int v4 = 0; v4 < 4; ++v4)
@@ -342,10 +428,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
               make_uint4(pkd[v4 * 4], pkd[v4 * 4 + 1], pkd[v4 * 4 + 2], pkd[v4 * 4 + 3]);
       }
     }
-    if (valid)
-      lse[q_row0 + row] = alive ? (m_run + log2f(l_run)) * 0.69314718055994530942f : -INFINITY;
-    const unsigned dead = __ballot_sync(0xffffffffu, valid && !alive);
-    if (lane == 0 && dead) atomicAdd(skipped, __popc(dead));
+    if (wg == 0) {
+      if (valid)
+        lse[q_row0 + row] = alive ? (m_run + log2f(l_tot)) * 0.69314718055994530942f : -INFINITY;
+      const unsigned dead = __ballot_sync(0xffffffffu, valid && !alive);
+      if (lane == 0 && dead) atomicAdd(skipped, __popc(dead));
+    }
   }
 
   // ---------------------------------------------------------------- teardown
@@ -430,7 +518,7 @@ static int launch_attn(const void* q, const void* k, const void* v, const void* 
     rc = encode_2d(&maps.v[h - 1], vb, rows, D, sz);
     if (rc) return rc;
   }
-  const size_t smem = sizeof(AttnSmem<D>) + 1024;
+  const size_t smem = sizeof(AttnSmem<D>);
   cudaFuncSetAttribute(psa_attn_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(smem));
   const int64_t units = batch * hq * p.n_q;

@@ -31,9 +31,9 @@ PSA_DEV void dmma_m8n8k4(double& d0, double& d1, double a, double b) {
 
 template <int D>
 struct ImpSmem {
-  static constexpr int kLd = D + 4;  // padded fp64 row (bank spread for fragment loads)
-  double qs[kImpRows * kLd];
-  double ks[kImpCols * kLd];
+  static constexpr int kLd = D + 8;  // padded bf16 row: 8 rows of a fragment hit distinct banks
+  uint16_t qs[kImpRows * kLd];
+  uint16_t ks[kImpCols * kLd];
   double x[kImpRows * (kImpCols + 1)];
 };
 
@@ -57,26 +57,24 @@ PSA_DEV void gather_rows_regs(const uint16_t* __restrict__ base, const int32_t* 
 }
 
 template <int D>
-PSA_DEV void store_rows_f64(double* dst, const uint4 (&buf)[kImpCols * D / 8 / kImpThreads]) {
+PSA_DEV void store_rows_bf16(uint16_t* dst, const uint4 (&buf)[kImpCols * D / 8 / kImpThreads]) {
   constexpr int kVecPerRow = D / 8;
   constexpr int kPer = kImpCols * D / 8 / kImpThreads;
-  constexpr int kLd = D + 4;
+  constexpr int kLd = D + 8;
 #pragma unroll
   for (int p = 0; p < kPer; ++p) {
     const int idx = threadIdx.x + p * kImpThreads;
     const int r = idx / kVecPerRow, c = idx % kVecPerRow;
-    const uint32_t w[4] = {buf[p].x, buf[p].y, buf[p].z, buf[p].w};
-    double* o = dst + r * kLd + c * 8;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      o[2 * e] = bf16_bits_to_dbl(static_cast<uint16_t>(w[e] & 0xFFFFu));
-      o[2 * e + 1] = bf16_bits_to_dbl(static_cast<uint16_t>(w[e] >> 16));
-    }
+    *reinterpret_cast<uint4*>(dst + r * kLd + c * 8) = buf[p];
   }
 }
 
+PSA_DEV double bf16_to_f64(uint16_t h) {
+  return static_cast<double>(__uint_as_float(static_cast<uint32_t>(h) << 16));
+}
+
 template <int D, bool MEAN>
-__global__ void __launch_bounds__(kImpThreads, 1)
+__global__ void __launch_bounds__(kImpThreads, 2)
     importance_stats_kernel(const uint16_t* __restrict__ q, const uint16_t* __restrict__ k,
                             int hq, int hkv, int64_t n, const int32_t* __restrict__ q_rows,
                             const int32_t* __restrict__ k_rows, int R, int s_k, int n_k,
@@ -100,7 +98,7 @@ __global__ void __launch_bounds__(kImpThreads, 1)
   {
     uint4 buf[kPer];
     gather_rows_regs<D>(qh, q_rows, a0, rows_here, buf);
-    store_rows_f64<D>(sm.qs, buf);
+    store_rows_bf16<D>(sm.qs, buf);
   }
 
   const int blocks_per_chunk = kImpCols / s_k;  // s_k <= 64 checked on the host
@@ -115,6 +113,7 @@ __global__ void __launch_bounds__(kImpThreads, 1)
   const bool row_ok = a_loc < rows_here;
 
   double m_run = -INFINITY, l_run = 0.0;
+  const double inv_sqrt_d = 1.0 / sqrt_d;
   double m_fin = 0.0, l_fin = 1.0;
   if (MEAN && row_ok) {
     m_fin = mstat[static_cast<int64_t>(bhq) * R + a_glob];
@@ -128,7 +127,7 @@ __global__ void __launch_bounds__(kImpThreads, 1)
     const int b0 = ch * cw;
     const int cols = min(cw, C - b0);
     __syncthreads();  // previous chunk's X/K consumers are done
-    store_rows_f64<D>(sm.ks, pref);
+    store_rows_bf16<D>(sm.ks, pref);
     if (ch + 1 < n_chunks) gather_rows_regs<D>(kh, k_rows, b0 + cw, min(cw, C - b0 - cw), pref);
     __syncthreads();
 
@@ -138,15 +137,15 @@ __global__ void __launch_bounds__(kImpThreads, 1)
     for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
       for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-    const double* qa = sm.qs + (wr * 32 + (lane >> 2)) * kLd + (lane & 3);
-    const double* kb = sm.ks + (wc * 16 + (lane >> 2)) * kLd + (lane & 3);
+    const uint16_t* qa = sm.qs + (wr * 32 + (lane >> 2)) * kLd + (lane & 3);
+    const uint16_t* kb = sm.ks + (wc * 16 + (lane >> 2)) * kLd + (lane & 3);
 #pragma unroll 4
     for (int k4 = 0; k4 < D / 4; ++k4) {
       double af[4], bf[2];
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt) af[mt] = qa[mt * 8 * kLd + k4 * 4];
+      for (int mt = 0; mt < 4; ++mt) af[mt] = bf16_to_f64(qa[mt * 8 * kLd + k4 * 4]);
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt) bf[nt] = kb[nt * 8 * kLd + k4 * 4];
+      for (int nt = 0; nt < 2; ++nt) bf[nt] = bf16_to_f64(kb[nt * 8 * kLd + k4 * 4]);
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
@@ -160,7 +159,7 @@ __global__ void __launch_bounds__(kImpThreads, 1)
         for (int e = 0; e < 2; ++e) {
           const int r = wr * 32 + mt * 8 + (lane >> 2);
           const int c = wc * 16 + nt * 8 + (lane & 3) * 2 + e;
-          sm.x[r * kXld + c] = __ddiv_rn(acc[mt][nt][e], sqrt_d);  // importance.py:80
+          sm.x[r * kXld + c] = acc[mt][nt][e];  // raw fp64 dot (exact); scaled below
         }
     __syncthreads();
 
@@ -169,19 +168,24 @@ __global__ void __launch_bounds__(kImpThreads, 1)
     const int nb = cols / s_k;
     const int j0 = b0 / s_k;
     if (!MEAN) {
+      // block max of the raw dots, then ONE IEEE division per block: x -> fl(x / sqrt(d)) is
+      // monotone, so fl(max(x) / sqrt(d)) is exactly the reference's block-max logit.
       double lmax = -INFINITY;
       for (int bb = quad; bb < nb; bb += 4) {
         double bm = -INFINITY;
         for (int t = 0; t < s_k; ++t) bm = fmax(bm, xr[bb * s_k + t]);
+        bm = __ddiv_rn(bm, sqrt_d);  // importance.py:80
         lmax = fmax(lmax, bm);
         if (row_ok) M[(static_cast<int64_t>(bhq) * R + a_glob) * n_k + j0 + bb] = bm;
       }
       lmax = fmax(lmax, __shfl_xor_sync(0xffffffffu, lmax, 1));
       lmax = fmax(lmax, __shfl_xor_sync(0xffffffffu, lmax, 2));
       const double m_new = fmax(m_run, lmax);
+      // softmax denominator (only its value, not its summation order, matters downstream)
       double part = 0.0;
       for (int bb = quad; bb < nb; bb += 4)
-        for (int t = 0; t < s_k; ++t) part = __dadd_rn(part, exp(__dsub_rn(xr[bb * s_k + t], m_new)));
+        for (int t = 0; t < s_k; ++t)
+          part = __dadd_rn(part, exp(__fma_rn(xr[bb * s_k + t], inv_sqrt_d, -m_new)));
       part = __dadd_rn(part, __shfl_xor_sync(0xffffffffu, part, 1));
       part = __dadd_rn(part, __shfl_xor_sync(0xffffffffu, part, 2));
       l_run = __dadd_rn(__dmul_rn(l_run, exp(__dsub_rn(m_run, m_new))), part);
@@ -190,7 +194,7 @@ __global__ void __launch_bounds__(kImpThreads, 1)
       for (int bb = quad; bb < nb; bb += 4) {
         double s = 0.0;
         for (int t = 0; t < s_k; ++t)
-          s = __dadd_rn(s, __ddiv_rn(exp(__dsub_rn(xr[bb * s_k + t], m_fin)), l_fin));
+          s = __dadd_rn(s, __ddiv_rn(exp(__dsub_rn(__ddiv_rn(xr[bb * s_k + t], sqrt_d), m_fin)), l_fin));
         if (row_ok) M[(static_cast<int64_t>(bhq) * R + a_glob) * n_k + j0 + bb] = s;
       }
     }

@@ -1,0 +1,63 @@
+"""CPU, world_size 2 (gloo): the (batch, head) sharding covers every head exactly once and the
+optional output gather reassembles the single-process result bit-for-bit."""
+
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2512_04025_b200.parallel import gather_outputs, shard_heads
+
+
+@pytest.mark.parametrize("hq,hkv,world", [(40, 40, 8), (12, 12, 8), (28, 4, 8), (28, 4, 3),
+                                          (2, 2, 2), (40, 40, 1)])
+def test_shards_partition_heads(hq, hkv, world):
+    seen_q, seen_kv = [], []
+    for r in range(world):
+        q, kv = shard_heads(hq, hkv, world, r)
+        seen_q += q
+        seen_kv += kv
+        assert all(h // (hq // hkv) in kv for h in q)
+    assert sorted(seen_q) == list(range(hq)) and sorted(seen_kv) == list(range(hkv))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, hq, hkv, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        full = torch.arange(2 * hq * 8 * 4, dtype=torch.float32).reshape(2, hq, 8, 4)
+        heads, _ = shard_heads(hq, hkv, world, rank)
+        local = full[:, heads] * 1.0  # the "computation" of this rank's shard
+        got = gather_outputs(local, hq, hkv, dst=0)
+        if rank == 0:
+            q.put(bool(torch.equal(got, full)))
+        else:
+            q.put(got is None)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("hq,hkv", [(6, 3), (5, 5)])
+def test_gather_world2_gloo(hq, hkv):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, hq, hkv, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+    res = [q.get(timeout=5) for _ in range(2)]
+    assert all(res) and all(p.exitcode == 0 for p in procs)
