@@ -38,11 +38,13 @@ constexpr int kSoftmaxWarps = 8;
 constexpr int kSoftmaxThreads = kSoftmaxWarps * 32;
 constexpr int kAttnThreads = 4 * 32 + kSoftmaxThreads;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+// TMEM columns: S0 | S1 | O (D) | P (64 packed bf16x2 columns)
+constexpr uint32_t kTmemS = 0, kTmemO = 256, kTmemP = 384;
 
 template <int D>
 struct AttnCfg {
   static constexpr int kKStages = D == 128 ? 3 : 4;
-  static constexpr int kVStages = D == 128 ? 2 : 3;
+  static constexpr int kVStages = D == 128 ? 2 : 4;
   static constexpr int kTileBytes = kTileRows * D * 2;  // one K or V tile
 };
 
@@ -56,19 +58,16 @@ struct AttnParams {
   int64_t n;
   int hq, hkv, b_q, b_k, levels, n_q, n_k, causal;
   float scale_log2;
-  int rows_lvl[kMaxLevels];
-  int slot_lvl[kMaxLevels];
-  int64_t nh_lvl[kMaxLevels];
 };
 
 template <int D>
 struct AttnSmem {
   using C = AttnCfg<D>;
   uint8_t q[kTileRows * D * 2];                   // [D/64][128 rows][128 B]
-  uint8_t p[kTileRows * kTileRows * 2];           // [2][128 rows][128 B]
   uint8_t k[C::kKStages][C::kTileBytes];          // [D/64][128 rows][128 B]
   uint8_t v[C::kVStages][C::kTileBytes];
-  uint32_t meta[kMetaRing][kChunks];
+  float bias[kMetaRing][kTileRows];               // per KV column: level-1 (log2) or -inf
+  uint32_t meta[kMetaRing][kChunks];              // causal: key position | straddle flag
   float red[2][2][kTileRows];                     // [tile parity][warpgroup][row]
   uint64_t q_full;
   uint64_t k_full[C::kKStages], k_empty[C::kKStages];
@@ -76,6 +75,59 @@ struct AttnSmem {
   uint64_t meta_full[kMetaRing], meta_empty[kMetaRing];
   uint64_t s_full[2], s_free[2], p_full, o_done;
   uint32_t tmem_base;
+};
+
+// Tile packing shared by the K and V producer warps: lane l (< 16) owns plan entry e + l; a
+// warp inclusive scan of the slot sizes gives each segment's row offset in the tile, and the
+// lanes whose running total fits in 128 rows form the tile.
+struct TileSeg {
+  int j, h, L, sz, off, row, total, nseg;
+  bool fits;
+};
+
+struct PlanCursor {
+  const uint16_t* plan;
+  int n_ent, e, base;
+  uint32_t cur, nxt;
+  PSA_DEV void init(const uint16_t* pl, int n, int lane) {
+    plan = pl;
+    n_ent = n;
+    e = 0;
+    base = 0;
+    cur = lane < n ? plan[lane] : 0u;
+    nxt = 32 + lane < n ? plan[32 + lane] : 0u;
+  }
+  PSA_DEV TileSeg next(const AttnParams& p, int64_t bhkv, int lane) {
+    TileSeg s;
+    const int rel = e - base + lane;
+    const uint32_t a = __shfl_sync(0xffffffffu, cur, rel & 31);
+    const uint32_t b = __shfl_sync(0xffffffffu, nxt, rel & 31);
+    const uint32_t ent = rel < 32 ? a : b;
+    const bool valid = lane < kChunks && e + lane < n_ent;
+    s.j = static_cast<int>(ent & 0xFFFu);
+    s.h = valid ? static_cast<int>(ent >> 12) : 1;
+    s.L = valid ? (p.b_k >> (s.h - 1)) : 0;
+    s.sz = 256;  // never fits: keeps the fitting lanes a prefix
+    if (valid) s.sz = s.L <= 8 ? 8 : (1 << (32 - __clz(s.L - 1)));
+    int incl = s.sz;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    s.fits = incl <= kTileRows;
+    s.nseg = __popc(__ballot_sync(0xffffffffu, s.fits));
+    s.total = __shfl_sync(0xffffffffu, incl, s.nseg - 1);
+    s.off = incl - s.sz;
+    s.row = static_cast<int>(bhkv * (p.n >> (s.h - 1)) + static_cast<int64_t>(s.j) * s.L);
+    e += s.nseg;
+    if (e - base >= 32) {  // advance the two-window cache (warp-uniform)
+      base += 32;
+      cur = nxt;
+      nxt = base + 32 + lane < n_ent ? plan[base + 32 + lane] : 0u;
+    }
+    return s;
+  }
 };
 
 template <int D>
@@ -135,10 +187,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     tmem_alloc(&sm.tmem_base, 512);
     tmem_relinquish();
   }
-  {  // V tiles may be read past the last filled slot of a tile: keep them finite (zero)
-    uint4* vz = reinterpret_cast<uint4*>(&sm.v[0][0]);
-    const int nvec = VST * C::kTileBytes / 16;
-    for (int t = threadIdx.x; t < nvec; t += kAttnThreads) vz[t] = make_uint4(0, 0, 0, 0);
+  {  // K/V rows past the last filled slot of a tile are read by the MMA: keep them finite
+    uint4* z = reinterpret_cast<uint4*>(&sm.k[0][0]);
+    const int nvec = (KST + VST) * C::kTileBytes / 16;
+    for (int t = threadIdx.x; t < nvec; t += kAttnThreads) z[t] = make_uint4(0, 0, 0, 0);
     fence_proxy_async_smem();
   }
   tc_fence_before();
@@ -147,11 +199,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   const uint32_t tmem = sm.tmem_base;
 
   if (warp == 0) {
-    // ================================================================ TMA producer
-    // Lane-parallel tile packing: lane l owns plan entry e+l (l < 16; a tile holds at most
-    // 128/8 segments). A warp inclusive scan of the slot sizes yields every segment's row
-    // offset; the segments whose running total fits in 128 rows form tile t. Each such lane
-    // issues its own K/V TMA boxes and writes the meta words of its 8-column chunks.
+    // ================================================================ K producer (+ Q, bias)
     if (T > 0) {
       if (lane == 0) {
         mbar_arrive_expect_tx(&sm.q_full, kTileRows * D * 2);
@@ -159,76 +207,62 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           tma_load_2d(&maps.q, &sm.q_full, sm.q + c * kTileRows * 128, c * 64,
                       static_cast<int>(q_row0));
       }
-      const uint16_t* plan = csr + unit * p.n_k;
       const int64_t q_lo = static_cast<int64_t>(i) * p.b_q;
-      uint32_t cur = lane < n_ent ? plan[lane] : 0u;
-      uint32_t nxt = 32 + lane < n_ent ? plan[32 + lane] : 0u;
-      int base = 0;  // plan index held by lane 0 of `cur`
-      int e = 0;
+      PlanCursor pc;
+      pc.init(csr + unit * p.n_k, n_ent, lane);
       for (int t = 0; t < T; ++t) {
-        const int ks = t % KST, vs = t % VST, ms = t % kMetaRing;
-        // entry e + lane from the two-window register cache
-        const int rel = e - base + lane;
-        const uint32_t a = __shfl_sync(0xffffffffu, cur, rel & 31);
-        const uint32_t bb = __shfl_sync(0xffffffffu, nxt, rel & 31);
-        const uint32_t ent = rel < 32 ? a : bb;
-        const bool valid = lane < kChunks && e + lane < n_ent;
-        const int j = static_cast<int>(ent & 0xFFFu);
-        const int h = valid ? static_cast<int>(ent >> 12) : 1;
-        const int L = valid ? (p.b_k >> (h - 1)) : 0;
-        int sz = 256;  // never fits: keeps the fitting lanes a prefix
-        if (valid) sz = L <= 8 ? 8 : (1 << (32 - __clz(L - 1)));
-        int incl = sz;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += y;
-        }
-        const bool fits = incl <= kTileRows;
-        const int nseg = __popc(__ballot_sync(0xffffffffu, fits));
-        const int total = __shfl_sync(0xffffffffu, incl, nseg - 1);
-        const int off = incl - sz;
-        const int row = static_cast<int>(bhkv * (p.n >> (h - 1)) + static_cast<int64_t>(j) * L);
-        const uint32_t bytes = static_cast<uint32_t>(total) * D * 2;
-
+        const int ks = t % KST, ms = t % kMetaRing;
+        const TileSeg s = pc.next(p, bhkv, lane);
+        const uint32_t bytes = static_cast<uint32_t>(s.total) * D * 2;
         if (t >= KST) mbar_wait(&sm.k_empty[ks], ((t / KST) - 1) & 1);
         if (lane == 0) mbar_arrive_expect_tx(&sm.k_full[ks], bytes);
         __syncwarp();
-        if (fits)
+        if (s.fits)
           for (int c = 0; c < D / 64; ++c)
-            tma_load_2d(&maps.k[h - 1], &sm.k_full[ks], sm.k[ks] + c * kTileRows * 128 + off * 128,
-                        c * 64, row);
-
+            tma_load_2d(&maps.k[s.h - 1], &sm.k_full[ks],
+                        sm.k[ks] + c * kTileRows * 128 + s.off * 128, c * 64, s.row);
+        // per-column bias (h-1 in log2 units, -inf on pad rows) and causal chunk meta
         if (t >= kMetaRing) mbar_wait(&sm.meta_empty[ms], ((t / kMetaRing) - 1) & 1);
-        if (fits) {
-          const bool straddle = p.causal && (static_cast<int64_t>(j + 1) * p.b_k - 1 > q_lo);
-          for (int c = 0; c < sz / 8; ++c) {
-            const int first = c * 8;
-            const int nv = min(max(L - first, 0), 8);
-            const uint32_t kpos = static_cast<uint32_t>(j * p.b_k + first);
-            sm.meta[ms][off / 8 + c] = static_cast<uint32_t>(nv) |
-                                       (static_cast<uint32_t>(h - 1) << 4) |
-                                       ((straddle ? 1u : 0u) << 8) | (kpos << 9);
+        if (s.fits) {
+          const float bv = static_cast<float>(s.h - 1);
+          for (int c = 0; c < s.sz; c += 4) {
+            float4 w;
+            w.x = c + 0 < s.L ? bv : -INFINITY;
+            w.y = c + 1 < s.L ? bv : -INFINITY;
+            w.z = c + 2 < s.L ? bv : -INFINITY;
+            w.w = c + 3 < s.L ? bv : -INFINITY;
+            *reinterpret_cast<float4*>(&sm.bias[ms][s.off + c]) = w;
+          }
+          if (p.causal) {
+            const bool straddle = static_cast<int64_t>(s.j + 1) * p.b_k - 1 > q_lo;
+            for (int c = 0; c < s.sz / 8; ++c)
+              sm.meta[ms][s.off / 8 + c] =
+                  (straddle ? 1u : 0u) | (static_cast<uint32_t>(s.j * p.b_k + c * 8) << 1);
           }
         }
-        if (lane < kChunks && lane >= total / 8) sm.meta[ms][lane] = 0u;  // unused tail chunks
+        if (4 * lane >= s.total)
+          *reinterpret_cast<float4*>(&sm.bias[ms][4 * lane]) =
+              make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+        if (p.causal && lane < kChunks && 8 * lane >= s.total) sm.meta[ms][lane] = 0u;
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.meta_full[ms]);
-
+      }
+    }
+  } else if (warp == 3) {
+    // ================================================================ V producer
+    if (T > 0) {
+      PlanCursor pc;
+      pc.init(csr + unit * p.n_k, n_ent, lane);
+      for (int t = 0; t < T; ++t) {
+        const int vs = t % VST;
+        const TileSeg s = pc.next(p, bhkv, lane);
         if (t >= VST) mbar_wait(&sm.v_empty[vs], ((t / VST) - 1) & 1);
-        if (lane == 0) mbar_arrive_expect_tx(&sm.v_full[vs], bytes);
+        if (lane == 0) mbar_arrive_expect_tx(&sm.v_full[vs], static_cast<uint32_t>(s.total) * D * 2);
         __syncwarp();
-        if (fits)
+        if (s.fits)
           for (int c = 0; c < D / 64; ++c)
-            tma_load_2d(&maps.v[h - 1], &sm.v_full[vs], sm.v[vs] + c * kTileRows * 128 + off * 128,
-                        c * 64, row);
-
-        e += nseg;
-        if (e - base >= 32) {  // advance the window (warp-uniform)
-          base += 32;
-          cur = nxt;
-          nxt = base + 32 + lane < n_ent ? plan[base + 32 + lane] : 0u;
-        }
+            tma_load_2d(&maps.v[s.h - 1], &sm.v_full[vs],
+                        sm.v[vs] + c * kTileRows * 128 + s.off * 128, c * 64, s.row);
       }
     }
   } else if (warp == 1) {
@@ -236,7 +270,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     if (lane == 0 && T > 0) {
       constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128, false, false);
       constexpr uint32_t idesc_o = umma_idesc_bf16(128, D, false, true);
-      const uint32_t q_base = smem_u32(sm.q), p_base = smem_u32(sm.p);
+      const uint32_t q_base = smem_u32(sm.q);
       auto issue_pv = [&](int u) {
         const int vs = u % VST;
         mbar_wait(&sm.v_full[vs], (u / VST) & 1);
@@ -245,9 +279,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         const uint32_t v_base = smem_u32(sm.v[vs]);
 #pragma unroll
         for (int kk = 0; kk < kTileRows / 16; ++kk) {
-          const uint64_t a = umma_desc_sw128(p_base + (kk >> 2) * kTileRows * 128 + (kk & 3) * 32, 16, 1024);
           const uint64_t bdesc = umma_desc_sw128(v_base + kk * 16 * 128, kTileRows * 128, 1024);
-          mma_bf16_ss(tmem + 256, a, bdesc, idesc_o, (u > 0 || kk > 0) ? 1u : 0u);
+          mma_bf16_ts(tmem + kTmemO, tmem + kTmemP + kk * 8, bdesc, idesc_o,
+                      (u > 0 || kk > 0) ? 1u : 0u);
         }
         mma_commit(&sm.v_empty[vs]);
         mma_commit(&sm.o_done);
@@ -265,7 +299,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           const uint32_t koff = (kk >> 2) * kTileRows * 128 + (kk & 3) * 32;
           const uint64_t a = umma_desc_sw128(q_base + koff, 16, 1024);
           const uint64_t bdesc = umma_desc_sw128(k_base + koff, 16, 1024);
-          mma_bf16_ss(tmem + sb * 128, a, bdesc, idesc_s, kk > 0 ? 1u : 0u);
+          mma_bf16_ss(tmem + kTmemS + sb * 128, a, bdesc, idesc_s, kk > 0 ? 1u : 0u);
         }
         mma_commit(&sm.k_empty[ks]);
         mma_commit(&sm.s_full[sb]);
@@ -280,51 +314,60 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     const int row = wq * 32 + lane;
     const uint32_t t_lane = tmem + (static_cast<uint32_t>(wq * 32) << 16);
     const int qpos = i * p.b_q + row;
-    const float scale = p.scale_log2;
-    const float2 scale2 = make_float2(scale, scale);
+    const float2 scale2 = make_float2(p.scale_log2, p.scale_log2);
     float m_run = -INFINITY, l_run = 0.f;
     for (int t = 0; t < T; ++t) {
       const int sb = t & 1, ms = t % kMetaRing;
       mbar_wait(&sm.s_full[sb], (t >> 1) & 1);
       tc_fence_after();
       uint32_t s[2][32];
-      tmem_ld32(t_lane + sb * 128 + wg * 64, s[0]);
-      tmem_ld32(t_lane + sb * 128 + wg * 64 + 32, s[1]);
+      tmem_ld32(t_lane + kTmemS + sb * 128 + wg * 64, s[0]);
+      tmem_ld32(t_lane + kTmemS + sb * 128 + wg * 64 + 32, s[1]);
       tmem_ld_wait(s[0]);
       tmem_ld_wait(s[1]);
       tc_fence_before();
       mbar_arrive(&sm.s_free[sb]);
 
+      // y = s * scale + bias_col  (bias: level-1 in log2 units; -inf on pad columns)
       mbar_wait(&sm.meta_full[ms], (t / kMetaRing) & 1);
-      uint32_t mw[8];
-      {
-        const uint4 w0 = *reinterpret_cast<const uint4*>(&sm.meta[ms][wg * 8]);
-        const uint4 w1 = *reinterpret_cast<const uint4*>(&sm.meta[ms][wg * 8 + 4]);
-        mw[0] = w0.x; mw[1] = w0.y; mw[2] = w0.z; mw[3] = w0.w;
-        mw[4] = w1.x; mw[5] = w1.y; mw[6] = w1.z; mw[7] = w1.w;
+      float y[64];
+      const float4* bias4 = reinterpret_cast<const float4*>(&sm.bias[ms][wg * 64]);
+#pragma unroll
+      for (int q4 = 0; q4 < 16; ++q4) {
+        const float4 bv = bias4[q4];
+        const float* x = reinterpret_cast<const float*>(&s[q4 >> 3][(q4 & 7) * 4]);
+        const float2 a = ffma2(make_float2(x[0], x[1]), scale2, make_float2(bv.x, bv.y));
+        const float2 c = ffma2(make_float2(x[2], x[3]), scale2, make_float2(bv.z, bv.w));
+        y[q4 * 4 + 0] = a.x;
+        y[q4 * 4 + 1] = a.y;
+        y[q4 * 4 + 2] = c.x;
+        y[q4 * 4 + 3] = c.y;
+      }
+      if (p.causal) {  // token-level mask on straddling level-1 chunks (attention.py:88-108)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint32_t w = sm.meta[ms][wg * 8 + c];
+          if (w & 1u) {
+            const int lim = qpos - static_cast<int>(w >> 1);  // key k visible iff k <= lim
+#pragma unroll
+            for (int e = 0; e < 8; ++e) y[c * 8 + e] = (e <= lim) ? y[c * 8 + e] : -INFINITY;
+          }
+        }
       }
       mbar_arrive(&sm.meta_empty[ms]);
 
-      // ---- row max over this half (chunk-wise; warp-uniform fast path for full chunks)
-      int nvc[8];
-      float mt = -INFINITY;
+      float mx0 = fmax3(y[0], y[1], y[2]), mx1 = fmax3(y[3], y[4], y[5]);
+      float mx2 = fmax3(y[6], y[7], y[8]), mx3 = fmax3(y[9], y[10], y[11]);
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const uint32_t w = mw[c];
-        const float* x = reinterpret_cast<const float*>(&s[c >> 2][(c & 3) * 8]);
-        int nv = static_cast<int>(w & 15u);
-        float mx;
-        if (nv == 8 && !(w & 256u)) {
-          mx = fmax3(fmax3(x[0], x[1], x[2]), fmax3(x[3], x[4], x[5]), fmaxf(x[6], x[7]));
-        } else {
-          if (w & 256u) nv = min(nv, max(qpos - static_cast<int>(w >> 9) + 1, 0));
-          mx = -INFINITY;
-#pragma unroll
-          for (int e = 0; e < 8; ++e) mx = (e < nv) ? fmaxf(mx, x[e]) : mx;
-        }
-        nvc[c] = nv;
-        mt = fmaxf(mt, fmaf(mx, scale, static_cast<float>((w >> 4) & 15u)));
+      for (int e = 12; e < 60; e += 8) {
+        mx0 = fmax3(mx0, y[e], y[e + 1]);
+        mx1 = fmax3(mx1, y[e + 2], y[e + 3]);
+        mx2 = fmax3(mx2, y[e + 4], y[e + 5]);
+        mx3 = fmax3(mx3, y[e + 6], y[e + 7]);
       }
+      mx0 = fmax3(mx0, y[60], y[61]);
+      mx1 = fmax3(mx1, y[62], y[63]);
+      float mt = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
       sm.red[t & 1][wg][row] = mt;
       named_bar_sync(1, kSoftmaxThreads);
       mt = fmaxf(sm.red[t & 1][0][row], sm.red[t & 1][1][row]);
@@ -337,58 +380,41 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         m_run = m_new;
       }
       const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
-      float2 lsum = make_float2(0.f, 0.f);
+      const float2 negm = make_float2(-m_use, -m_use);
+      float2 ls0 = make_float2(0.f, 0.f), ls1 = make_float2(0.f, 0.f);
       uint32_t pk[32];
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const uint32_t w = mw[c];
-        const float off = static_cast<float>((w >> 4) & 15u) - m_use;
-        const float2 off2 = make_float2(off, off);
-        const float* x = reinterpret_cast<const float*>(&s[c >> 2][(c & 3) * 8]);
-        const int nv = nvc[c];
-        if (nv == 8) {
-#pragma unroll
-          for (int e = 0; e < 8; e += 2) {
-            float2 y = ffma2(make_float2(x[e], x[e + 1]), scale2, off2);
-            y.x = ex2_approx(y.x);
-            y.y = ex2_approx(y.y);
-            lsum = fadd2(lsum, y);
-            pk[c * 4 + e / 2] = pack_bf16x2(y.x, y.y);
-          }
-        } else {
-#pragma unroll
-          for (int e = 0; e < 8; e += 2) {
-            float2 y = ffma2(make_float2(x[e], x[e + 1]), scale2, off2);
-            y.x = (e < nv) ? ex2_approx(y.x) : 0.f;
-            y.y = (e + 1 < nv) ? ex2_approx(y.y) : 0.f;
-            lsum = fadd2(lsum, y);
-            pk[c * 4 + e / 2] = pack_bf16x2(y.x, y.y);
-          }
-        }
+      for (int e = 0; e < 64; e += 4) {
+        float2 a = fadd2(make_float2(y[e], y[e + 1]), negm);
+        float2 c = fadd2(make_float2(y[e + 2], y[e + 3]), negm);
+        a.x = ex2_approx(a.x);
+        a.y = ex2_approx(a.y);
+        c.x = ex2_approx(c.x);
+        c.y = ex2_approx(c.y);
+        ls0 = fadd2(ls0, a);
+        ls1 = fadd2(ls1, c);
+        pk[e / 2] = pack_bf16x2(a.x, a.y);
+        pk[e / 2 + 1] = pack_bf16x2(c.x, c.y);
       }
-      l_run = l_run * alpha + (lsum.x + lsum.y);
+      const float2 ls = fadd2(ls0, ls1);
+      l_run = l_run * alpha + (ls.x + ls.y);
 
       const bool need = (t > 0) && __any_sync(0xffffffffu, resc);
-      if (t > 0) mbar_wait(&sm.o_done, (t - 1) & 1);  // PV(t-1) done: P tile free, O stable
+      if (t > 0) mbar_wait(&sm.o_done, (t - 1) & 1);  // PV(t-1) done: P columns free, O stable
+      tc_fence_after();
       if (need) {
-        tc_fence_after();
 #pragma unroll
         for (int c4 = 0; c4 < OC / 32; ++c4) {
           uint32_t o[32];
-          tmem_ld32(t_lane + 256 + wg * OC + c4 * 32, o);
+          tmem_ld32(t_lane + kTmemO + wg * OC + c4 * 32, o);
           tmem_ld_wait(o);
 #pragma unroll
           for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-          tmem_st32(t_lane + 256 + wg * OC + c4 * 32, o);
+          tmem_st32(t_lane + kTmemO + wg * OC + c4 * 32, o);
         }
-        tmem_st_wait();
       }
-      uint8_t* prow = sm.p + wg * kTileRows * 128 + row * 128;
-#pragma unroll
-      for (int cc = 0; cc < 8; ++cc)
-        *reinterpret_cast<uint4*>(prow + ((cc ^ (row & 7)) << 4)) =
-            make_uint4(pk[cc * 4], pk[cc * 4 + 1], pk[cc * 4 + 2], pk[cc * 4 + 3]);
-      fence_proxy_async_smem();
+      tmem_st32(t_lane + kTmemP + wg * 32, pk);  // P row half: keys [64 wg, 64 wg + 64)
+      tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.p_full);
@@ -411,7 +437,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     for (int c4 = 0; c4 < OC / 32; ++c4) {
       uint32_t o[32];
       if (T > 0) {
-        tmem_ld32(t_lane + 256 + wg * OC + c4 * 32, o);
+        tmem_ld32(t_lane + kTmemO + wg * OC + c4 * 32, o);
         tmem_ld_wait(o);
       } else {
 #pragma unroll
@@ -506,9 +532,6 @@ static int launch_attn(const void* q, const void* k, const void* v, const void* 
     const int L = b_k >> (h - 1);
     int sz = 8;
     while (sz < L) sz <<= 1;
-    p.rows_lvl[h - 1] = L;
-    p.slot_lvl[h - 1] = sz;
-    p.nh_lvl[h - 1] = n >> (h - 1);
     const uint64_t rows = static_cast<uint64_t>(bhkv * (n >> (h - 1)));
     const void* kb = h == 1 ? k : static_cast<const void*>(static_cast<const uint16_t*>(k_pyr) + off_elems);
     const void* vb = h == 1 ? v : static_cast<const void*>(static_cast<const uint16_t*>(v_pyr) + off_elems);
