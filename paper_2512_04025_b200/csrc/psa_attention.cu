@@ -38,6 +38,7 @@ constexpr int kSoftmaxWarps = 8;
 constexpr int kSoftmaxThreads = kSoftmaxWarps * 32;
 constexpr int kAttnThreads = 4 * 32 + kSoftmaxThreads;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+constexpr int kPolyFrom = 48;  // softmax columns [48, 64) of each warp use the FMA-pipe exp2
 // TMEM columns: S0 | S1 | O (D) | P (64 packed bf16x2 columns)
 constexpr uint32_t kTmemS = 0, kTmemO = 256, kTmemP = 384;
 
@@ -119,7 +120,7 @@ struct PlanCursor {
     s.nseg = __popc(__ballot_sync(0xffffffffu, s.fits));
     s.total = __shfl_sync(0xffffffffu, incl, s.nseg - 1);
     s.off = incl - s.sz;
-    s.row = static_cast<int>(bhkv * (p.n >> (s.h - 1)) + static_cast<int64_t>(s.j) * s.L);
+    s.row = static_cast<int>(bhkv) * static_cast<int>(p.n >> (s.h - 1)) + s.j * s.L;
     e += s.nseg;
     if (e - base >= 32) {  // advance the two-window cache (warp-uniform)
       base += 32;
@@ -199,7 +200,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   const uint32_t tmem = sm.tmem_base;
 
   if (warp == 0) {
-    // ================================================================ K producer (+ Q, bias)
+    // ================================================================ K producer (+ Q)
     if (T > 0) {
       if (lane == 0) {
         mbar_arrive_expect_tx(&sm.q_full, kTileRows * D * 2);
@@ -207,21 +208,30 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           tma_load_2d(&maps.q, &sm.q_full, sm.q + c * kTileRows * 128, c * 64,
                       static_cast<int>(q_row0));
       }
-      const int64_t q_lo = static_cast<int64_t>(i) * p.b_q;
       PlanCursor pc;
       pc.init(csr + unit * p.n_k, n_ent, lane);
       for (int t = 0; t < T; ++t) {
-        const int ks = t % KST, ms = t % kMetaRing;
+        const int ks = t % KST;
         const TileSeg s = pc.next(p, bhkv, lane);
-        const uint32_t bytes = static_cast<uint32_t>(s.total) * D * 2;
         if (t >= KST) mbar_wait(&sm.k_empty[ks], ((t / KST) - 1) & 1);
-        if (lane == 0) mbar_arrive_expect_tx(&sm.k_full[ks], bytes);
+        if (lane == 0) mbar_arrive_expect_tx(&sm.k_full[ks], static_cast<uint32_t>(s.total) * D * 2);
         __syncwarp();
         if (s.fits)
           for (int c = 0; c < D / 64; ++c)
             tma_load_2d(&maps.k[s.h - 1], &sm.k_full[ks],
                         sm.k[ks] + c * kTileRows * 128 + s.off * 128, c * 64, s.row);
-        // per-column bias (h-1 in log2 units, -inf on pad rows) and causal chunk meta
+      }
+    }
+  } else if (warp == 2) {
+    // ================================================================ bias/meta producer
+    // per KV column: level-1 (log2 units) or -inf on pad rows; causal: straddle flag + key pos
+    if (T > 0) {
+      const int64_t q_lo = static_cast<int64_t>(i) * p.b_q;
+      PlanCursor pc;
+      pc.init(csr + unit * p.n_k, n_ent, lane);
+      for (int t = 0; t < T; ++t) {
+        const int ms = t % kMetaRing;
+        const TileSeg s = pc.next(p, bhkv, lane);
         if (t >= kMetaRing) mbar_wait(&sm.meta_empty[ms], ((t / kMetaRing) - 1) & 1);
         if (s.fits) {
           const float bv = static_cast<float>(s.h - 1);
@@ -387,10 +397,15 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       for (int e = 0; e < 64; e += 4) {
         float2 a = fadd2(make_float2(y[e], y[e + 1]), negm);
         float2 c = fadd2(make_float2(y[e + 2], y[e + 3]), negm);
-        a.x = ex2_approx(a.x);
-        a.y = ex2_approx(a.y);
-        c.x = ex2_approx(c.x);
-        c.y = ex2_approx(c.y);
+        if (e >= kPolyFrom) {  // last quarter of the columns on the FMA pipe (MUFU offload)
+          a = ex2_poly2(a);
+          c = ex2_poly2(c);
+        } else {
+          a.x = ex2_approx(a.x);
+          a.y = ex2_approx(a.y);
+          c.x = ex2_approx(c.x);
+          c.y = ex2_approx(c.y);
+        }
         ls0 = fadd2(ls0, a);
         ls1 = fadd2(ls1, c);
         pk[e / 2] = pack_bf16x2(a.x, a.y);
