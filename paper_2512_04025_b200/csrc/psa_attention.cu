@@ -233,26 +233,30 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         const int ms = t % kMetaRing;
         const TileSeg s = pc.next(p, bhkv, lane);
         if (t >= kMetaRing) mbar_wait(&sm.meta_empty[ms], ((t / kMetaRing) - 1) & 1);
-        if (s.fits) {
-          const float bv = static_cast<float>(s.h - 1);
-          for (int c = 0; c < s.sz; c += 4) {
-            float4 w;
-            w.x = c + 0 < s.L ? bv : -INFINITY;
-            w.y = c + 1 < s.L ? bv : -INFINITY;
-            w.z = c + 2 < s.L ? bv : -INFINITY;
-            w.w = c + 3 < s.L ? bv : -INFINITY;
-            *reinterpret_cast<float4*>(&sm.bias[ms][s.off + c]) = w;
+        {  // lane l fills columns [4l, 4l+4): find the owning segment (offsets ascend)
+          int g = 0;
+          for (int q = 1; q < s.nseg; ++q)
+            if (__shfl_sync(0xffffffffu, s.off, q) <= 4 * lane) g = q;
+          const int goff = __shfl_sync(0xffffffffu, s.off, g);
+          const int gL = __shfl_sync(0xffffffffu, s.L, g);
+          const int gh = __shfl_sync(0xffffffffu, s.h, g);
+          const int r0 = 4 * lane - goff;  // row of column 4l inside its segment slot
+          const float bv = static_cast<float>(gh - 1);
+          float4 w = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+          if (4 * lane < s.total) {
+            w.x = r0 + 0 < gL ? bv : -INFINITY;
+            w.y = r0 + 1 < gL ? bv : -INFINITY;
+            w.z = r0 + 2 < gL ? bv : -INFINITY;
+            w.w = r0 + 3 < gL ? bv : -INFINITY;
           }
-          if (p.causal) {
-            const bool straddle = static_cast<int64_t>(s.j + 1) * p.b_k - 1 > q_lo;
-            for (int c = 0; c < s.sz / 8; ++c)
-              sm.meta[ms][s.off / 8 + c] =
-                  (straddle ? 1u : 0u) | (static_cast<uint32_t>(s.j * p.b_k + c * 8) << 1);
-          }
+          *reinterpret_cast<float4*>(&sm.bias[ms][4 * lane]) = w;
         }
-        if (4 * lane >= s.total)
-          *reinterpret_cast<float4*>(&sm.bias[ms][4 * lane]) =
-              make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+        if (p.causal && s.fits) {
+          const bool straddle = static_cast<int64_t>(s.j + 1) * p.b_k - 1 > q_lo;
+          for (int c = 0; c < s.sz / 8; ++c)
+            sm.meta[ms][s.off / 8 + c] =
+                (straddle ? 1u : 0u) | (static_cast<uint32_t>(s.j * p.b_k + c * 8) << 1);
+        }
         if (p.causal && lane < kChunks && 8 * lane >= s.total) sm.meta[ms][lane] = 0u;
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.meta_full[ms]);
@@ -277,24 +281,26 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     }
   } else if (warp == 1) {
     // ================================================================ MMA issuer
-    if (lane == 0 && T > 0) {
+    // warp-uniform loop; one elected lane issues the tcgen05 instructions
+    if (T > 0) {
       constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128, false, false);
       constexpr uint32_t idesc_o = umma_idesc_bf16(128, D, false, true);
-      const uint32_t q_base = smem_u32(sm.q);
+      const uint64_t q_desc0 = umma_desc_sw128(smem_u32(sm.q), 16, 1024);
       auto issue_pv = [&](int u) {
         const int vs = u % VST;
         mbar_wait(&sm.v_full[vs], (u / VST) & 1);
         mbar_wait(&sm.p_full, u & 1);
         tc_fence_after();
-        const uint32_t v_base = smem_u32(sm.v[vs]);
+        const uint64_t v_desc0 = umma_desc_sw128(smem_u32(sm.v[vs]), kTileRows * 128, 1024);
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < kTileRows / 16; ++kk) {
-          const uint64_t bdesc = umma_desc_sw128(v_base + kk * 16 * 128, kTileRows * 128, 1024);
-          mma_bf16_ts(tmem + kTmemO, tmem + kTmemP + kk * 8, bdesc, idesc_o,
-                      (u > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < kTileRows / 16; ++kk)
+            mma_bf16_ts(tmem + kTmemO, tmem + kTmemP + kk * 8, v_desc0 + ((kk * 16 * 128) >> 4),
+                        idesc_o, (u > 0 || kk > 0) ? 1u : 0u);
+          mma_commit(&sm.v_empty[vs]);
+          mma_commit(&sm.o_done);
         }
-        mma_commit(&sm.v_empty[vs]);
-        mma_commit(&sm.o_done);
+        __syncwarp();
       };
       mbar_wait(&sm.q_full, 0);
       tc_fence_after();
@@ -303,16 +309,18 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         mbar_wait(&sm.k_full[ks], (t / KST) & 1);
         if (t >= 2) mbar_wait(&sm.s_free[sb], ((t >> 1) - 1) & 1);
         tc_fence_after();
-        const uint32_t k_base = smem_u32(sm.k[ks]);
+        const uint64_t k_desc0 = umma_desc_sw128(smem_u32(sm.k[ks]), 16, 1024);
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t koff = (kk >> 2) * kTileRows * 128 + (kk & 3) * 32;
-          const uint64_t a = umma_desc_sw128(q_base + koff, 16, 1024);
-          const uint64_t bdesc = umma_desc_sw128(k_base + koff, 16, 1024);
-          mma_bf16_ss(tmem + kTmemS + sb * 128, a, bdesc, idesc_s, kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t koff = ((kk >> 2) * kTileRows * 128 + (kk & 3) * 32) >> 4;
+            mma_bf16_ss(tmem + kTmemS + sb * 128, q_desc0 + koff, k_desc0 + koff, idesc_s,
+                        kk > 0 ? 1u : 0u);
+          }
+          mma_commit(&sm.k_empty[ks]);
+          mma_commit(&sm.s_full[sb]);
         }
-        mma_commit(&sm.k_empty[ks]);
-        mma_commit(&sm.s_full[sb]);
+        __syncwarp();
         if (t >= 1) issue_pv(t - 1);
       }
       issue_pv(T - 1);
