@@ -62,7 +62,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
@@ -146,7 +146,8 @@ def _cpu_worker(args):
     # psa_streaming's per-query-block loop restricted to the first n_blocks query blocks
     _stream_blocks(orc, q, kl, vl, m[:n_blocks], lay, n_blocks, causal)
     t2 = time.perf_counter()
-    return t1 - t0, t2 - t1
+    counts = [int((m == h).sum()) for h in range(lay.levels + 1)]
+    return t1 - t0, t2 - t1, counts
 
 
 def _stream_blocks(orc, q, kl, vl, mask, lay, n_blocks, causal):
@@ -178,10 +179,12 @@ def _stream_blocks(orc, q, kl, vl, mask, lay, n_blocks, causal):
             m_run = m_new
 
 
-def cpu_baseline(cfg, q_dev, k_dev, v_dev, flops_total, n_blocks=None, max_workers=None):
+def cpu_baseline(cfg, q_dev, k_dev, v_dev, n_blocks=None, max_workers=None):
     """Run the oracle on min(cores, heads) heads in parallel processes (1 BLAS thread each), each
     on a bounded sample (full pyramid/importance/assignment + n_blocks query blocks of the
-    streaming executor); extrapolate to the whole workload."""
+    streaming executor); extrapolate to the whole workload. The executed FLOPs come from the
+    oracle's own level maps (mean over the sampled heads x all heads), so this arm never touches
+    the GPU path. q_dev/k_dev/v_dev hold (at least) heads 0..min(cores, heads)-1."""
     import multiprocessing as mp
 
     import torch
@@ -191,7 +194,8 @@ def cpu_baseline(cfg, q_dev, k_dev, v_dev, flops_total, n_blocks=None, max_worke
     N, bq = cfg["N"], cfg["b_q"]
     n_q = N // bq
     if n_blocks is None:
-        n_blocks = max(2, min(n_q, int(4.0e6 / max(N, 1))))  # ~10-20 s per worker at cfg3
+        n_blocks = int(4.0e6 / max(N, 1))  # ~10-20 s per worker at cfg3
+    n_blocks = max(1, min(n_q, n_blocks))
     lay_t = (N, cfg["d"], bq, cfg["b_k"], cfg["levels"])
     group = cfg["Hq"] // cfg["Hkv"]
     jobs = []
@@ -219,9 +223,11 @@ def cpu_baseline(cfg, q_dev, k_dev, v_dev, flops_total, n_blocks=None, max_worke
                 os.environ[k_] = v_
     pre = statistics.mean(r[0] for r in res)
     att = statistics.mean(r[1] for r in res)
+    flops_head = statistics.mean(flops_from_counts(r[2], cfg) for r in res)
     per_head = pre + att * (n_q / n_blocks)
     total_heads = cfg["B"] * cfg["Hq"]
     est_time = per_head * math.ceil(total_heads / workers)
+    flops_total = flops_head * total_heads
     return {
         "value": flops_total / est_time / 1e12, "unit": "TFLOP/s", "cores": workers,
         "kind": "port",
@@ -230,6 +236,7 @@ def cpu_baseline(cfg, q_dev, k_dev, v_dev, flops_total, n_blocks=None, max_worke
                    f"({pre:.2f} s) + psa_streaming on {n_blocks}/{n_q} query blocks "
                    f"({att:.2f} s); extrapolated to {total_heads} heads = {est_time:.1f} s/forward"),
         "extrapolated_s_per_forward": est_time, "sample_wall_s": wall,
+        "executed_tflop_per_forward": flops_total / 1e12,
     }
 
 
@@ -237,7 +244,7 @@ def cpu_baseline(cfg, q_dev, k_dev, v_dev, flops_total, n_blocks=None, max_worke
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
@@ -363,7 +370,7 @@ def main():
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         try:
-            cpu = cpu_baseline(cfg, q, k, v, flops_all)
+            cpu = cpu_baseline(cfg, q, k, v)
         except Exception as exc:  # the baseline must not kill the GPU line
             cpu = {"value": None, "unit": "TFLOP/s", "cores": 0, "kind": "port",
                    "sample": f"failed: {exc!r}"}
@@ -397,61 +404,63 @@ def main():
 
 
 def run_e2e(psa, rc, q, k, v, args, stream, flops_all, world, device):
-    """Same metric through psa.psa_attention with pinned host inputs: H2D of Q/K/V and D2H of O
-    are inside every timed step."""
+    """Same metric through the public call a user makes with host data: psa.psa_attention on
+    pinned host Q/K/V returns O and lse in pinned host memory. Every timed step includes the H2D
+    of Q/K/V and the D2H of O/lse (the call pipelines head groups over copy-in / compute /
+    copy-out streams, staging.py)."""
     import torch
     import torch.distributed as dist
     hq, hk, hv = (x.cpu().pin_memory() for x in (q, k, v))
     out_h = torch.empty(q.shape, dtype=torch.bfloat16).pin_memory()
+    lse_h = torch.empty(q.shape[:-1], dtype=torch.float32).pin_memory()
 
     def one():
-        qd = hq.to(device, non_blocking=True)
-        kd = hk.to(device, non_blocking=True)
-        vd = hv.to(device, non_blocking=True)
-        res = psa.psa_attention(qd, kd, vd, rc)
-        out_h.copy_(res.out, non_blocking=True)
+        return psa.psa_attention(hq, hk, hv, rc, device=device, out=out_h, lse=lse_h)
 
     for _ in range(2):
         one()
     torch.cuda.synchronize()
-    steps = max(1, min(args.steps, 3))
+    steps = max(1, min(args.steps, 5))
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
+    t0 = time.perf_counter()
     a.record(stream)
     for _ in range(steps):
         one()
     b.record(stream)
     torch.cuda.synchronize()
+    wall = (time.perf_counter() - t0) * 1e3 / steps
     ms = a.elapsed_time(b) / steps
     t = torch.tensor([ms], dtype=torch.float64, device=device)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t[0])
     return {"value": round(flops_all / (ms * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
-            "ms_per_step": round(ms, 3), "steps": steps,
+            "ms_per_step": round(ms, 3), "host_wall_ms_per_step": round(wall, 3), "steps": steps,
+            "api": "psa_attention(pinned host q, k, v) -> host out, lse (staged H2D/compute/D2H)",
             "h2d_bytes_per_step": int(sum(x.numel() * x.element_size() for x in (hq, hk, hv))),
-            "d2h_bytes_per_step": int(out_h.numel() * out_h.element_size())}
+            "d2h_bytes_per_step": int(out_h.numel() * out_h.element_size()
+                                      + lse_h.numel() * lse_h.element_size())}
 
 
 def main_reference(args, cfg, rank, world, device):
-    """--impl reference: the reference path's CPU implementation (oracle port, numpy fp64) on the
-    host cores, same config/metric/unit; rank 0 only."""
-    import torch
+    """--impl reference: the reference path's CPU implementation (the oracle port, numpy fp64) on
+    the host cores, same config/metric/unit; rank 0 only. Nothing from the GPU package runs here:
+    inputs are synthesised with torch's RNG (on the GPU when present, the same per-head streams as
+    our arm) and the executed FLOPs come from the oracle's own level maps."""
     if rank != 0:
         return
-    import paper_2512_04025_b200 as psa  # only to size the workload's executed FLOPs
-    heads = list(range(cfg["Hq"]))
-    kvh = list(range(cfg["Hkv"]))
-    q, k, v = make_inputs(cfg, heads, kvh, device)
-    rc = run_config(cfg)
-    res = psa.psa_attention(q, k, v, rc)
-    counts = res.plan.level_counts.cpu().tolist()
-    flops = flops_from_counts(counts, cfg)
-    vals = []
-    last = None
+    import torch
+    cores = os.cpu_count() or 1
+    heads = list(range(min(cores, cfg["Hq"])))
+    group = cfg["Hq"] // cfg["Hkv"]
+    kvh = sorted({h // group for h in heads})
+    gen_dev = device if torch.cuda.is_available() else torch.device("cpu")
+    q, k, v = make_inputs(cfg, heads, kvh, gen_dev)
+    vals, last = [], None
     for s in range(max(args.warmup, 0) + args.steps):
-        last = cpu_baseline(cfg, q, k, v, flops, n_blocks=max(2, int(1.0e6 / cfg["N"])))
+        last = cpu_baseline(cfg, q, k, v, n_blocks=max(2, int(1.0e6 / cfg["N"])))
         if s >= args.warmup:
             vals.append(last["value"])
     value = statistics.mean(vals)
@@ -460,7 +469,8 @@ def main_reference(args, cfg, rank, world, device):
         "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": last["extrapolated_s_per_forward"] * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic N(0,1) bf16-rounded Q/K/V", "config": {"workload": f"{args.config}: {cfg['desc']}"},
+        "data": "synthetic N(0,1) bf16-rounded Q/K/V", "config": {"workload": f"{args.config}: {cfg['desc']}",
+                                                                  "executed_tflop_per_step": last["executed_tflop_per_forward"]},
         "cpu_baseline": {k_: last[k_] for k_ in ("kind", "cores", "sample")} | {"value": value, "unit": "TFLOP/s"},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }

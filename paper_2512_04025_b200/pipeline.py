@@ -163,8 +163,10 @@ def _mask_rule(cfg: RunConfig, levels: int):
     return "quantile", rule
 
 
-def psa_forward_4d(q4, k4, v4, cfg: RunConfig, keep_scores: bool = False) -> PSAResult:
-    """Fused PSA forward on contiguous bf16 [B, H, N, d] device tensors."""
+def psa_forward_4d(q4, k4, v4, cfg: RunConfig, keep_scores: bool = False,
+                   out: torch.Tensor | None = None, lse: torch.Tensor | None = None) -> PSAResult:
+    """Fused PSA forward on contiguous bf16 [B, H, N, d] device tensors (``out``/``lse``:
+    optional preallocated device outputs)."""
     lay = cfg.layout()
     lay.check_gpu()
     if cfg.grid is not None:
@@ -185,9 +187,22 @@ def psa_forward_4d(q4, k4, v4, cfg: RunConfig, keep_scores: bool = False) -> PSA
         caps = _stage("similarity-cap", similarity_caps, k4, lay, SimThresholds(cfg.sim_thresholds))
     plan = _stage("mask", assign_levels_device, scores, mode=mode, rule=rule, levels=lay.levels,
                   b_q=lay.q_block, b_k=lay.k_block, hkv=Hkv, caps=caps, causal=cfg.causal)
-    out, lse, skipped = _stage("executor", attention_forward, q4, pyr, plan, cfg.causal)
+    out, lse, skipped = _stage("executor", attention_forward, q4, pyr, plan, cfg.causal, out, lse)
     return PSAResult(out=out, lse=lse, plan=plan, skipped=skipped,
                      scores=scores if keep_scores else None, pyramid=pyr)
+
+
+def resolve_config(cfg: RunConfig | None, n: int, d: int, overrides: dict) -> RunConfig:
+    """RunConfig from an explicit config and/or keyword overrides; n, d from the tensors."""
+    if cfg is None:
+        data = {"n": n, "d": d, "tile_len": 128}
+        data.update(overrides)
+        cfg = RunConfig.from_dict(data)
+    elif overrides:
+        cfg = RunConfig.from_dict({**cfg.to_dict(), **overrides})
+    if (cfg.n, cfg.d) != (n, d):
+        raise ValidationError(f"tensor shape {(n, d)} does not match config ({cfg.n}, {cfg.d})")
+    return cfg
 
 
 def psa_attention(q, k, v, cfg: RunConfig | None = None, *, keep_scores: bool = False,
@@ -197,22 +212,22 @@ def psa_attention(q, k, v, cfg: RunConfig | None = None, *, keep_scores: bool = 
     ``q``: (n, d), (Hq, n, d) or (B, Hq, n, d); ``k``/``v``: same with Hkv heads (Hq % Hkv == 0).
     Configuration by ``RunConfig`` or its keys as keyword arguments (n and d are taken from
     the tensors; tile_len defaults to 128).
+
+    CUDA tensors run in place on their device. Host tensors (ideally pinned) go through
+    ``staging.psa_attention_staged``: head groups are copied in, computed and copied back on
+    three overlapped streams, and the result lives in host memory (the reference's
+    arrays-in/arrays-out contract); the compute is the same sm_100a path, never a CPU one.
     """
+    if isinstance(q, torch.Tensor) and not q.is_cuda:
+        from .staging import psa_attention_staged  # host tensors: pipelined staging onto the GPU
+        return psa_attention_staged(q, k, v, cfg, keep_scores=keep_scores, **overrides)
     q4, lead = as_bhnd(q, "Q")
     k4, _ = as_bhnd(k, "K", q4.shape[2], q4.shape[3])
     v4, _ = as_bhnd(v, "V", q4.shape[2], q4.shape[3])
     if k4.shape != v4.shape or k4.shape[0] != q4.shape[0]:
         raise ValidationError(f"Q/K/V shapes differ: {tuple(q4.shape)}/{tuple(k4.shape)}/"
                               f"{tuple(v4.shape)}")
-    if cfg is None:
-        data = {"n": q4.shape[2], "d": q4.shape[3], "tile_len": 128}
-        data.update(overrides)
-        cfg = RunConfig.from_dict(data)
-    elif overrides:
-        cfg = RunConfig.from_dict({**cfg.to_dict(), **overrides})
-    if (cfg.n, cfg.d) != (q4.shape[2], q4.shape[3]):
-        raise ValidationError(f"tensor shape {tuple(q4.shape[2:])} does not match config "
-                              f"({cfg.n}, {cfg.d})")
+    cfg = resolve_config(cfg, q4.shape[2], q4.shape[3], overrides)
     res = psa_forward_4d(q4, k4, v4, cfg, keep_scores=keep_scores)
     res.out = restore(res.out, lead)
     res.lse = res.lse.reshape(lead + (cfg.n,))

@@ -284,3 +284,28 @@ def test_pipeline_level_map_and_output(case):
         mism += int((lm[h] != r["mask"]).sum())
         assert rel_l2(out[h], r["out"]) <= 5e-3, h
     assert mism == 0
+
+
+# ------------------------------------------------------------------ host staging (e2e API)
+@pytest.mark.parametrize("hq,hkv,causal,per_group", [(6, 6, False, 2), (8, 2, True, 1),
+                                                      (3, 3, False, None)])
+def test_staged_host_path_bit_identical(hq, hkv, causal, per_group):
+    """psa_attention on host tensors (pipelined H2D/compute/D2H over head groups) returns exactly
+    the device path's O, lse, level map and counts."""
+    psa = _psa()
+    n, d, b = 2048, 128, 64
+    q, k, v = gaussian_qkv(11, hq, n, d, kv_heads=hkv)
+    qh, kh, vh = (torch.from_numpy(x).to(torch.bfloat16).unsqueeze(0) for x in (q, k, v))
+    kw = dict(b_q=b, b_k=b, levels=4, estimator="sampled-max", s_q=8, s_k=8, seed=0,
+              mask="threshold", thresholds=TAUS_CFG1, causal=causal)
+    dev = psa.psa_attention(qh.cuda(), kh.cuda(), vh.cuda(), **kw)
+    torch.cuda.synchronize()
+    host = psa.psa_attention(qh.pin_memory(), kh.pin_memory(), vh.pin_memory(),
+                             kv_heads_per_group=per_group, keep_level_map=True, **kw)
+    assert not host.out.is_cuda and host.out.shape == qh.shape
+    assert torch.equal(host.out.view(torch.int16), dev.out.cpu().view(torch.int16))
+    assert torch.equal(host.lse, dev.lse.cpu())
+    assert torch.equal(host.level_map, dev.level_map.cpu())
+    assert host.level_counts == dev.plan.level_counts.cpu().tolist()
+    assert host.skipped_rows() == dev.skipped_rows()
+    assert host.sparsity().rho_bar == dev.sparsity().rho_bar
