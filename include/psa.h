@@ -57,7 +57,7 @@ int psa_pyramid_build(const void* k, const void* v, int64_t bh, int64_t n, int d
 
 /*
  * Similarity cap (Alg. 3).  Replaces level_cap_from_similarity / _strided_block_similarity
- * (pkg/src/pyrattn/mask.py:347-399).  sim_taus: HOST array of levels-1 thresholds.
+ * (pkg/src/pyrattn/mask.py:182-234).  sim_taus: HOST array of levels-1 thresholds.
  * caps: int8 [bh, n/b_k], each in 1..levels.
  */
 int psa_similarity_caps(const void* k, int64_t bh, int64_t n, int d, int b_k, int levels,
@@ -80,13 +80,13 @@ int psa_importance_sampled(const void* q, const void* k, int64_t batch, int hq, 
 
 /*
  * K3 — level assignment + compact plan.  Replaces assign_threshold / binary_mask /
- * assign_quantile (pkg/src/pyrattn/mask.py:293-344), combine_mask (mask.py:402-412) and
- * causal_premask (mask.py:489-514), and emits the selected-block lists the attention
+ * assign_quantile (pkg/src/pyrattn/mask.py:128-179), combine_mask (mask.py:237-247) and
+ * causal_premask (mask.py:324-349), and emits the selected-block lists the attention
  * kernel walks.
  * mode 0 (threshold): taus = HOST array of n_cuts thresholds (Alg. 2: stable descending sort,
  *   exactly-rounded row total, sequential Neumaier cumulative sum, searchsorted 'left').
  * mode 1 (quantile) : counts = HOST array of n_cuts cumulative rank counts
- *   (mask.py:326-329 computed on the host exactly as the reference does).
+ *   (mask.py:161-164 computed on the host exactly as the reference does).
  * caps: optional int8 [batch*hkv, n_k]; causal: apply the causal pre-pass.
  * Outputs: level_map int8 [batch*hq, n_q, n_k];
  *   plan_csr uint16 [batch*hq*n_q, n_k]: per (head, query block) the selected blocks as

@@ -111,12 +111,12 @@ def importance_antidiagonal(q, k, lay, stride):
 
 # --------------------------------------------------------------------------- mask
 def descending_order(s):
-    """mask.py:272-274 — stable argsort of -s."""
+    """mask.py:107-109 — stable argsort of -s."""
     return np.argsort(-s, axis=1, kind="stable")
 
 
 def neumaier_cumsum(vec):
-    """mask.py:277-290 — sequential Neumaier running sums, out[i] = total + comp."""
+    """mask.py:112-125 — sequential Neumaier running sums, out[i] = total + comp."""
     out = np.empty_like(vec)
     total = comp = 0.0
     for i, x in enumerate(vec):
@@ -128,7 +128,7 @@ def neumaier_cumsum(vec):
 
 
 def assign_threshold(scores, taus):
-    """mask.py:293-316 (Alg. 2)."""
+    """mask.py:128-151 (Alg. 2)."""
     s = np.asarray(scores, np.float64)
     taus = np.asarray(taus, np.float64)
     n_q, n_k = s.shape
@@ -145,18 +145,18 @@ def assign_threshold(scores, taus):
 
 
 def binary_mask(scores, tau):
-    """mask.py:319-323."""
+    """mask.py:154-158."""
     return assign_threshold(scores, (tau,))
 
 
 def fraction_counts(points, n_k):
-    """mask.py:326-329."""
+    """mask.py:161-164."""
     c = [min(n_k, int(math.floor(p * n_k + 0.5))) for p in points]
     return np.maximum.accumulate(np.asarray(c, dtype=np.int64))
 
 
 def assign_quantile(scores, points):
-    """mask.py:332-344."""
+    """mask.py:167-179."""
     s = np.asarray(scores, np.float64)
     n_q, n_k = s.shape
     counts = fraction_counts(points, n_k)
@@ -176,7 +176,7 @@ PRESETS = {
 
 
 def strided_block_similarity(block, stride):
-    """mask.py:347-360 — mean clipped cosine of row pairs `stride` apart; None if none."""
+    """mask.py:182-195 — mean clipped cosine of row pairs `stride` apart; None if none."""
     if block.shape[0] <= stride:
         return None
     a, b = block[:-stride], block[stride:]
@@ -189,7 +189,7 @@ def strided_block_similarity(block, stride):
 
 
 def level_caps(k, lay, sim_taus):
-    """mask.py:363-399 — caps start at 1, max over levels whose similarity > tau (strict)."""
+    """mask.py:198-234 — caps start at 1, max over levels whose similarity > tau (strict)."""
     caps = np.ones(lay.n_k, dtype=np.int64)
     for j in range(lay.n_k):
         blk = k[j * lay.k_block:(j + 1) * lay.k_block]
@@ -201,12 +201,12 @@ def level_caps(k, lay, sim_taus):
 
 
 def combine_mask(mask, caps):
-    """mask.py:402-412."""
+    """mask.py:237-247."""
     return np.minimum(np.asarray(mask, np.int64), np.asarray(caps, np.int64)[None, :])
 
 
 def causal_premask(mask, lay):
-    """mask.py:489-514."""
+    """mask.py:324-349."""
     m = np.asarray(mask, np.int64).copy()
     i = np.arange(lay.n_q)[:, None]
     j = np.arange(lay.n_k)[None, :]
@@ -218,7 +218,7 @@ def causal_premask(mask, lay):
 
 
 def report_from_counts(counts, total):
-    """mask.py:443-465 — exact rationals rounded once."""
+    """mask.py:278-300 — exact rationals rounded once."""
     counts = [int(c) for c in counts]
     rho = sum((Fraction(counts[h], total) * Fraction(1, 1 << (h - 1))
                for h in range(1, len(counts))), Fraction(0))
@@ -228,7 +228,7 @@ def report_from_counts(counts, total):
 
 
 def sparsity_report(mask, levels):
-    """mask.py:468-486."""
+    """mask.py:303-321."""
     m = np.asarray(mask, np.int64)
     return report_from_counts([int((m == h).sum()) for h in range(levels + 1)], m.size)
 

@@ -1,14 +1,14 @@
 // K3: multi-level mask assignment + compact per-query-block plan.
 //
 // Reference semantics (pkg/src/pyrattn/mask.py):
-//   _descending_order      :272-274  stable argsort of -s (ties -> ascending block index)
-//   _compensated_cumsum    :277-290  sequential Neumaier, out[i] = total + comp
-//   assign_threshold       :293-316  row/fsum(row) (uniform 1/n_k if the total is 0), clip 1.0,
+//   _descending_order      :107-109  stable argsort of -s (ties -> ascending block index)
+//   _compensated_cumsum    :112-125  sequential Neumaier, out[i] = total + comp
+//   assign_threshold       :128-151  row/fsum(row) (uniform 1/n_k if the total is 0), clip 1.0,
 //                                    searchsorted(taus, cum, 'left') -> level t+1, 0 past tau_H
-//   binary_mask            :319-323  threshold with a single tau
-//   assign_quantile        :332-344  rank levels via searchsorted(counts, rank, 'right')
-//   combine_mask           :402-412  min(M, caps[j])
-//   causal_premask         :489-514  future -> 0, straddling -> 1, visible -> keep
+//   binary_mask            :154-158  threshold with a single tau
+//   assign_quantile        :167-179  rank levels via searchsorted(counts, rank, 'right')
+//   combine_mask           :237-247  min(M, caps[j])
+//   causal_premask         :324-349  future -> 0, straddling -> 1, visible -> keep
 //
 // One CTA (128 threads) per (head, query block) row. The sort is a bitonic network in shared
 // memory; the row total is computed EXACTLY (a 256-bit fixed-point superaccumulator reduced

@@ -5,8 +5,7 @@
 //   build_pyramid / _pool_stack / mean_pool_rows   pkg/src/pyrattn/blocks.py:86-109,
 //                                                  pkg/src/pyrattn/linalg.py:46-58
 //   level_cap_from_similarity / _strided_block_similarity
-//                                                  pkg/src/pyrattn/mask.py:182-234 (file
-//                                                  lines 347-399 in the shipped source)
+//                                                  pkg/src/pyrattn/mask.py:182-234
 //
 // Pooling is a dyadic tree of 0.5*(a+b) over raw rows; because b_k is a multiple of
 // 2^(H-1) and blocks start at multiples of b_k, level-h row t of the flattened

@@ -136,7 +136,7 @@ class QuantileCutpoints:
 
     def counts(self, n_k: int) -> list:
         """Cumulative rank counts: floor(p*n_k + 0.5) clamped to n_k, running max
-        (the reference's _fraction_counts, mask.py:326-329)."""
+        (the reference's _fraction_counts, mask.py:161-164)."""
         out, run = [], 0
         for p in self.points:
             c = min(n_k, int(math.floor(p * n_k + 0.5)))

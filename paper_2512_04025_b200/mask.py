@@ -1,9 +1,9 @@
 """Multi-level mask generation (K3), the compact plan, and budget accounting.
 
-Drop-ins for pkg/src/pyrattn/mask.py (shipped file lines):
-  assign_threshold :293-316, binary_mask :319-323, assign_quantile :332-344,
-  combine_mask :402-412, causal_premask :489-514,
-  SparsityReport / report_from_counts / sparsity_report :415-486.
+Drop-ins for pkg/src/pyrattn/mask.py :
+  assign_threshold :128-151, binary_mask :154-158, assign_quantile :167-179,
+  combine_mask :237-247, causal_premask :324-349,
+  SparsityReport / report_from_counts / sparsity_report :250-321.
 Level assignment and plan emission run in libpsa (psa_assign_levels); the report is exact
 rational arithmetic on the host from device-side level counts, as in the reference.
 """
@@ -122,28 +122,28 @@ def _check_scores(scores) -> tuple:
 
 
 def assign_threshold(scores, thresholds: LevelThresholds) -> torch.Tensor:
-    """Alg. 2 level assignment (mask.py:293-316); int64, same shape as ``scores``."""
+    """Alg. 2 level assignment (mask.py:128-151); int64, same shape as ``scores``."""
     s4, lead = _check_scores(scores)
     plan = assign_levels_device(s4, mode="threshold", rule=thresholds, levels=len(thresholds))
     return plan.level_map.to(torch.int64).reshape(lead + tuple(s4.shape[2:]))
 
 
 def binary_mask(scores, tau: float) -> torch.Tensor:
-    """0/1 keep/drop mask (mask.py:319-323)."""
+    """0/1 keep/drop mask (mask.py:154-158)."""
     if not 0.0 <= tau <= 1.0:
         raise ValidationError(f"tau must lie in [0, 1], got {tau}")
     return assign_threshold(scores, LevelThresholds((tau,)))
 
 
 def assign_quantile(scores, cutpoints: QuantileCutpoints) -> torch.Tensor:
-    """Rank-fraction level assignment (mask.py:332-344); int64."""
+    """Rank-fraction level assignment (mask.py:167-179); int64."""
     s4, lead = _check_scores(scores)
     plan = assign_levels_device(s4, mode="quantile", rule=cutpoints, levels=len(cutpoints))
     return plan.level_map.to(torch.int64).reshape(lead + tuple(s4.shape[2:]))
 
 
 def combine_mask(mask, caps) -> torch.Tensor:
-    """min(M, caps[j]) with zeros kept (mask.py:402-412). Elementwise on the device."""
+    """min(M, caps[j]) with zeros kept (mask.py:237-247). Elementwise on the device."""
     require_cuda(mask, "mask")
     require_cuda(caps, "caps")
     m = mask.to(torch.int64)
@@ -156,7 +156,7 @@ def combine_mask(mask, caps) -> torch.Tensor:
 
 
 def causal_premask(mask, layout: BlockLayout) -> torch.Tensor:
-    """Causal pre-pass (mask.py:489-514): future -> 0, straddling -> 1, visible -> keep."""
+    """Causal pre-pass (mask.py:324-349): future -> 0, straddling -> 1, visible -> keep."""
     require_cuda(mask, "mask")
     m = mask.to(torch.int64)
     if tuple(m.shape[-2:]) != (layout.n_q, layout.n_k):
@@ -207,7 +207,7 @@ def report_from_counts(level_counts, total: int) -> SparsityReport:
 
 
 def sparsity_report(mask, levels: int | None = None) -> SparsityReport:
-    """Budget, sparsity and coverage of a level map (mask.py:468-486)."""
+    """Budget, sparsity and coverage of a level map (mask.py:303-321)."""
     m = mask.to(torch.int64) if isinstance(mask, torch.Tensor) else torch.as_tensor(mask)
     if m.ndim < 2 or m.numel() == 0:
         raise ValidationError("mask must be a non-empty 2D integer array")

@@ -1,7 +1,7 @@
 """Pooled K/V pyramid (K1) and the similarity cap, on the GPU.
 
 Drop-in for pkg/src/pyrattn/blocks.py:67-109 (PyramidKV, build_pyramid) and
-pkg/src/pyrattn/mask.py:363-399 (level_cap_from_similarity). The pyramid lives in HBM as one
+pkg/src/pyrattn/mask.py:198-234 (level_cap_from_similarity). The pyramid lives in HBM as one
 bf16 buffer per tensor holding levels 2..H back to back ([B, Hkv, N >> (h-1), d] each);
 level 1 is the caller's K/V (never copied).
 """
@@ -118,7 +118,7 @@ def similarity_caps(k4: torch.Tensor, layout: BlockLayout, sim: SimThresholds) -
 
 def level_cap_from_similarity(source, sim_thresholds: SimThresholds,
                               layout: BlockLayout | None = None) -> torch.Tensor:
-    """Per-KV-block maximum admissible level (mask.py:363-399), int64.
+    """Per-KV-block maximum admissible level (mask.py:198-234), int64.
 
     ``source`` is a PyramidKV or a raw key tensor with an explicit layout. Returns (n_k,) for a
     single head input, else [..., n_k] following the input's leading dims.
