@@ -79,6 +79,20 @@ int psa_importance_sampled(const void* q, const void* k, int64_t batch, int hq, 
                            double* scores, void* workspace, void* stream);
 
 /*
+ * K2b — antidiagonal importance.  Replaces importance_antidiagonal
+ * (pkg/src/pyrattn/importance.py:97-132).  Query row p of a block reads the keys whose in-block
+ * column c has (p + c) % stride == 0 (antidiagonal_selection, importance.py:88-94); logits are
+ * fp64 dot products (exact for bf16 inputs) times fl(1/sqrt(d)); row softmax over all picks,
+ * probability mass per KV block, mean over the query block's rows.
+ * Constraints: stride divides b_k, b_k / stride <= 64.  scores: fp64 [batch*hq, n_q, n_k].
+ * workspace: psa_antidiag_workspace_bytes(batch*hq, n, b_k, stride) bytes (0 = invalid).
+ */
+size_t psa_antidiag_workspace_bytes(int64_t bhq, int64_t n, int b_k, int stride);
+int psa_importance_antidiagonal(const void* q, const void* k, int64_t batch, int hq, int hkv,
+                                int64_t n, int d, int b_q, int b_k, int stride, double* scores,
+                                void* workspace, void* stream);
+
+/*
  * K3 — level assignment + compact plan.  Replaces assign_threshold / binary_mask /
  * assign_quantile (pkg/src/pyrattn/mask.py:128-179), combine_mask (mask.py:237-247) and
  * causal_premask (mask.py:324-349), and emits the selected-block lists the attention

@@ -9,7 +9,8 @@ no CPU fallback: calling with CPU tensors or without the built library raises.
 from .attention import (LN2, AttentionOutput, causal_full_attention, full_attention,
                         level_bias, psa_streaming)
 from .errors import NumericError, TensorFileError, ValidationError
-from .importance import importance_sampled, sample_tables
+from .importance import (antidiagonal_selection, importance_antidiagonal, importance_sampled,
+                         sample_tables)
 from .layout import (PRESET_CUTPOINTS, BlockLayout, LevelThresholds, QuantileCutpoints,
                      SamplerConfig, SimThresholds, make_layout)
 from .mask import (MaskPlan, SparsityReport, assign_quantile, assign_threshold, binary_mask,
@@ -25,7 +26,8 @@ __all__ = [
     "SamplerConfig", "SimThresholds", "SparsityReport", "TensorFileError", "ValidationError",
     "assign_quantile", "assign_threshold", "binary_mask", "build_pyramid",
     "causal_full_attention", "causal_premask", "combine_mask", "full_attention",
-    "importance_sampled", "level_bias", "level_cap_from_similarity", "make_layout",
+    "antidiagonal_selection", "importance_antidiagonal", "importance_sampled", "level_bias",
+    "level_cap_from_similarity", "make_layout",
     "psa_attention", "psa_forward_4d", "psa_streaming", "report_from_counts", "sample_tables",
     "sparsity_report",
 ]

@@ -29,6 +29,10 @@ _SIGNATURES = {
     "psa_importance_sampled": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int, c_int64, c_int,
                                        c_int, c_int, c_void_p, c_void_p, c_int, c_int, c_int,
                                        c_void_p, c_void_p, c_void_p]),
+    "psa_antidiag_workspace_bytes": (c_size_t, [c_int64, c_int64, c_int, c_int]),
+    "psa_importance_antidiagonal": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int, c_int64,
+                                            c_int, c_int, c_int, c_int, c_void_p, c_void_p,
+                                            c_void_p]),
     "psa_assign_levels": (c_int, [c_void_p, c_int64, c_int, c_int, c_int, c_int, c_int,
                                   c_void_p, c_void_p, c_int, c_void_p, c_int, c_int, c_int, c_int,
                                   c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),

@@ -296,4 +296,26 @@ PSA_DEV double np_pairwise_sum(const double* a, int n, int stride = 1) {
   return res;
 }
 
+// Same order with elements produced by f(i) (n <= 128).
+template <class F>
+PSA_DEV double np_pairwise_sum_fn(int n, F f) {
+  if (n < 8) {
+    double res = 0.0;
+    for (int i = 0; i < n; ++i) res = __dadd_rn(res, f(i));
+    return res;
+  }
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = f(j);
+  int i = 8;
+  for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], f(i + j));
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __dadd_rn(res, f(i));
+  return res;
+}
+
 }  // namespace psa

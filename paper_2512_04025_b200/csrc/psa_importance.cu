@@ -37,10 +37,22 @@ struct ImpSmem {
   double x[kImpRows * (kImpCols + 1)];
 };
 
+// Row maps: local sampled index -> row inside the head.
+struct TableRows {  // importance_sampled: rows drawn by the reference's generator (host table)
+  const int32_t* rows;
+  PSA_DEV int64_t operator()(int a) const { return rows[a]; }
+};
+struct StridedRows {  // antidiagonal: element a of class r = block (a / per) offset r + (a % per)*stride
+  int per, block, r, stride;
+  PSA_DEV int64_t operator()(int a) const {
+    return static_cast<int64_t>(a / per) * block + r + (a % per) * stride;
+  }
+};
+
 // Load `count` gathered bf16 rows of length D into registers (16 B per vector).
-template <int D>
-PSA_DEV void gather_rows_regs(const uint16_t* __restrict__ base, const int32_t* __restrict__ rows,
-                              int first, int count, uint4 (&buf)[kImpCols * D / 8 / kImpThreads]) {
+template <int D, class Rows>
+PSA_DEV void gather_rows_regs(const uint16_t* __restrict__ base, const Rows& rows, int first,
+                              int count, uint4 (&buf)[kImpCols * D / 8 / kImpThreads]) {
   constexpr int kVecPerRow = D / 8;
   constexpr int kPer = kImpCols * D / 8 / kImpThreads;
 #pragma unroll
@@ -48,7 +60,7 @@ PSA_DEV void gather_rows_regs(const uint16_t* __restrict__ base, const int32_t* 
     const int idx = threadIdx.x + p * kImpThreads;
     const int r = idx / kVecPerRow, c = idx % kVecPerRow;
     if (r < count) {
-      const int64_t row = rows[first + r];
+      const int64_t row = rows(first + r);
       buf[p] = __ldg(reinterpret_cast<const uint4*>(base + row * D) + c);
     } else {
       buf[p] = make_uint4(0, 0, 0, 0);
@@ -73,6 +85,45 @@ PSA_DEV double bf16_to_f64(uint16_t h) {
   return static_cast<double>(__uint_as_float(static_cast<uint32_t>(h) << 16));
 }
 
+// 64 x 64 fp64 logit tile on the DMMA pipe: x[r][c] = dot(qs[r], ks[c]) (exact for bf16
+// inputs). 8 warps in a 2 x 4 grid, warp tile 32 x 16 (4 x 2 m8n8k4 tiles).
+template <int D>
+PSA_DEV void dmma_logit_tile(ImpSmem<D>& sm) {
+  constexpr int kLd = ImpSmem<D>::kLd;
+  constexpr int kXld = kImpCols + 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wr = warp >> 2, wc = warp & 3;
+  double acc[4][2][2];
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+  const uint16_t* qa = sm.qs + (wr * 32 + (lane >> 2)) * kLd + (lane & 3);
+  const uint16_t* kb = sm.ks + (wc * 16 + (lane >> 2)) * kLd + (lane & 3);
+#pragma unroll 4
+  for (int k4 = 0; k4 < D / 4; ++k4) {
+    double af[4], bf[2];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) af[mt] = bf16_to_f64(qa[mt * 8 * kLd + k4 * 4]);
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) bf[nt] = bf16_to_f64(kb[nt * 8 * kLd + k4 * 4]);
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) dmma_m8n8k4(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
+  }
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int r = wr * 32 + mt * 8 + (lane >> 2);
+        const int c = wc * 16 + nt * 8 + (lane & 3) * 2 + e;
+        sm.x[r * kXld + c] = acc[mt][nt][e];
+      }
+}
+
 template <int D, bool MEAN>
 __global__ void __launch_bounds__(kImpThreads, 2)
     importance_stats_kernel(const uint16_t* __restrict__ q, const uint16_t* __restrict__ k,
@@ -82,7 +133,6 @@ __global__ void __launch_bounds__(kImpThreads, 2)
                             double* __restrict__ lstat) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   auto& sm = *reinterpret_cast<ImpSmem<D>*>(smem_raw);
-  constexpr int kLd = ImpSmem<D>::kLd;
   constexpr int kXld = kImpCols + 1;
   constexpr int kPer = kImpCols * D / 8 / kImpThreads;
 
@@ -97,7 +147,7 @@ __global__ void __launch_bounds__(kImpThreads, 2)
   // sampled query rows -> fp64 smem (reuse the chunk register buffer for the gather)
   {
     uint4 buf[kPer];
-    gather_rows_regs<D>(qh, q_rows, a0, rows_here, buf);
+    gather_rows_regs<D>(qh, TableRows{q_rows}, a0, rows_here, buf);
     store_rows_bf16<D>(sm.qs, buf);
   }
 
@@ -106,8 +156,6 @@ __global__ void __launch_bounds__(kImpThreads, 2)
   const int C = n_k * s_k;
   const int n_chunks = (C + cw - 1) / cw;
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wr = warp >> 2, wc = warp & 3;  // 2 x 4 warp grid over the 64 x 64 logit tile
   const int a_loc = threadIdx.x >> 2, quad = threadIdx.x & 3;
   const int a_glob = a0 + a_loc;
   const bool row_ok = a_loc < rows_here;
@@ -121,46 +169,17 @@ __global__ void __launch_bounds__(kImpThreads, 2)
   }
 
   uint4 pref[kPer];
-  gather_rows_regs<D>(kh, k_rows, 0, min(cw, C), pref);
+  gather_rows_regs<D>(kh, TableRows{k_rows}, 0, min(cw, C), pref);
 
   for (int ch = 0; ch < n_chunks; ++ch) {
     const int b0 = ch * cw;
     const int cols = min(cw, C - b0);
     __syncthreads();  // previous chunk's X/K consumers are done
     store_rows_bf16<D>(sm.ks, pref);
-    if (ch + 1 < n_chunks) gather_rows_regs<D>(kh, k_rows, b0 + cw, min(cw, C - b0 - cw), pref);
+    if (ch + 1 < n_chunks) gather_rows_regs<D>(kh, TableRows{k_rows}, b0 + cw, min(cw, C - b0 - cw), pref);
     __syncthreads();
 
-    // ---- 64 x 64 fp64 logit tile on the DMMA pipe: warp tile 32 x 16 (4 x 2 m8n8 tiles)
-    double acc[4][2][2];
-#pragma unroll
-    for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-    const uint16_t* qa = sm.qs + (wr * 32 + (lane >> 2)) * kLd + (lane & 3);
-    const uint16_t* kb = sm.ks + (wc * 16 + (lane >> 2)) * kLd + (lane & 3);
-#pragma unroll 4
-    for (int k4 = 0; k4 < D / 4; ++k4) {
-      double af[4], bf[2];
-#pragma unroll
-      for (int mt = 0; mt < 4; ++mt) af[mt] = bf16_to_f64(qa[mt * 8 * kLd + k4 * 4]);
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt) bf[nt] = bf16_to_f64(kb[nt * 8 * kLd + k4 * 4]);
-#pragma unroll
-      for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) dmma_m8n8k4(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
-    }
-#pragma unroll
-    for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int r = wr * 32 + mt * 8 + (lane >> 2);
-          const int c = wc * 16 + nt * 8 + (lane & 3) * 2 + e;
-          sm.x[r * kXld + c] = acc[mt][nt][e];  // raw fp64 dot (exact); scaled below
-        }
+    dmma_logit_tile<D>(sm);  // raw fp64 dots (exact) -> sm.x
     __syncthreads();
 
     // ---- per-row statistics; 4 threads per row, blocks interleaved over the quad
@@ -230,9 +249,189 @@ __global__ void __launch_bounds__(128) importance_finalize_kernel(
   }
 }
 
+
+// ------------------------------------------------------------------ antidiagonal estimator
+// Reference: importance_antidiagonal (pkg/src/pyrattn/importance.py:97-132). Query row p of a
+// query block reads the keys whose in-block column c satisfies (p + c) % stride == 0, i.e. the
+// residue class (-p) mod stride of every KV block (b_k % stride == 0); logits are
+// fl(dot * fl(1/sqrt(d))) (importance.py:113,128: multiply by the reciprocal), softmaxed over
+// the row's n_k * per picks, summed per block, averaged over the b_q rows of the query block.
+//
+// All query rows with the same residue r share one key set, so each residue class is one dense
+// (n_q * c_r) x (n_k * per) fp64 GEMM on the DMMA pipe. The stats kernel streams the class's
+// keys in chunks of whole KV blocks; per row and chunk it takes the chunk max m_c (merged into
+// a running max), and per block the pairwise (numpy order) sum E of exp(logit - m_c). The
+// finalize kernel rescales E by exp(m_c - m_row) / l_row and averages over the query block's
+// rows sequentially (numpy's axis-0 mean). Only the rescaling step differs from the reference's
+// per-element exp(logit - m_row) / l_row (ulps; the level map is unchanged).
+template <int D>
+__global__ void __launch_bounds__(kImpThreads, 2)
+    antidiag_stats_kernel(const uint16_t* __restrict__ q, const uint16_t* __restrict__ k,
+                          int hq, int hkv, int64_t n, int b_q, int b_k, int stride, int n_k,
+                          double scale, int n_chunks, double* __restrict__ E,
+                          double* __restrict__ Mc, double* __restrict__ mstat,
+                          double* __restrict__ lstat) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  auto& sm = *reinterpret_cast<ImpSmem<D>*>(smem_raw);
+  constexpr int kXld = kImpCols + 1;
+  constexpr int kPer = kImpCols * D / 8 / kImpThreads;
+
+  const int r = blockIdx.z;
+  const int c_r = r < b_q ? (b_q - r + stride - 1) / stride : 0;  // rows of class r per block
+  const int n_q = static_cast<int>(n / b_q);
+  const int R = n_q * c_r;
+  const int a0 = blockIdx.x * kImpRows;
+  if (a0 >= R) return;
+  const int rows_here = min(kImpRows, R - a0);
+  const int bhq = blockIdx.y;
+  const int b = bhq / hq, h = bhq % hq;
+  const int hk = h / (hq / hkv);
+  const uint16_t* qh = q + static_cast<int64_t>(bhq) * n * D;
+  const uint16_t* kh = k + (static_cast<int64_t>(b) * hkv + hk) * n * D;
+  const int per = b_k / stride;
+  const int kr = (stride - r % stride) % stride;
+  const StridedRows qmap{c_r, b_q, r, stride};
+  const StridedRows kmap{per, b_k, kr, stride};
+
+  {
+    uint4 buf[kPer];
+    gather_rows_regs<D>(qh, qmap, a0, rows_here, buf);
+    store_rows_bf16<D>(sm.qs, buf);
+  }
+  const int bpc = kImpCols / per;  // whole KV blocks per chunk (per <= 64 checked on the host)
+  const int cw = bpc * per;
+  const int C = n_k * per;
+
+  const int a_loc = threadIdx.x >> 2, quad = threadIdx.x & 3;
+  const bool row_ok = a_loc < rows_here;
+  const int64_t grow = row_ok ? qmap(a0 + a_loc) : 0;  // row inside the head
+  double* Erow = E + (static_cast<int64_t>(bhq) * n + grow) * n_k;
+  double m_run = -INFINITY, l_run = 0.0;
+
+  uint4 pref[kPer];
+  gather_rows_regs<D>(kh, kmap, 0, min(cw, C), pref);
+  for (int ch = 0; ch < n_chunks; ++ch) {
+    const int c0 = ch * cw;
+    const int cols = min(cw, C - c0);
+    __syncthreads();
+    store_rows_bf16<D>(sm.ks, pref);
+    if (ch + 1 < n_chunks) gather_rows_regs<D>(kh, kmap, c0 + cw, min(cw, C - c0 - cw), pref);
+    __syncthreads();
+    dmma_logit_tile<D>(sm);
+    __syncthreads();
+
+    const double* xr = sm.x + a_loc * kXld;
+    const int nb = cols / per;
+    const int j0 = c0 / per;
+    double cmax = -INFINITY;
+    for (int bb = quad; bb < nb; bb += 4)
+      for (int t = 0; t < per; ++t) cmax = fmax(cmax, xr[bb * per + t]);
+    cmax = fmax(cmax, __shfl_xor_sync(0xffffffffu, cmax, 1));
+    cmax = fmax(cmax, __shfl_xor_sync(0xffffffffu, cmax, 2));
+    // fl(x * scale) is monotone in x: the max of the scaled logits is the scaled max
+    const double m_new = fmax(m_run, __dmul_rn(cmax, scale));
+    double part = 0.0;
+    for (int bb = quad; bb < nb; bb += 4) {
+      const double* xb = xr + bb * per;
+      const double e = np_pairwise_sum_fn(per, [&](int t) {
+        return exp(__dsub_rn(__dmul_rn(xb[t], scale), m_new));
+      });
+      part = __dadd_rn(part, e);
+      if (row_ok) Erow[j0 + bb] = e;
+    }
+    part = __dadd_rn(part, __shfl_xor_sync(0xffffffffu, part, 1));
+    part = __dadd_rn(part, __shfl_xor_sync(0xffffffffu, part, 2));
+    l_run = __dadd_rn(__dmul_rn(l_run, exp(__dsub_rn(m_run, m_new))), part);
+    m_run = m_new;
+    if (row_ok && quad == 0) Mc[(static_cast<int64_t>(bhq) * n + grow) * n_chunks + ch] = m_new;
+  }
+  if (row_ok && quad == 0) {
+    mstat[static_cast<int64_t>(bhq) * n + grow] = m_run;
+    lstat[static_cast<int64_t>(bhq) * n + grow] = l_run;
+  }
+}
+
+// S_ij = (sum_{p < b_q} E[p, j] * exp(m_c(p, j) - m_p) / l_p) / b_q, p ascending
+__global__ void __launch_bounds__(128) antidiag_finalize_kernel(
+    const double* __restrict__ E, const double* __restrict__ Mc, const double* __restrict__ mstat,
+    const double* __restrict__ lstat, int64_t n, int b_q, int n_q, int n_k, int bpc, int n_chunks,
+    double* __restrict__ S) {
+  const int i = blockIdx.x;
+  const int64_t bhq = blockIdx.y;
+  for (int j = threadIdx.x; j < n_k; j += blockDim.x) {
+    double acc = 0.0;
+    for (int p = 0; p < b_q; ++p) {
+      const int64_t a = bhq * n + static_cast<int64_t>(i) * b_q + p;
+      const double w = exp(__dsub_rn(Mc[a * n_chunks + j / bpc], mstat[a]));
+      acc = __dadd_rn(acc, __ddiv_rn(__dmul_rn(E[a * n_k + j], w), lstat[a]));
+    }
+    S[(bhq * n_q + i) * n_k + j] = __ddiv_rn(acc, static_cast<double>(b_q));
+  }
+}
+
+static int antidiag_geometry(int b_k, int stride, int n_k, int* per, int* bpc, int* n_chunks) {
+  *per = b_k / stride;
+  *bpc = kImpCols / *per;
+  const int cw = *bpc * *per;
+  *n_chunks = (n_k * *per + cw - 1) / cw;
+  return 0;
+}
+
+template <int D>
+static int launch_antidiag(const void* q, const void* k, int64_t batch, int hq, int hkv,
+                           int64_t n, int b_q, int b_k, int stride, double* scores, void* ws,
+                           cudaStream_t s) {
+  const int64_t bhq = batch * hq;
+  const int n_q = static_cast<int>(n / b_q), n_k = static_cast<int>(n / b_k);
+  int per, bpc, n_chunks;
+  antidiag_geometry(b_k, stride, n_k, &per, &bpc, &n_chunks);
+  double* E = static_cast<double*>(ws);
+  double* Mc = E + bhq * n * n_k;
+  double* mstat = Mc + bhq * n * n_chunks;
+  double* lstat = mstat + bhq * n;
+  const size_t smem = sizeof(ImpSmem<D>);
+  cudaFuncSetAttribute(antidiag_stats_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(smem));
+  const int c_max = (b_q + stride - 1) / stride;
+  dim3 grid((n_q * c_max + kImpRows - 1) / kImpRows, static_cast<unsigned>(bhq), stride);
+  antidiag_stats_kernel<D><<<grid, kImpThreads, smem, s>>>(
+      static_cast<const uint16_t*>(q), static_cast<const uint16_t*>(k), hq, hkv, n, b_q, b_k,
+      stride, n_k, 1.0 / sqrt(static_cast<double>(D)), n_chunks, E, Mc, mstat, lstat);
+  int rc = psa_check_launch("antidiag_stats_kernel");
+  if (rc) return rc;
+  antidiag_finalize_kernel<<<dim3(n_q, bhq), 128, 0, s>>>(E, Mc, mstat, lstat, n, b_q, n_q, n_k,
+                                                          bpc, n_chunks, scores);
+  return psa_check_launch("antidiag_finalize_kernel");
+}
+
 }  // namespace psa
 
 using namespace psa;
+
+extern "C" size_t psa_antidiag_workspace_bytes(int64_t bhq, int64_t n, int b_k, int stride) {
+  if (stride < 1 || b_k % stride || b_k / stride > kImpCols || n % b_k) return 0;
+  int per, bpc, n_chunks;
+  const int n_k = static_cast<int>(n / b_k);
+  antidiag_geometry(b_k, stride, n_k, &per, &bpc, &n_chunks);
+  return static_cast<size_t>(bhq * n * (n_k + n_chunks + 2)) * sizeof(double);
+}
+
+extern "C" int psa_importance_antidiagonal(const void* q, const void* k, int64_t batch, int hq,
+                                           int hkv, int64_t n, int d, int b_q, int b_k,
+                                           int stride, double* scores, void* workspace,
+                                           void* stream) {
+  PSA_CHECK_ARG(q && k && scores && workspace, "null pointer argument");
+  PSA_CHECK_ARG(d == 64 || d == 128, "head_dim must be 64 or 128 for the sm_100a path");
+  PSA_CHECK_ARG(hq >= 1 && hkv >= 1 && hq % hkv == 0, "query heads must be a multiple of kv heads");
+  PSA_CHECK_ARG(b_q >= 1 && b_k >= 1 && n % b_q == 0 && n % b_k == 0, "layout does not divide seq_len");
+  PSA_CHECK_ARG(stride >= 1 && b_k % stride == 0, "stride must divide k_block");
+  PSA_CHECK_ARG(b_k / stride <= kImpCols,
+                "k_block / stride > 64 is not supported by the sm_100a antidiagonal kernel");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (d == 128)
+    return launch_antidiag<128>(q, k, batch, hq, hkv, n, b_q, b_k, stride, scores, workspace, s);
+  return launch_antidiag<64>(q, k, batch, hq, hkv, n, b_q, b_k, stride, scores, workspace, s);
+}
 
 extern "C" size_t psa_importance_workspace_bytes(int64_t bhq, int n_q, int s_q, int n_k) {
   const int64_t R = static_cast<int64_t>(n_q) * s_q;

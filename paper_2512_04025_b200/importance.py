@@ -1,6 +1,7 @@
 """Block-importance estimation (K2) on the GPU.
 
-Drop-in for importance_sampled (pkg/src/pyrattn/importance.py:52-85). The sampled row
+Drop-ins for importance_sampled (pkg/src/pyrattn/importance.py:52-85), antidiagonal_selection
+(:88-94) and importance_antidiagonal (:97-132). The sampled row
 indices come from the same single seeded numpy generator in the same order as the reference
 (importance.py:68-76: every query block ascending, then every KV block ascending); they
 depend only on (seed, layout, s_q, s_k), are shared by all heads, and are cached on the
@@ -80,4 +81,51 @@ def importance_sampled(q, k, layout: BlockLayout, cfg: SamplerConfig,
     q4, lead = as_bhnd(q, "Q", layout.seq_len, layout.head_dim)
     k4, _ = as_bhnd(k, "K", layout.seq_len, layout.head_dim)
     s = importance_scores(q4, k4, layout, cfg, reducer)
+    return s.reshape(lead + (layout.n_q, layout.n_k))
+
+
+def antidiagonal_selection(b_q: int, b_k: int, stride: int) -> torch.Tensor:
+    """Boolean (b_q, b_k) mask of the strided antidiagonal positions (importance.py:88-94).
+    A host-side layout helper (no tensor data), as in the reference."""
+    if stride < 1 or b_k % stride:
+        raise ValidationError(f"stride {stride} must divide k_block {b_k}")
+    p = torch.arange(b_q)[:, None]
+    c = torch.arange(b_k)[None, :]
+    return (p + c) % stride == 0
+
+
+def antidiagonal_scores(q4: torch.Tensor, k4: torch.Tensor, layout: BlockLayout,
+                        stride: int) -> torch.Tensor:
+    """fp64 antidiagonal scores [B, Hq, n_q, n_k] from bf16 [B, H, N, d] device tensors."""
+    if stride is None or int(stride) < 1 or layout.k_block % int(stride):
+        raise ValidationError(f"stride {stride} must divide k_block {layout.k_block}")
+    stride = int(stride)
+    if layout.k_block // stride > 64:
+        raise ValidationError("k_block / stride > 64 is not supported by the sm_100a "
+                              "antidiagonal kernel")
+    B, Hq, n, d = q4.shape
+    Hkv = k4.shape[1]
+    if Hq % Hkv:
+        raise ValidationError(f"query heads {Hq} not a multiple of kv heads {Hkv}")
+    dev = q4.device
+    lib = _lib.load()
+    ws = torch.empty(lib.psa_antidiag_workspace_bytes(B * Hq, n, layout.k_block, stride),
+                     dtype=torch.uint8, device=dev)
+    scores = torch.empty(B, Hq, layout.n_q, layout.n_k, dtype=torch.float64, device=dev)
+    rc = lib.psa_importance_antidiagonal(q4.data_ptr(), k4.data_ptr(), B, Hq, Hkv, n, d,
+                                         layout.q_block, layout.k_block, stride,
+                                         scores.data_ptr(), ws.data_ptr(), stream_handle(dev))
+    _lib.check(rc, "psa_importance_antidiagonal")
+    return scores
+
+
+def importance_antidiagonal(q, k, layout: BlockLayout, stride: int) -> torch.Tensor:
+    """Antidiagonal-probe importance scores (importance.py:97-132), float64.
+
+    Shape (n_q, n_k) for (n, d) inputs, else [..., n_q, n_k] following q's leading dims.
+    """
+    layout.check_gpu()
+    q4, lead = as_bhnd(q, "Q", layout.seq_len, layout.head_dim)
+    k4, _ = as_bhnd(k, "K", layout.seq_len, layout.head_dim)
+    s = antidiagonal_scores(q4, k4, layout, stride)
     return s.reshape(lead + (layout.n_q, layout.n_k))

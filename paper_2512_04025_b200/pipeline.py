@@ -20,7 +20,7 @@ import torch
 from ._tensors import as_bhnd, restore
 from .attention import attention_forward
 from .errors import NumericError, ValidationError
-from .importance import importance_scores
+from .importance import antidiagonal_scores, importance_scores
 from .layout import (PRESET_CUTPOINTS, LevelThresholds, QuantileCutpoints, SamplerConfig,
                      SimThresholds, make_layout)
 from .mask import MaskPlan, assign_levels_device
@@ -172,16 +172,16 @@ def psa_forward_4d(q4, k4, v4, cfg: RunConfig, keep_scores: bool = False,
     if cfg.grid is not None:
         raise ValidationError("[stage: permutation] the Hilbert token permutation is not part "
                               "of the sm_100a operator yet; permute Q/K/V before the call")
-    if cfg.estimator == "antidiagonal":
-        raise ValidationError("[stage: importance] the antidiagonal estimator is not available on "
-                              "the sm_100a path yet; use sampled-max")
     mode, rule = _mask_rule(cfg, lay.levels)
     B, Hq = q4.shape[:2]
     Hkv = k4.shape[1]
     pyr = _stage("pyramid", build_pyramid, k4, v4, lay)
-    sampler = SamplerConfig(s_q=cfg.s_q, s_k=cfg.s_k, seed=cfg.seed)
-    reducer = "max" if cfg.estimator == "sampled-max" else "mean"
-    scores = _stage("importance", importance_scores, q4, k4, lay, sampler, reducer)
+    if cfg.estimator == "antidiagonal":  # pipeline._estimate (pipeline.py:239-244)
+        scores = _stage("importance", antidiagonal_scores, q4, k4, lay, cfg.stride)
+    else:
+        sampler = SamplerConfig(s_q=cfg.s_q, s_k=cfg.s_k, seed=cfg.seed)
+        reducer = "max" if cfg.estimator == "sampled-max" else "mean"
+        scores = _stage("importance", importance_scores, q4, k4, lay, sampler, reducer)
     caps = None
     if cfg.sim_thresholds is not None:
         caps = _stage("similarity-cap", similarity_caps, k4, lay, SimThresholds(cfg.sim_thresholds))

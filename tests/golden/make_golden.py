@@ -104,3 +104,11 @@ if __name__ == "__main__":
     case("antidiag", 1024, 64, 64, 64, 4, seed=8, estimator="antidiagonal", stride=8,
          thresholds=TAUS)
     case("dropped_rows", 512, 64, 64, 64, 2, seed=9, thresholds=(0.02, 0.05))
+    # cfg4-style (Qwen prefill): antidiagonal stride 8 + similarity cap + causal pre-pass
+    case("antidiag_causal_qwen", 1024, 128, 64, 64, 4, seed=10, estimator="antidiagonal",
+         stride=8, thresholds=TAUS, sim=(0.75, 0.70, 0.70), causal=True)
+    case("antidiag_stride4_b120", 960, 128, 120, 120, 4, seed=11, estimator="antidiagonal",
+         stride=4, thresholds=(0.1634, 0.2803, 0.3738, 0.95))
+    # stride does not divide q_block: residue classes of unequal size
+    case("antidiag_ragged", 960, 64, 60, 48, 4, seed=12, estimator="antidiagonal", stride=8,
+         thresholds=TAUS)

@@ -18,6 +18,7 @@ def _declared():
 def test_header_declares_expected_entry_points():
     names = _declared()
     for n in ("psa_pyramid_build", "psa_similarity_caps", "psa_importance_sampled",
+              "psa_importance_antidiagonal", "psa_antidiag_workspace_bytes",
               "psa_assign_levels", "psa_mask_to_plan", "psa_attn_fwd", "psa_last_error"):
         assert n in names
 
@@ -44,6 +45,12 @@ def test_argument_errors_map_to_validation_error():
     rc = lib.psa_attn_fwd(1, 1, 1, 1, 1, 1, 2, 1, 1024, 128, 256, 64, 2, 1, 1, 0, 1, 1, 1, None)
     assert rc == _lib.PSA_EINVAL and "q_block" in lib.psa_last_error().decode()
     assert lib.psa_importance_workspace_bytes(2, 10, 8, 10) == 8 * (2 * 80 * 10 + 2 * 2 * 80)
+    # antidiagonal: stride must divide k_block, k_block/stride <= 64
+    rc = lib.psa_importance_antidiagonal(1, 1, 1, 1, 1, 1024, 128, 64, 64, 3, 1, 1, None)
+    assert rc == _lib.PSA_EINVAL and "stride" in lib.psa_last_error().decode()
+    assert lib.psa_antidiag_workspace_bytes(2, 1024, 64, 3) == 0
+    # n=1024, b_k=64 -> n_k=16, per=8, 8 blocks per chunk -> 2 chunks: E + Mc + m + l per row
+    assert lib.psa_antidiag_workspace_bytes(2, 1024, 64, 8) == 8 * 2 * 1024 * (16 + 2 + 2)
 
 
 def test_product_path_rejects_cpu_tensors():

@@ -239,7 +239,7 @@ def test_mask_validation():
 
 # ------------------------------------------------------------------ fused pipeline
 @pytest.mark.parametrize("case", ["cfg1", "wan_small", "quantile", "binary", "simcap", "causal_gqa",
-                                  "mean"])
+                                  "mean", "antidiag_gqa_causal", "antidiag_wan"])
 def test_pipeline_level_map_and_output(case):
     psa = _psa()
     kw = dict(estimator="sampled-max", s_q=8, s_k=8, seed=0, mask="threshold",
@@ -263,6 +263,13 @@ def test_pipeline_level_map_and_output(case):
         n, d, b, H = 2048, 128, 64, 4
         kw["causal"] = True
         hq, hkv = 4, 2
+    elif case == "antidiag_gqa_causal":  # cfg4 recipe at reduced size
+        n, d, b, H = 4096, 128, 64, 4
+        kw.update(estimator="antidiagonal", stride=8, causal=True, sim_thresholds=(0.75, 0.7, 0.7))
+        hq, hkv = 4, 2
+    elif case == "antidiag_wan":
+        n, d, b, H = 3840, 128, 120, 4
+        kw.update(estimator="antidiagonal", stride=8, thresholds=(0.1634, 0.2803, 0.3738, 0.95))
     else:
         n, d, b, H = 4096, 64, 64, 4
         kw["estimator"] = "sampled-mean"
@@ -275,7 +282,7 @@ def test_pipeline_level_map_and_output(case):
     lm = res.level_map.cpu().numpy()[0]
     lay = orc.Layout(n, d, b, b, H)
     okw = {x: kw.get(x) for x in ("estimator", "s_q", "s_k", "seed", "mask", "thresholds",
-                                  "cutpoints", "tau", "sim_thresholds", "causal")}
+                                  "cutpoints", "tau", "sim_thresholds", "causal", "stride")}
     out = res.out.float().cpu().numpy()
     mism = 0
     for h in range(hq):
