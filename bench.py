@@ -36,10 +36,15 @@ CONFIGS = {
                  d=128, b_q=120, b_k=120, levels=4, taus=WAN_TAUS, causal=False),
     "cfg3": dict(desc="Wan2.1-14B 720p/81f: L=75600 H=40 d=128", B=1, Hq=40, Hkv=40, N=75600,
                  d=128, b_q=120, b_k=120, levels=4, taus=WAN_TAUS, causal=False),
-    "cfg4": dict(desc="Qwen2.5-VL-7B-style prefill: L=32768 Hq=28 Hkv=4 d=128 causal "
-                      "(sampled-max estimator)", B=1, Hq=28, Hkv=4, N=32768, d=128, b_q=128,
-                 b_k=64, levels=4, taus=WAN_TAUS, causal=True),
+    "cfg4": dict(desc="Qwen2.5-VL-7B-style prefill: L=32768 Hq=28 Hkv=4 d=128 causal, "
+                      "antidiagonal stride 8 + similarity cap (0.75,0.70,0.70)", B=1, Hq=28,
+                 Hkv=4, N=32768, d=128, b_q=128, b_k=64, levels=4, taus=WAN_TAUS, causal=True,
+                 estimator="antidiagonal", stride=8, sim=(0.75, 0.70, 0.70)),
 }
+for _c in CONFIGS.values():
+    _c.setdefault("estimator", "sampled-max")
+    _c.setdefault("stride", None)
+    _c.setdefault("sim", None)
 
 
 def log(*a):
@@ -117,16 +122,36 @@ def make_inputs(cfg, heads, kv_heads, device, seed=0):
 def run_config(cfg):
     from paper_2512_04025_b200 import RunConfig
     return RunConfig.from_dict(dict(n=cfg["N"], d=cfg["d"], b_q=cfg["b_q"], b_k=cfg["b_k"],
-                                    levels=cfg["levels"], estimator="sampled-max", s_q=8, s_k=8,
-                                    seed=0, mask="threshold", thresholds=list(cfg["taus"]),
+                                    levels=cfg["levels"], estimator=cfg["estimator"], s_q=8, s_k=8,
+                                    seed=0, stride=cfg["stride"], mask="threshold",
+                                    thresholds=list(cfg["taus"]), sim_thresholds=cfg["sim"],
                                     tile_len=128, causal=cfg["causal"]))
 
 
-def flops_from_counts(counts, cfg):
-    """Executed algorithmic FLOPs = 4*d*sum_h count_h * b_q * (b_k >> (h-1)) (non-causal;
-    causal straddling blocks are counted in full — an upper bound, stated in DESIGN.md)."""
-    return 4 * cfg["d"] * sum(int(c) * cfg["b_q"] * (cfg["b_k"] >> (h - 1))
-                              for h, c in enumerate(counts) if h >= 1)
+def flops_from_counts(counts, cfg, heads=1):
+    """Executed algorithmic FLOPs = 4*d*sum_h count_h * b_q * (b_k >> (h-1)),
+    over ``heads`` (batch*q-head) units. Causal: the straddling level-1 pairs (always present
+    after the causal pre-pass, mask.py:324-349) count only their visible (q, k) pairs."""
+    d, bq, bk = cfg["d"], cfg["b_q"], cfg["b_k"]
+    f = 4 * d * sum(int(c) * bq * (bk >> (h - 1)) for h, c in enumerate(counts) if h >= 1)
+    if cfg["causal"]:
+        f -= 4 * d * heads * _causal_hidden_pairs(cfg["N"], bq, bk)
+    return f
+
+
+def _causal_hidden_pairs(n, bq, bk):
+    """Number of masked (q, k) pairs inside straddling level-1 block pairs of one head."""
+    hidden = 0
+    for i in range(n // bq):
+        q_lo, q_hi = i * bq, i * bq + bq - 1
+        for j in range(q_lo // bk, min(n // bk, q_hi // bk + 1)):
+            k_lo = j * bk
+            if k_lo + bk - 1 <= q_lo:
+                continue  # fully visible
+            for r in range(q_lo, q_hi + 1):
+                vis = max(0, min(bk, r - k_lo + 1))
+                hidden += bk - vis
+    return hidden
 
 
 # ------------------------------------------------------------------------- CPU baseline
@@ -134,12 +159,17 @@ def _cpu_worker(args):
     """Time the oracle port of the reference path on a bounded sample of one head."""
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     from oracle import psa_oracle as orc
-    q, k, v, lay_t, taus, n_blocks, causal = args
+    q, k, v, lay_t, taus, n_blocks, causal, estimator, stride, sim = args
     lay = orc.Layout(*lay_t)
     t0 = time.perf_counter()
     kl, vl = orc.build_pyramid(k, v, lay)
-    scores = orc.importance_sampled(q, k, lay, 8, 8, 0)
+    if estimator == "antidiagonal":
+        scores = orc.importance_antidiagonal(q, k, lay, stride)
+    else:
+        scores = orc.importance_sampled(q, k, lay, 8, 8, 0)
     m = orc.assign_threshold(scores, taus)
+    if sim is not None:
+        m = orc.combine_mask(m, orc.level_caps(k, lay, sim))
     if causal:
         m = orc.causal_premask(m, lay)
     t1 = time.perf_counter()
@@ -205,7 +235,7 @@ def cpu_baseline(cfg, q_dev, k_dev, v_dev, n_blocks=None, max_workers=None):
         jobs.append((q_dev[0, h].to(torch.float64).cpu().numpy(),
                      k_dev[0, hk].to(torch.float64).cpu().numpy(),
                      v_dev[0, hk].to(torch.float64).cpu().numpy(), lay_t, cfg["taus"],
-                     n_blocks, cfg["causal"]))
+                     n_blocks, cfg["causal"], cfg["estimator"], cfg["stride"], cfg["sim"]))
     ctx = mp.get_context("spawn")
     saved = {k_: os.environ.get(k_) for k_ in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS")}
     for k_ in saved:  # children inherit: one BLAS thread per worker process
@@ -223,7 +253,7 @@ def cpu_baseline(cfg, q_dev, k_dev, v_dev, n_blocks=None, max_workers=None):
                 os.environ[k_] = v_
     pre = statistics.mean(r[0] for r in res)
     att = statistics.mean(r[1] for r in res)
-    flops_head = statistics.mean(flops_from_counts(r[2], cfg) for r in res)
+    flops_head = statistics.mean(flops_from_counts(r[2], cfg, 1) for r in res)
     per_head = pre + att * (n_q / n_blocks)
     total_heads = cfg["B"] * cfg["Hq"]
     est_time = per_head * math.ceil(total_heads / workers)
@@ -270,10 +300,10 @@ def main():
     import paper_2512_04025_b200 as psa
     from paper_2512_04025_b200 import _lib
     from paper_2512_04025_b200.attention import attention_forward
-    from paper_2512_04025_b200.importance import importance_scores
-    from paper_2512_04025_b200.layout import LevelThresholds, SamplerConfig
+    from paper_2512_04025_b200.importance import antidiagonal_scores, importance_scores
+    from paper_2512_04025_b200.layout import LevelThresholds, SamplerConfig, SimThresholds
     from paper_2512_04025_b200.mask import assign_levels_device
-    from paper_2512_04025_b200.pyramid import build_pyramid
+    from paper_2512_04025_b200.pyramid import build_pyramid, similarity_caps
 
     _lib.load()
     # strong scaling: the workload's query heads are split evenly; KV heads follow (GQA groups)
@@ -290,18 +320,23 @@ def main():
     stream = torch.cuda.current_stream(device)
 
     stage_names = ("pyramid", "importance", "assign", "attention")
-    launches_per_step = 1 + 2 + 1 + 1
+    launches_per_step = 1 + 2 + 1 + 1 + (1 if cfg["sim"] else 0)
+    sim = SimThresholds(cfg["sim"]) if cfg["sim"] else None
 
     def step(events=None):
         ev = events
         if ev: ev[0].record(stream)
         pyr = build_pyramid(k, v, lay)
+        caps = similarity_caps(k, lay, sim) if sim is not None else None
         if ev: ev[1].record(stream)
-        scores = importance_scores(q, k, lay, sampler, "max")
+        if cfg["estimator"] == "antidiagonal":
+            scores = antidiagonal_scores(q, k, lay, cfg["stride"])
+        else:
+            scores = importance_scores(q, k, lay, sampler, "max")
         if ev: ev[2].record(stream)
         plan = assign_levels_device(scores, mode="threshold", rule=rule, levels=lay.levels,
                                     b_q=lay.q_block, b_k=lay.k_block, hkv=k.shape[1],
-                                    causal=cfg["causal"])
+                                    caps=caps, causal=cfg["causal"])
         if ev: ev[3].record(stream)
         out, lse, skipped = attention_forward(q, pyr, plan, cfg["causal"])
         if ev: ev[4].record(stream)
@@ -311,7 +346,7 @@ def main():
         plan, _ = step()
     torch.cuda.synchronize()
     counts = plan.level_counts.cpu().tolist()
-    flops_local = flops_from_counts(counts, cfg)
+    flops_local = flops_from_counts(counts, cfg, cfg["B"] * len(heads))
     rho_bar = psa.report_from_counts(counts, sum(counts)).rho_bar
 
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
@@ -382,7 +417,9 @@ def main():
         "data": "synthetic N(0,1) bf16 Q/K/V (seeded torch.Generator per head)",
         "config": {"workload": f"{args.config}: {cfg['desc']}", "B": cfg["B"], "Hq": Hq,
                    "Hkv": Hkv, "L": cfg["N"], "d": cfg["d"], "b_q": cfg["b_q"],
-                   "b_k": cfg["b_k"], "levels": cfg["levels"], "estimator": "sampled-max s_q=s_k=8 (fp64)",
+                   "b_k": cfg["b_k"], "levels": cfg["levels"], "estimator": (f"antidiagonal stride {cfg['stride']} (fp64)" if cfg["estimator"] == "antidiagonal"
+                                 else "sampled-max s_q=s_k=8 (fp64)"),
+                   "sim_thresholds": cfg["sim"],
                    "mask": f"threshold taus={[round(t, 6) for t in cfg['taus']]}",
                    "rho_bar": rho_bar, "level_counts": counts, "causal": cfg["causal"],
                    "executed_tflop_per_step": flops_all / 1e12,
