@@ -391,7 +391,7 @@ def main():
     attn_flops_launch = float(flops_local)
     achieved = attn_flops_launch / (stage_ms["attention"] * 1e-3) / 1e12
     traffic = None
-    prof = ROOT / "profiles" / "attention_ncu_summary.json"
+    prof = ROOT / "profiles" / f"attention_ncu_summary_{args.config}.json"
     if prof.exists():
         try:
             traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")

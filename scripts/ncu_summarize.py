@@ -1,6 +1,6 @@
 """Summarise ncu captures from gpurun_out/ into profiles/ (tracked).
 
-    python scripts/ncu_summarize.py ROUND_TAG
+    python scripts/ncu_summarize.py ROUND_TAG [CONFIG]
 
 Reads gpurun_out/launches.csv (the `--metrics gpu__time_duration.sum` launch list) and every
 gpurun_out/*_full.ncu-rep (`ncu --set full` captures), and writes per round:
@@ -8,7 +8,7 @@ gpurun_out/*_full.ncu-rep (`ncu --set full` captures), and writes per round:
   profiles/<tag>_launch_summary.json     mean duration per kernel and its share of the step
   profiles/<tag>_<name>_ncu.txt          the details page of each full capture
   profiles/<tag>_<name>_ncu.json         key raw metrics (time, dram bytes, pipe utilisation)
-and refreshes profiles/attention_ncu_summary.json (read by bench.py for roofline.traffic).
+and refreshes profiles/attention_ncu_summary_<CONFIG>.json (read by bench.py for roofline.traffic).
 """
 
 from __future__ import annotations
@@ -17,7 +17,6 @@ import collections
 import csv
 import io
 import json
-import shutil
 import subprocess
 import sys
 from pathlib import Path
@@ -94,12 +93,11 @@ def main(tag: str) -> None:
                         "dram_gbs": ((rd or 0) + (wr or 0)) / t / 1e9 if t else None}
         (PROF / f"{tag}_{name}_ncu.json").write_text(json.dumps(m, indent=1) + "\n")
         print(name, m["summary"])
-        if name == "attn":
-            (PROF / "attention_ncu_summary.json").write_text(json.dumps(
-                {"source": f"profiles/{tag}_attn_ncu.json", "kernel": m.get("kernel"),
+        if name in ("attn", "psa_attn_fwd"):
+            cfg = sys.argv[2] if len(sys.argv) > 2 else "cfg3"
+            (PROF / f"attention_ncu_summary_{cfg}.json").write_text(json.dumps(
+                {"source": f"profiles/{tag}_{name}_ncu.json", "kernel": m.get("kernel"),
                  **m["summary"]}, indent=1) + "\n")
-        if name == "attn" and len(sys.argv) > 2 and sys.argv[2] == "--keep-rep":
-            shutil.copy(rep, PROF / f"{tag}_attn.ncu-rep")
 
 
 if __name__ == "__main__":
