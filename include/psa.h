@@ -63,19 +63,25 @@ int psa_pyramid_build(const void* k, const void* v, int64_t bh, int64_t n, int d
 int psa_similarity_caps(const void* k, int64_t bh, int64_t n, int d, int b_k, int levels,
                         const double* sim_taus, int8_t* caps, void* stream);
 
+/* Importance flags (psa_importance_sampled / psa_importance_antidiagonal). */
+#define PSA_IMP_FP64_ONLY 1 /* skip the int8-sliced tensor-core logits; fp64 DMMA for every head */
+
 /*
  * K2 — sampled importance.  Replaces importance_sampled (pkg/src/pyrattn/importance.py:52-85).
  * q_rows/k_rows: DEVICE int32 tables of sampled row indices inside a head, in the order the
  *   reference's single seeded generator produces them (n_q*s_q and n_k*s_k entries).
  * reducer: 0 = max, 1 = mean.  scores: fp64 [batch*hq, n_q, n_k].
- * Logits are formed in fp64 (exact for bf16 inputs) and divided by sqrt(d) as the reference
- * does; the row softmax over all n_k*s_k sampled keys is fp64.
- * workspace: psa_importance_workspace_bytes(...) bytes of device memory.
+ * Logits are the exact dot products of the bf16 rows, rounded once to fp64 (max reducer with
+ * s_k <= 32: int8-sliced tcgen05 GEMMs + exact corrections, psa_xlogits.cu; otherwise, for
+ * heads it cannot represent, or with PSA_IMP_FP64_ONLY: fp64 DMMA), divided by sqrt(d) as the
+ * reference does; the row softmax over all n_k*s_k sampled keys is fp64.
+ * workspace: psa_importance_workspace_bytes(batch*hq, batch*hkv, n_q, s_q, n_k, s_k) bytes.
  */
-size_t psa_importance_workspace_bytes(int64_t bhq, int n_q, int s_q, int n_k);
+size_t psa_importance_workspace_bytes(int64_t bhq, int64_t bkv, int n_q, int s_q, int n_k,
+                                      int s_k);
 int psa_importance_sampled(const void* q, const void* k, int64_t batch, int hq, int hkv,
                            int64_t n, int d, int b_q, int b_k, const int32_t* q_rows,
-                           const int32_t* k_rows, int s_q, int s_k, int reducer,
+                           const int32_t* k_rows, int s_q, int s_k, int reducer, int flags,
                            double* scores, void* workspace, void* stream);
 
 /*
@@ -84,13 +90,16 @@ int psa_importance_sampled(const void* q, const void* k, int64_t batch, int hq, 
  * column c has (p + c) % stride == 0 (antidiagonal_selection, importance.py:88-94); logits are
  * fp64 dot products (exact for bf16 inputs) times fl(1/sqrt(d)); row softmax over all picks,
  * probability mass per KV block, mean over the query block's rows.
+ * Logits as for psa_importance_sampled (int8-sliced tensor cores when b_k/stride <= 32).
  * Constraints: stride divides b_k, b_k / stride <= 64.  scores: fp64 [batch*hq, n_q, n_k].
- * workspace: psa_antidiag_workspace_bytes(batch*hq, n, b_k, stride) bytes (0 = invalid).
+ * workspace: psa_antidiag_workspace_bytes(batch*hq, batch*hkv, n, b_q, b_k, stride) bytes
+ * (0 = invalid geometry).
  */
-size_t psa_antidiag_workspace_bytes(int64_t bhq, int64_t n, int b_k, int stride);
+size_t psa_antidiag_workspace_bytes(int64_t bhq, int64_t bkv, int64_t n, int b_q, int b_k,
+                                    int stride);
 int psa_importance_antidiagonal(const void* q, const void* k, int64_t batch, int hq, int hkv,
-                                int64_t n, int d, int b_q, int b_k, int stride, double* scores,
-                                void* workspace, void* stream);
+                                int64_t n, int d, int b_q, int b_k, int stride, int flags,
+                                double* scores, void* workspace, void* stream);
 
 /*
  * K3 — level assignment + compact plan.  Replaces assign_threshold / binary_mask /

@@ -17,6 +17,7 @@ LIB_PATH = Path(__file__).with_name("libpsa.so")
 _lib = None
 
 PSA_OK, PSA_EINVAL, PSA_ENUMERIC, PSA_ECUDA = 0, -2, -4, -5
+PSA_IMP_FP64_ONLY = 1
 
 _SIGNATURES = {
     "psa_last_error": (ctypes.c_char_p, []),
@@ -25,13 +26,13 @@ _SIGNATURES = {
                                   c_void_p, c_void_p, c_void_p, c_void_p]),
     "psa_similarity_caps": (c_int, [c_void_p, c_int64, c_int64, c_int, c_int, c_int,
                                     c_void_p, c_void_p, c_void_p]),
-    "psa_importance_workspace_bytes": (c_size_t, [c_int64, c_int, c_int, c_int]),
+    "psa_importance_workspace_bytes": (c_size_t, [c_int64, c_int64, c_int, c_int, c_int, c_int]),
     "psa_importance_sampled": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int, c_int64, c_int,
                                        c_int, c_int, c_void_p, c_void_p, c_int, c_int, c_int,
-                                       c_void_p, c_void_p, c_void_p]),
-    "psa_antidiag_workspace_bytes": (c_size_t, [c_int64, c_int64, c_int, c_int]),
+                                       c_int, c_void_p, c_void_p, c_void_p]),
+    "psa_antidiag_workspace_bytes": (c_size_t, [c_int64, c_int64, c_int64, c_int, c_int, c_int]),
     "psa_importance_antidiagonal": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int, c_int64,
-                                            c_int, c_int, c_int, c_int, c_void_p, c_void_p,
+                                            c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p,
                                             c_void_p]),
     "psa_assign_levels": (c_int, [c_void_p, c_int64, c_int, c_int, c_int, c_int, c_int,
                                   c_void_p, c_void_p, c_int, c_void_p, c_int, c_int, c_int, c_int,

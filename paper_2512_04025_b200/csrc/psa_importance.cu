@@ -130,7 +130,8 @@ __global__ void __launch_bounds__(kImpThreads, 2)
                             int hq, int hkv, int64_t n, const int32_t* __restrict__ q_rows,
                             const int32_t* __restrict__ k_rows, int R, int s_k, int n_k,
                             double sqrt_d, double* __restrict__ M, double* __restrict__ mstat,
-                            double* __restrict__ lstat) {
+                            double* __restrict__ lstat, const int32_t* __restrict__ qflag,
+                            const int32_t* __restrict__ kflag) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   auto& sm = *reinterpret_cast<ImpSmem<D>*>(smem_raw);
   constexpr int kXld = kImpCols + 1;
@@ -139,6 +140,8 @@ __global__ void __launch_bounds__(kImpThreads, 2)
   const int bhq = blockIdx.y;
   const int b = bhq / hq, h = bhq % hq;
   const int hk = h / (hq / hkv);
+  // with flags: only the heads the int8 path (psa_xlogits.cu) handed over
+  if (qflag != nullptr && !(qflag[bhq] | kflag[b * hkv + hk])) return;
   const uint16_t* qh = q + static_cast<int64_t>(bhq) * n * D;
   const uint16_t* kh = k + (static_cast<int64_t>(b) * hkv + hk) * n * D;
   const int a0 = blockIdx.x * kImpRows;
@@ -268,9 +271,10 @@ template <int D>
 __global__ void __launch_bounds__(kImpThreads, 2)
     antidiag_stats_kernel(const uint16_t* __restrict__ q, const uint16_t* __restrict__ k,
                           int hq, int hkv, int64_t n, int b_q, int b_k, int stride, int n_k,
-                          double scale, int n_chunks, double* __restrict__ E,
+                          double scale, int bpc, int n_chunks, double* __restrict__ E,
                           double* __restrict__ Mc, double* __restrict__ mstat,
-                          double* __restrict__ lstat) {
+                          double* __restrict__ lstat, const int32_t* __restrict__ qflag,
+                          const int32_t* __restrict__ kflag) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   auto& sm = *reinterpret_cast<ImpSmem<D>*>(smem_raw);
   constexpr int kXld = kImpCols + 1;
@@ -286,6 +290,7 @@ __global__ void __launch_bounds__(kImpThreads, 2)
   const int bhq = blockIdx.y;
   const int b = bhq / hq, h = bhq % hq;
   const int hk = h / (hq / hkv);
+  if (qflag != nullptr && !(qflag[bhq] | kflag[b * hkv + hk])) return;
   const uint16_t* qh = q + static_cast<int64_t>(bhq) * n * D;
   const uint16_t* kh = k + (static_cast<int64_t>(b) * hkv + hk) * n * D;
   const int per = b_k / stride;
@@ -298,8 +303,7 @@ __global__ void __launch_bounds__(kImpThreads, 2)
     gather_rows_regs<D>(qh, qmap, a0, rows_here, buf);
     store_rows_bf16<D>(sm.qs, buf);
   }
-  const int bpc = kImpCols / per;  // whole KV blocks per chunk (per <= 64 checked on the host)
-  const int cw = bpc * per;
+  const int cw = bpc * per;  // whole KV blocks per chunk (cw <= 64 checked on the host)
   const int C = n_k * per;
 
   const int a_loc = threadIdx.x >> 2, quad = threadIdx.x & 3;
@@ -369,57 +373,63 @@ __global__ void __launch_bounds__(128) antidiag_finalize_kernel(
   }
 }
 
-static int antidiag_geometry(int b_k, int stride, int n_k, int* per, int* bpc, int* n_chunks) {
-  *per = b_k / stride;
-  *bpc = kImpCols / *per;
-  const int cw = *bpc * *per;
-  *n_chunks = (n_k * *per + cw - 1) / cw;
-  return 0;
+// Chunk geometry of the antidiagonal statistics: the int8 path's key tiles when it applies
+// (so the fp64 fallback heads produce identically laid-out chunk maxima), else 64-key chunks.
+struct AdGeom {
+  int per, bpc, n_chunks, c_max;
+  XlGeometry xl;
+};
+static AdGeom ad_geometry(int64_t bhq, int64_t bkv, int64_t n, int b_q, int b_k, int stride,
+                          bool allow_xl) {
+  AdGeom a{};
+  a.per = b_k / stride;
+  a.c_max = (b_q + stride - 1) / stride;
+  const int n_q = static_cast<int>(n / b_q), n_k = static_cast<int>(n / b_k);
+  a.xl = xl_geometry(bhq, bkv, n_q, n_k, stride, n_q * a.c_max, a.per);
+  a.xl.ok = a.xl.ok && allow_xl;
+  a.bpc = a.xl.ok ? a.xl.bpt : kImpCols / a.per;
+  a.n_chunks = (n_k + a.bpc - 1) / a.bpc;
+  return a;
 }
 
 template <int D>
-static int launch_antidiag(const void* q, const void* k, int64_t batch, int hq, int hkv,
-                           int64_t n, int b_q, int b_k, int stride, double* scores, void* ws,
-                           cudaStream_t s) {
+static int launch_antidiag_dmma(const void* q, const void* k, int64_t batch, int hq, int hkv,
+                                int64_t n, int b_q, int b_k, int stride, const AdGeom& g,
+                                double* E, double* Mc, double* mstat, double* lstat,
+                                const int32_t* qflag, const int32_t* kflag, cudaStream_t s) {
   const int64_t bhq = batch * hq;
   const int n_q = static_cast<int>(n / b_q), n_k = static_cast<int>(n / b_k);
-  int per, bpc, n_chunks;
-  antidiag_geometry(b_k, stride, n_k, &per, &bpc, &n_chunks);
-  double* E = static_cast<double*>(ws);
-  double* Mc = E + bhq * n * n_k;
-  double* mstat = Mc + bhq * n * n_chunks;
-  double* lstat = mstat + bhq * n;
   const size_t smem = sizeof(ImpSmem<D>);
   cudaFuncSetAttribute(antidiag_stats_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(smem));
-  const int c_max = (b_q + stride - 1) / stride;
-  dim3 grid((n_q * c_max + kImpRows - 1) / kImpRows, static_cast<unsigned>(bhq), stride);
+  dim3 grid((n_q * g.c_max + kImpRows - 1) / kImpRows, static_cast<unsigned>(bhq), stride);
   antidiag_stats_kernel<D><<<grid, kImpThreads, smem, s>>>(
       static_cast<const uint16_t*>(q), static_cast<const uint16_t*>(k), hq, hkv, n, b_q, b_k,
-      stride, n_k, 1.0 / sqrt(static_cast<double>(D)), n_chunks, E, Mc, mstat, lstat);
-  int rc = psa_check_launch("antidiag_stats_kernel");
-  if (rc) return rc;
-  antidiag_finalize_kernel<<<dim3(n_q, bhq), 128, 0, s>>>(E, Mc, mstat, lstat, n, b_q, n_q, n_k,
-                                                          bpc, n_chunks, scores);
-  return psa_check_launch("antidiag_finalize_kernel");
+      stride, n_k, 1.0 / sqrt(static_cast<double>(D)), g.bpc, g.n_chunks, E, Mc, mstat, lstat,
+      qflag, kflag);
+  return psa_check_launch("antidiag_stats_kernel");
 }
 
 }  // namespace psa
 
 using namespace psa;
 
-extern "C" size_t psa_antidiag_workspace_bytes(int64_t bhq, int64_t n, int b_k, int stride) {
-  if (stride < 1 || b_k % stride || b_k / stride > kImpCols || n % b_k) return 0;
-  int per, bpc, n_chunks;
-  const int n_k = static_cast<int>(n / b_k);
-  antidiag_geometry(b_k, stride, n_k, &per, &bpc, &n_chunks);
+static size_t ad_fp64_bytes(int64_t bhq, int64_t n, int n_k, int n_chunks) {
   return static_cast<size_t>(bhq * n * (n_k + n_chunks + 2)) * sizeof(double);
+}
+
+extern "C" size_t psa_antidiag_workspace_bytes(int64_t bhq, int64_t bkv, int64_t n, int b_q,
+                                               int b_k, int stride) {
+  if (stride < 1 || b_q < 1 || b_k % stride || b_k / stride > kImpCols || n % b_k || n % b_q)
+    return 0;
+  const AdGeom g = ad_geometry(bhq, bkv, n, b_q, b_k, stride, true);
+  return ad_fp64_bytes(bhq, n, static_cast<int>(n / b_k), g.n_chunks) + (g.xl.ok ? g.xl.bytes : 0);
 }
 
 extern "C" int psa_importance_antidiagonal(const void* q, const void* k, int64_t batch, int hq,
                                            int hkv, int64_t n, int d, int b_q, int b_k,
-                                           int stride, double* scores, void* workspace,
-                                           void* stream) {
+                                           int stride, int flags, double* scores,
+                                           void* workspace, void* stream) {
   PSA_CHECK_ARG(q && k && scores && workspace, "null pointer argument");
   PSA_CHECK_ARG(d == 64 || d == 128, "head_dim must be 64 or 128 for the sm_100a path");
   PSA_CHECK_ARG(hq >= 1 && hkv >= 1 && hq % hkv == 0, "query heads must be a multiple of kv heads");
@@ -428,25 +438,75 @@ extern "C" int psa_importance_antidiagonal(const void* q, const void* k, int64_t
   PSA_CHECK_ARG(b_k / stride <= kImpCols,
                 "k_block / stride > 64 is not supported by the sm_100a antidiagonal kernel");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (d == 128)
-    return launch_antidiag<128>(q, k, batch, hq, hkv, n, b_q, b_k, stride, scores, workspace, s);
-  return launch_antidiag<64>(q, k, batch, hq, hkv, n, b_q, b_k, stride, scores, workspace, s);
+  const int64_t bhq = batch * hq, bkv = batch * hkv;
+  const int n_q = static_cast<int>(n / b_q), n_k = static_cast<int>(n / b_k);
+  const AdGeom g = ad_geometry(bhq, bkv, n, b_q, b_k, stride, !(flags & PSA_IMP_FP64_ONLY));
+  double* E = static_cast<double*>(workspace);
+  double* Mc = E + bhq * n * n_k;
+  double* mstat = Mc + bhq * n * g.n_chunks;
+  double* lstat = mstat + bhq * n;
+  const int32_t* qflag = nullptr;
+  const int32_t* kflag = nullptr;
+  int rc = PSA_OK;
+  if (g.xl.ok) {
+    void* xws = static_cast<uint8_t*>(workspace) + ad_fp64_bytes(bhq, n, n_k, g.n_chunks);
+    rc = xl_antidiag(q, k, batch, hq, hkv, n, d, b_q, b_k, stride, g.xl, xws, E, Mc, mstat,
+                     lstat, s);
+    if (rc) return rc;
+    qflag = xl_qflags(g.xl, xws);
+    kflag = qflag + bhq;
+  }
+  rc = d == 128 ? launch_antidiag_dmma<128>(q, k, batch, hq, hkv, n, b_q, b_k, stride, g, E, Mc,
+                                            mstat, lstat, qflag, kflag, s)
+                : launch_antidiag_dmma<64>(q, k, batch, hq, hkv, n, b_q, b_k, stride, g, E, Mc,
+                                           mstat, lstat, qflag, kflag, s);
+  if (rc) return rc;
+  antidiag_finalize_kernel<<<dim3(n_q, bhq), 128, 0, s>>>(E, Mc, mstat, lstat, n, b_q, n_q, n_k,
+                                                          g.bpc, g.n_chunks, scores);
+  return psa_check_launch("antidiag_finalize_kernel");
 }
 
-extern "C" size_t psa_importance_workspace_bytes(int64_t bhq, int n_q, int s_q, int n_k) {
+static XlGeometry sampled_xl_geometry(int64_t bhq, int64_t bkv, int n_q, int s_q, int n_k,
+                                      int s_k, bool allow) {
+  XlGeometry g = xl_geometry(bhq, bkv, n_q, n_k, 1, n_q * s_q, s_k);
+  g.ok = g.ok && allow;
+  return g;
+}
+
+static size_t sampled_fp64_bytes(int64_t bhq, int n_q, int s_q, int n_k) {
   const int64_t R = static_cast<int64_t>(n_q) * s_q;
   return static_cast<size_t>(bhq * R * n_k + 2 * bhq * R) * sizeof(double);
+}
+
+extern "C" size_t psa_importance_workspace_bytes(int64_t bhq, int64_t bkv, int n_q, int s_q,
+                                                 int n_k, int s_k) {
+  const XlGeometry g = sampled_xl_geometry(bhq, bkv, n_q, s_q, n_k, s_k, true);
+  return sampled_fp64_bytes(bhq, n_q, s_q, n_k) + (g.ok ? g.bytes : 0);
 }
 
 template <int D>
 static int launch_importance(const void* q, const void* k, int64_t batch, int hq, int hkv,
                              int64_t n, const int32_t* q_rows, const int32_t* k_rows, int R,
-                             int s_q, int s_k, int n_q, int n_k, int reducer, double* scores,
-                             void* ws, cudaStream_t s) {
-  const int64_t bhq = batch * hq;
+                             int s_q, int s_k, int n_q, int n_k, int reducer, int flags,
+                             double* scores, void* ws, cudaStream_t s) {
+  const int64_t bhq = batch * hq, bkv = batch * hkv;
   double* M = static_cast<double*>(ws);
   double* mstat = M + bhq * R * n_k;
   double* lstat = mstat + bhq * R;
+  const int32_t* qflag = nullptr;
+  const int32_t* kflag = nullptr;
+  int rc = PSA_OK;
+  const XlGeometry g = sampled_xl_geometry(bhq, bkv, n_q, s_q, n_k, s_k,
+                                           reducer == 0 && !(flags & PSA_IMP_FP64_ONLY));
+  if (g.ok) {  // exact logits on the int8 tensor cores; DMMA only for the heads it flags
+    void* xws = static_cast<uint8_t*>(ws) + sampled_fp64_bytes(bhq, n_q, s_q, n_k);
+    rc = xl_sampled_max(q, k, batch, hq, hkv, n, D, static_cast<int>(n / n_q),
+                        static_cast<int>(n / n_k), q_rows, k_rows, s_q, s_k, g, xws, M, mstat,
+                        lstat, s);
+    if (rc) return rc;
+    qflag = xl_qflags(g, xws);
+    kflag = qflag + bhq;
+  }
   const size_t smem = sizeof(ImpSmem<D>);
   cudaFuncSetAttribute(importance_stats_kernel<D, false>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -457,12 +517,13 @@ static int launch_importance(const void* q, const void* k, int64_t batch, int hq
   auto* qq = static_cast<const uint16_t*>(q);
   auto* kk = static_cast<const uint16_t*>(k);
   importance_stats_kernel<D, false><<<grid, kImpThreads, smem, s>>>(
-      qq, kk, hq, hkv, n, q_rows, k_rows, R, s_k, n_k, sqrt_d, M, mstat, lstat);
-  int rc = psa_check_launch("importance_stats_kernel");
+      qq, kk, hq, hkv, n, q_rows, k_rows, R, s_k, n_k, sqrt_d, M, mstat, lstat, qflag, kflag);
+  rc = psa_check_launch("importance_stats_kernel");
   if (rc) return rc;
   if (reducer == 1) {
     importance_stats_kernel<D, true><<<grid, kImpThreads, smem, s>>>(
-        qq, kk, hq, hkv, n, q_rows, k_rows, R, s_k, n_k, sqrt_d, M, mstat, lstat);
+        qq, kk, hq, hkv, n, q_rows, k_rows, R, s_k, n_k, sqrt_d, M, mstat, lstat, nullptr,
+        nullptr);
     rc = psa_check_launch("importance_stats_kernel<mean>");
     if (rc) return rc;
     importance_finalize_kernel<true><<<dim3(n_q, bhq), 128, 0, s>>>(M, mstat, lstat, R, s_q, s_k,
@@ -477,8 +538,8 @@ static int launch_importance(const void* q, const void* k, int64_t batch, int hq
 extern "C" int psa_importance_sampled(const void* q, const void* k, int64_t batch, int hq,
                                       int hkv, int64_t n, int d, int b_q, int b_k,
                                       const int32_t* q_rows, const int32_t* k_rows, int s_q,
-                                      int s_k, int reducer, double* scores, void* workspace,
-                                      void* stream) {
+                                      int s_k, int reducer, int flags, double* scores,
+                                      void* workspace, void* stream) {
   PSA_CHECK_ARG(q && k && q_rows && k_rows && scores && workspace, "null pointer argument");
   PSA_CHECK_ARG(d == 64 || d == 128, "head_dim must be 64 or 128 for the sm_100a path");
   PSA_CHECK_ARG(hq >= 1 && hkv >= 1 && hq % hkv == 0, "query heads must be a multiple of kv heads");
@@ -492,7 +553,7 @@ extern "C" int psa_importance_sampled(const void* q, const void* k, int64_t batc
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (d == 128)
     return launch_importance<128>(q, k, batch, hq, hkv, n, q_rows, k_rows, R, s_q, s_k, n_q, n_k,
-                                  reducer, scores, workspace, s);
+                                  reducer, flags, scores, workspace, s);
   return launch_importance<64>(q, k, batch, hq, hkv, n, q_rows, k_rows, R, s_q, s_k, n_q, n_k,
-                               reducer, scores, workspace, s);
+                               reducer, flags, scores, workspace, s);
 }

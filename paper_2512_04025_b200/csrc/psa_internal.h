@@ -2,6 +2,7 @@
 // string, argument checks, launch checks, and small by-value parameter structs.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -24,6 +25,31 @@ struct LevelRule {  // thresholds (mode 0) or quantile rank counts (mode 1)
   int n_cuts;
   int mode;
 };
+
+// Exact int8-sliced importance logits (psa_xlogits.cu).
+struct XlGeometry {
+  bool ok;
+  int per, bpt, n_tiles, kp, rq_pad, classes;
+  size_t off_ks, off_qm, off_km, off_flags, bytes;
+};
+XlGeometry xl_geometry(int64_t bhq, int64_t bkv, int n_q, int n_k, int classes, int rows_per_class,
+                       int per);
+int xl_sampled_max(const void* q, const void* k, int64_t batch, int hq, int hkv, int64_t n, int d,
+                   int b_q, int b_k, const int32_t* q_rows, const int32_t* k_rows, int s_q,
+                   int s_k, const XlGeometry& g, void* ws, double* M, double* mstat,
+                   double* lstat, cudaStream_t s);
+int xl_antidiag(const void* q, const void* k, int64_t batch, int hq, int hkv, int64_t n, int d,
+                int b_q, int b_k, int stride, const XlGeometry& g, void* ws, double* E,
+                double* Mc, double* mstat, double* lstat, cudaStream_t s);
+// device flags [bhq] then [bkv]: heads the int8 path could not represent exactly
+const int32_t* xl_qflags(const XlGeometry& g, const void* ws);
+
+// cuTensorMapEncodeTiled from the driver (psa_attention.cu)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn get_encode_fn();
 
 }  // namespace psa
 

@@ -1,0 +1,619 @@
+// Exact fp64 importance logits on the int8 tensor cores (tcgen05 kind::i8), for K2/K2b.
+//
+// Both estimators of pkg/src/pyrattn/importance.py need fp64 logits of bf16 rows:
+//   importance_sampled      :52-85   fl(dot(q_a, k_b) / sqrt(d)) over sampled rows
+//   importance_antidiagonal :97-132  fl(dot(q_p, k_c) * fl(1/sqrt(d))) over strided picks
+// A dot product of bf16 vectors is an exact sum of 16-bit products, so BLAS (and the DMMA
+// kernels in psa_importance.cu) return it exactly whenever it fits in 53 bits. The FP64 pipe is
+// ~36 TFLOP/s; the int8 tensor cores are ~120x faster, so we compute the SAME exact value with
+// integer arithmetic (an Ozaki-style split):
+//
+//   every gathered row x is put on the grid 2^(E-20), E = floor(log2 max|x|):
+//     x = X * 2^(E-20) + r,  X integer, |X| < 2^21,  r = 0 unless |x_k| < 2^(E-13) ("tiny")
+//   X = d2 * 2^14 + d1 * 2^7 + d0 with int8 digits (d0, d1 in [0, 127], d2 in [-128, 127])
+//   dot(X, Y) = sum_{a,b} 2^(7(a+b)) * dot(x_a, y_b)        (9 int8 GEMMs, int32 exact)
+//
+// The 9 slice products accumulate into 5 int32 TMEM accumulators (one per weight class a+b);
+// the epilogue combines them in int64 (|dot(X,Y)| < 2^49: exact), converts exactly to fp64
+// and scales by 2^(Ex+Ey-40). Pairs involving tiny elements (at most 4 per row; ~3% of
+// Gaussian rows) add the exact fp64 correction sum_k (x_k y_k - xm_k ym_k) over the tiny
+// dimensions. Rows with more than 4 tiny elements (or non-finite values) mark their head for
+// the fp64 DMMA kernel instead, so the result is always the exact dot up to one final fp64
+// rounding. From the logits on, the epilogue is the DMMA kernels' arithmetic: per KV block the
+// max (sampled) or the numpy-ordered exp-sum (antidiagonal), and the online softmax (m, l).
+//
+// Kernel shape: one CTA per (head, residue class, 128 gathered query rows); 12 warps.
+//   warp 0  TMA: the 3 query slice tiles once, then 3 x (32 keys x 128 B) per key tile
+//   warp 1  MMA: 9 slice pairs x D/32 k-steps of tcgen05.mma.kind::i8 (M=128, N=32)
+//   warp 2  TMEM allocator (3 accumulator buffers x 5 classes x 32 columns)
+//   warps 4-11  epilogue, two groups taking alternate key tiles (their (m, l) merge at the end)
+#include "common.cuh"
+#include "psa_internal.h"
+
+namespace psa {
+
+constexpr int kXlSlices = 3;
+constexpr int kXlClasses = 2 * kXlSlices - 1;
+constexpr int kXlRowBytes = 128;  // one slice row: K-major, one 128-byte swizzle atom wide
+constexpr int kXlQRows = 128;     // MMA M
+constexpr int kXlKeys = 32;       // MMA N = keys per tile
+constexpr int kXlStages = 4;
+constexpr int kXlAccBufs = 3;
+constexpr int kXlMaxTiny = 4;
+constexpr int kXlThreads = 384;
+constexpr int kXlEpiThreads = 256;
+constexpr int kXlGridShift = 20;  // X = x * 2^(20 - E), |X| < 2^21
+
+struct XlMeta {
+  int32_t e;      // row exponent E (0 for an all-zero row)
+  uint32_t tiny;  // count << 28 | four 7-bit dimensions of the tiny elements
+};
+
+// ------------------------------------------------------------------ row slicer
+// Packed row p of a (head, class) set: p = g * G + j holds element g * cw + j (j < cw) of the
+// set, else zeros. Keys use G = 32 (tiles hold whole KV blocks), queries G = cw = padded rows.
+struct XlPack {
+  int G, cw, total, pad_rows;
+};
+
+template <int D, class Rows>
+__global__ void __launch_bounds__(256) xl_slice_kernel(const uint16_t* __restrict__ src,
+                                                       int64_t n, Rows rows_base, int classes,
+                                                       int stride, int block, XlPack pk,
+                                                       int8_t* __restrict__ slices,
+                                                       XlMeta* __restrict__ meta,
+                                                       int32_t* __restrict__ flag) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int p = blockIdx.x * 8 + warp;
+  if (p >= pk.pad_rows) return;
+  const int64_t bh = blockIdx.y;
+  const int cls = blockIdx.z;
+  Rows rows = rows_base;
+  rows.set_class(cls, stride, block);
+  const int g = p / pk.G, j = p % pk.G;
+  const int idx = g * pk.cw + j;
+  const bool valid = j < pk.cw && idx < rows.count(pk.total);
+  const int64_t set = (bh * classes + cls);
+  int8_t* dst = slices + set * kXlSlices * static_cast<int64_t>(pk.pad_rows) * kXlRowBytes;
+
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  if (valid) {
+    const uint16_t* row = src + (bh * n + rows(idx)) * D;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int c = lane * 4 + e;
+      if (c < D) v[e] = static_cast<double>(__uint_as_float(static_cast<uint32_t>(row[c]) << 16));
+    }
+  }
+  double amax = 0.0;
+  bool finite = true;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    amax = fmax(amax, fabs(v[e]));
+    finite = finite && isfinite(v[e]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  finite = __all_sync(0xffffffffu, finite);
+  const int E = (amax > 0.0 && finite) ? ilogb(amax) : 0;
+  const double up = ldexp(1.0, kXlGridShift - E);
+  uint32_t d[3] = {0u, 0u, 0u};
+  unsigned tiny_bits = 0;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const double xf = v[e] * up;
+    const double xt = trunc(xf);
+    if (finite && xt != xf) tiny_bits |= 1u << e;
+    const int X = finite ? static_cast<int>(xt) : 0;
+    d[0] |= static_cast<uint32_t>(X & 127) << (8 * e);
+    d[1] |= static_cast<uint32_t>((X >> 7) & 127) << (8 * e);
+    d[2] |= static_cast<uint32_t>((X >> 14) & 0xFF) << (8 * e);
+  }
+#pragma unroll
+  for (int s = 0; s < kXlSlices; ++s)
+    reinterpret_cast<uint32_t*>(dst + (static_cast<int64_t>(s) * pk.pad_rows + p) * kXlRowBytes)[lane] = d[s];
+  // tiny elements: at most kXlMaxTiny per row, else the head goes to the fp64 fallback
+  const int cnt = __popc(tiny_bits);
+  int before = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, before, o);
+    if (lane >= o) before += y;
+  }
+  const int total = __shfl_sync(0xffffffffu, before, 31);
+  before -= cnt;
+  uint32_t dims = 0;
+  int slot = before;
+#pragma unroll
+  for (int e = 0; e < 4; ++e)
+    if ((tiny_bits >> e) & 1u) {
+      if (slot < kXlMaxTiny) dims |= static_cast<uint32_t>(lane * 4 + e) << (7 * slot);
+      ++slot;
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dims |= __shfl_xor_sync(0xffffffffu, dims, o);
+  if (lane == 0) {
+    XlMeta m;
+    m.e = E;
+    m.tiny = (static_cast<uint32_t>(min(total, 7)) << 28) | dims;
+    meta[set * pk.pad_rows + p] = m;
+    if (valid && (total > kXlMaxTiny || !finite)) atomicOr(flag + bh, 1);
+  }
+}
+
+// Row maps (queries and keys of one class). count(total) = elements in the class.
+struct XlTableRows {  // sampled rows (host table of the reference's generator), one class
+  const int32_t* rows;
+  PSA_DEV void set_class(int, int, int) {}
+  PSA_DEV int count(int total) const { return total; }
+  PSA_DEV int64_t operator()(int a) const { return rows[a]; }
+};
+struct XlQueryClass {  // antidiagonal query rows p = r (mod stride) of every query block
+  int r, c_r, block, stride, n_blocks;
+  PSA_DEV void set_class(int cls, int stride_, int block_) {
+    r = cls;
+    stride = stride_;
+    block = block_;
+    c_r = r < block ? (block - r + stride - 1) / stride : 0;
+  }
+  PSA_DEV int count(int) const { return n_blocks * c_r; }
+  PSA_DEV int64_t operator()(int a) const {
+    return static_cast<int64_t>(a / c_r) * block + r + (a % c_r) * stride;
+  }
+};
+struct XlKeyClass {  // antidiagonal key columns c = kr (mod stride) of every KV block
+  int kr, per, block, stride, n_blocks;
+  PSA_DEV void set_class(int cls, int stride_, int block_) {
+    kr = cls;
+    stride = stride_;
+    block = block_;
+    per = block / stride;
+  }
+  PSA_DEV int count(int) const { return n_blocks * per; }
+  PSA_DEV int64_t operator()(int a) const {
+    return static_cast<int64_t>(a / per) * block + kr + (a % per) * stride;
+  }
+};
+
+// ------------------------------------------------------------------ stats kernel
+enum XlMode { kXlMax = 0, kXlAntidiag = 1 };
+
+struct XlParams {
+  int64_t n;
+  int hq, hkv, classes, stride, b_q, b_k, n_q, n_k;
+  int r_total, rq_pad, kp, n_tiles, per, bpt;
+  double sqrt_d, inv_sqrt_d, scale;
+  const uint16_t* q;
+  const uint16_t* k;
+  const int32_t* q_rows;  // sampled tables (MAX mode)
+  const int32_t* k_rows;
+  const XlMeta* qmeta;
+  const XlMeta* kmeta;
+  const int32_t* qflag;
+  const int32_t* kflag;
+  double* M;      // MAX: block maxima [bhq][R][n_k];  ANTIDIAG: E [bhq][n][n_k]
+  double* Mc;     // ANTIDIAG: chunk maxima [bhq][n][n_tiles]
+  double* mstat;  // [bhq][R or n]
+  double* lstat;
+};
+
+struct XlMaps {
+  CUtensorMap qs;
+  CUtensorMap ks;
+};
+
+template <int D>
+struct XlSmem {
+  uint8_t q[kXlSlices][kXlQRows * kXlRowBytes];
+  uint8_t k[kXlStages][kXlSlices][kXlKeys * kXlRowBytes];
+  double dots[kXlKeys][kXlEpiThreads];
+  double red_m[kXlQRows], red_l[kXlQRows];
+  uint64_t q_full;
+  uint64_t k_full[kXlStages], k_empty[kXlStages];
+  uint64_t acc_full[kXlAccBufs], acc_empty[kXlAccBufs];
+  uint32_t tmem_base;
+};
+
+PSA_DEV void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                 "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr)
+               : "memory");
+}
+PSA_DEV void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+PSA_DEV void mma_i8_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                       uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// kind::i8 instruction descriptor: s8 x s8 -> s32, both K-major.
+constexpr uint32_t xl_idesc(int M, int N) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
+         (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+PSA_DEV double pow2(int k) {  // exact 2^k for the normal range
+  return __longlong_as_double(static_cast<long long>(k + 1023) << 52);
+}
+// value of x on row grid E (the part the int8 slices carry exactly)
+PSA_DEV double grid_part(double x, int E) {
+  return trunc(x * pow2(kXlGridShift - E)) * pow2(E - kXlGridShift);
+}
+PSA_DEV double bf16_at(const uint16_t* row, int c) {
+  return static_cast<double>(__uint_as_float(static_cast<uint32_t>(row[c]) << 16));
+}
+// exact fp64 correction of dot(x, y) for the tiny dimensions of either row
+PSA_DEV double tiny_correction(const uint16_t* xr, const uint16_t* yr, XlMeta mx, XlMeta my) {
+  double c = 0.0;
+  const int nx = min(static_cast<int>(mx.tiny >> 28), kXlMaxTiny);
+  const int ny = min(static_cast<int>(my.tiny >> 28), kXlMaxTiny);
+  for (int s = 0; s < nx + ny; ++s) {
+    const int dim = s < nx ? (mx.tiny >> (7 * s)) & 127 : (my.tiny >> (7 * (s - nx))) & 127;
+    bool dup = false;
+    for (int u = 0; u < nx && s >= nx; ++u) dup = dup || (((mx.tiny >> (7 * u)) & 127) == dim);
+    if (dup) continue;
+    const double x = bf16_at(xr, dim), y = bf16_at(yr, dim);
+    c = __dadd_rn(c, __fma_rn(x, y, -(grid_part(x, mx.e) * grid_part(y, my.e))));
+  }
+  return c;
+}
+
+template <int D, class QRows, class KRows, int MODE>
+__global__ void __launch_bounds__(kXlThreads, 1)
+    xl_stats_kernel(const __grid_constant__ XlMaps maps, const XlParams p, QRows qrows0,
+                    KRows krows0) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  auto& sm = *reinterpret_cast<XlSmem<D>*>(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qt = blockIdx.x;
+  const int bhq = blockIdx.y;
+  const int cls = blockIdx.z;
+  const int b = bhq / p.hq, h = bhq % p.hq;
+  const int bkv = b * p.hkv + h / (p.hq / p.hkv);
+  if (p.qflag[bhq] | p.kflag[bkv]) return;  // head handled by the fp64 DMMA kernel
+  QRows qrows = qrows0;
+  qrows.set_class(cls, p.stride, p.b_q);
+  const int rows_valid = qrows.count(p.r_total);  // gathered query rows of this class
+  const int kcls = MODE == kXlAntidiag ? (p.stride - cls % p.stride) % p.stride : 0;
+  KRows krows = krows0;
+  krows.set_class(kcls, p.stride, p.b_k);
+  if (qt * kXlQRows >= rows_valid) return;
+  const int T = p.n_tiles;
+
+  if (threadIdx.x == 0) {
+    if (smem_u32(smem_raw) & 1023u) __trap();
+    mbar_init(&sm.q_full, 1);
+    for (int s = 0; s < kXlStages; ++s) {
+      mbar_init(&sm.k_full[s], 1);
+      mbar_init(&sm.k_empty[s], 1);
+    }
+    for (int s = 0; s < kXlAccBufs; ++s) {
+      mbar_init(&sm.acc_full[s], 1);
+      mbar_init(&sm.acc_empty[s], kXlEpiThreads / 2);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&maps.qs);
+    tma_prefetch_desc(&maps.ks);
+  }
+  if (warp == 2) {
+    tmem_alloc(&sm.tmem_base, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const int qset = (bhq * p.classes + cls) * kXlSlices;
+      mbar_arrive_expect_tx(&sm.q_full, kXlSlices * kXlQRows * kXlRowBytes);
+      for (int a = 0; a < kXlSlices; ++a)
+        tma_load_2d(&maps.qs, &sm.q_full, sm.q[a], 0, (qset + a) * p.rq_pad + qt * kXlQRows);
+      const int kset = (bkv * p.classes + kcls) * kXlSlices;
+      for (int t = 0; t < T; ++t) {
+        const int s = t % kXlStages;
+        if (t >= kXlStages) mbar_wait(&sm.k_empty[s], ((t / kXlStages) - 1) & 1);
+        mbar_arrive_expect_tx(&sm.k_full[s], kXlSlices * kXlKeys * kXlRowBytes);
+        for (int bb = 0; bb < kXlSlices; ++bb)
+          tma_load_2d(&maps.ks, &sm.k_full[s], sm.k[s][bb], 0, (kset + bb) * p.kp + t * kXlKeys);
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = xl_idesc(kXlQRows, kXlKeys);
+    mbar_wait(&sm.q_full, 0);
+    tc_fence_after();
+    for (int t = 0; t < T; ++t) {
+      const int s = t % kXlStages, ab = t % kXlAccBufs;
+      mbar_wait(&sm.k_full[s], (t / kXlStages) & 1);
+      if (t >= kXlAccBufs) mbar_wait(&sm.acc_empty[ab], ((t / kXlAccBufs) - 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        bool started[kXlClasses] = {false, false, false, false, false};
+#pragma unroll
+        for (int a = 0; a < kXlSlices; ++a)
+#pragma unroll
+          for (int bb = 0; bb < kXlSlices; ++bb) {
+            const int c = a + bb;
+            const uint64_t ad = umma_desc_sw128(smem_u32(sm.q[a]), 16, 1024);
+            const uint64_t bd = umma_desc_sw128(smem_u32(sm.k[s][bb]), 16, 1024);
+            const uint32_t dcol = tmem + ab * (kXlClasses * kXlKeys) + c * kXlKeys;
+#pragma unroll
+            for (int kk = 0; kk < D / 32; ++kk) {
+              mma_i8_ss(dcol, ad + ((kk * 32) >> 4), bd + ((kk * 32) >> 4), idesc,
+                        (started[c] || kk > 0) ? 1u : 0u);
+            }
+            started[c] = true;
+          }
+        mma_commit(&sm.k_empty[s]);
+        mma_commit(&sm.acc_full[ab]);
+      }
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    const int e_tid = threadIdx.x - 128;
+    const int grp = (warp - 4) >> 2;
+    const int wq = warp & 3;
+    const int row = wq * 32 + lane;
+    const int a = qt * kXlQRows + row;  // gathered query row of this class
+    const bool row_ok = a < rows_valid;
+    const int qset = bhq * p.classes + cls;
+    const XlMeta qm = p.qmeta[static_cast<int64_t>(qset) * p.rq_pad + a];
+    const bool q_tiny = (qm.tiny >> 28) != 0;
+    const int64_t qsrc = row_ok ? qrows(a) : 0;  // row inside the head
+    const uint16_t* qrow_ptr = p.q + (static_cast<int64_t>(bhq) * p.n + qsrc) * D;
+    const XlMeta* kmeta = p.kmeta + static_cast<int64_t>(bkv * p.classes + kcls) * p.kp;
+    const uint16_t* kbase = p.k + static_cast<int64_t>(bkv) * p.n * D;
+    const uint32_t t_lane = tmem + (static_cast<uint32_t>(wq * 32) << 16);
+    double* dots = &sm.dots[0][e_tid];
+    const int cw = p.bpt * p.per;
+    const int64_t out_row = MODE == kXlMax ? static_cast<int64_t>(bhq) * rows_valid + a
+                                           : static_cast<int64_t>(bhq) * p.n + qsrc;
+    double m_run = -INFINITY, l_run = 0.0;
+
+    for (int t = grp; t < T; t += 2) {
+      const int ab = t % kXlAccBufs;
+      const int j0 = t * p.bpt;  // first KV block of the tile
+      const int nb = min(p.bpt, p.n_k - j0);
+      const int nvalid = nb * p.per;
+      mbar_wait(&sm.acc_full[ab], (t / kXlAccBufs) & 1);
+      tc_fence_after();
+      const XlMeta* km = kmeta + t * kXlKeys;
+#pragma unroll
+      for (int c8 = 0; c8 < kXlKeys / 8; ++c8) {
+        uint32_t cv[kXlClasses][8];
+#pragma unroll
+        for (int c = 0; c < kXlClasses; ++c)
+          tmem_ld8(t_lane + ab * (kXlClasses * kXlKeys) + c * kXlKeys + c8 * 8, cv[c]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int j = c8 * 8 + e;
+          long long v = static_cast<int>(cv[0][e]);
+          v += static_cast<long long>(static_cast<int>(cv[1][e])) << 7;
+          v += static_cast<long long>(static_cast<int>(cv[2][e])) << 14;
+          v += static_cast<long long>(static_cast<int>(cv[3][e])) << 21;
+          v += static_cast<long long>(static_cast<int>(cv[4][e])) << 28;
+          // exact int64 -> fp64 for |v| < 2^51
+          const double vd = __dsub_rn(__longlong_as_double(v + 0x4338000000000000LL),
+                                      6755399441055744.0);
+          const XlMeta kmj = km[j];
+          double dot = vd * pow2(qm.e + kmj.e - 2 * kXlGridShift);
+          if ((q_tiny || (kmj.tiny >> 28) != 0) && j < nvalid && row_ok) {
+            const uint16_t* krow = kbase + krows(t * cw + j) * D;  // tile t: elements t*cw..
+            dot = __dadd_rn(dot, tiny_correction(qrow_ptr, krow, qm, kmj));
+          }
+          dots[j * kXlEpiThreads] = dot;
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&sm.acc_empty[ab]);
+
+      if (MODE == kXlMax) {
+        double lmax = -INFINITY;
+        for (int bb = 0; bb < nb; ++bb) {
+          double bm = -INFINITY;
+          for (int u = 0; u < p.per; ++u) bm = fmax(bm, dots[(bb * p.per + u) * kXlEpiThreads]);
+          bm = __ddiv_rn(bm, p.sqrt_d);  // importance.py:80 (one IEEE division per block)
+          lmax = fmax(lmax, bm);
+          if (row_ok) p.M[out_row * p.n_k + j0 + bb] = bm;
+        }
+        const double m_new = fmax(m_run, lmax);
+        double part = 0.0;
+        for (int u = 0; u < nvalid; ++u)
+          part = __dadd_rn(part, exp(__fma_rn(dots[u * kXlEpiThreads], p.inv_sqrt_d, -m_new)));
+        l_run = __dadd_rn(__dmul_rn(l_run, exp(__dsub_rn(m_run, m_new))), part);
+        m_run = m_new;
+      } else {
+        double cmax = -INFINITY;
+        for (int u = 0; u < nvalid; ++u) cmax = fmax(cmax, dots[u * kXlEpiThreads]);
+        const double m_new = fmax(m_run, __dmul_rn(cmax, p.scale));
+        double part = 0.0;
+        for (int bb = 0; bb < nb; ++bb) {
+          const double* xb = dots + bb * p.per * kXlEpiThreads;
+          const double e = np_pairwise_sum_fn(p.per, [&](int u) {
+            return exp(__dsub_rn(__dmul_rn(xb[u * kXlEpiThreads], p.scale), m_new));
+          });
+          part = __dadd_rn(part, e);
+          if (row_ok) p.M[out_row * p.n_k + j0 + bb] = e;
+        }
+        l_run = __dadd_rn(__dmul_rn(l_run, exp(__dsub_rn(m_run, m_new))), part);
+        m_run = m_new;
+        if (row_ok) p.Mc[out_row * p.n_tiles + t] = m_new;
+      }
+    }
+    // merge the two groups' running (m, l)
+    if (grp == 1) {
+      sm.red_m[row] = m_run;
+      sm.red_l[row] = l_run;
+    }
+    named_bar_sync(1, kXlEpiThreads);
+    if (grp == 0 && row_ok) {
+      const double m1 = sm.red_m[row], l1 = sm.red_l[row];
+      const double m = fmax(m_run, m1);
+      const double l = __dadd_rn(__dmul_rn(l_run, exp(__dsub_rn(m_run, m))),
+                                 __dmul_rn(l1, exp(__dsub_rn(m1, m))));
+      p.mstat[out_row] = m;
+      p.lstat[out_row] = l;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+static int xl_encode(CUtensorMap* m, const void* base, uint64_t rows, uint32_t box_rows) {
+  EncodeTiledFn fn = get_encode_fn();
+  if (fn == nullptr) return psa_fail(PSA_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(kXlRowBytes), rows};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(kXlRowBytes)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(kXlRowBytes), box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return psa_fail(PSA_ECUDA, "cuTensorMapEncodeTiled (int8) failed (%d)", (int)r);
+  return PSA_OK;
+}
+
+XlGeometry xl_geometry(int64_t bhq, int64_t bkv, int n_q, int n_k, int classes, int rows_per_class,
+                       int per) {
+  XlGeometry g{};
+  g.ok = per >= 1 && per <= kXlKeys;
+  if (!g.ok) return g;
+  g.per = per;
+  g.bpt = kXlKeys / per;
+  g.n_tiles = (n_k + g.bpt - 1) / g.bpt;
+  g.kp = g.n_tiles * kXlKeys;
+  g.rq_pad = (rows_per_class + kXlQRows - 1) / kXlQRows * kXlQRows;
+  g.classes = classes;
+  const size_t qs = static_cast<size_t>(bhq) * classes * kXlSlices * g.rq_pad * kXlRowBytes;
+  const size_t ks = static_cast<size_t>(bkv) * classes * kXlSlices * g.kp * kXlRowBytes;
+  const size_t qm = static_cast<size_t>(bhq) * classes * g.rq_pad * sizeof(XlMeta);
+  const size_t km = static_cast<size_t>(bkv) * classes * g.kp * sizeof(XlMeta);
+  g.off_ks = qs;
+  g.off_qm = g.off_ks + ks;
+  g.off_km = g.off_qm + qm;
+  g.off_flags = g.off_km + km;
+  g.bytes = g.off_flags + static_cast<size_t>(bhq + bkv) * sizeof(int32_t);
+  g.bytes = (g.bytes + 255) / 256 * 256;
+  return g;
+}
+
+template <int D, int MODE, class QR, class KR>
+static int xl_launch(const void* q, const void* k, int64_t batch, int hq, int hkv, int64_t n,
+                     int b_q, int b_k, int stride, const XlGeometry& g, QR qr, KR kr,
+                     int q_total, int k_total, void* ws, double* M, double* Mc, double* mstat,
+                     double* lstat, cudaStream_t s) {
+  const int64_t bhq = batch * hq, bkv = batch * hkv;
+  auto* base = static_cast<uint8_t*>(ws);
+  auto* qs = reinterpret_cast<int8_t*>(base);
+  auto* ks = reinterpret_cast<int8_t*>(base + g.off_ks);
+  auto* qm = reinterpret_cast<XlMeta*>(base + g.off_qm);
+  auto* km = reinterpret_cast<XlMeta*>(base + g.off_km);
+  auto* qflag = reinterpret_cast<int32_t*>(base + g.off_flags);
+  int32_t* kflag = qflag + bhq;
+  cudaMemsetAsync(qflag, 0, static_cast<size_t>(bhq + bkv) * sizeof(int32_t), s);
+  const auto* qq = static_cast<const uint16_t*>(q);
+  const auto* kk = static_cast<const uint16_t*>(k);
+  XlPack qp{g.rq_pad, g.rq_pad, q_total, g.rq_pad};
+  xl_slice_kernel<D, QR><<<dim3((g.rq_pad + 7) / 8, bhq, g.classes), 256, 0, s>>>(
+      qq, n, qr, g.classes, stride, b_q, qp, qs, qm, qflag);
+  int rc = psa_check_launch("xl_slice_kernel<q>");
+  if (rc) return rc;
+  XlPack kp{kXlKeys, g.bpt * g.per, k_total, g.kp};
+  xl_slice_kernel<D, KR><<<dim3((g.kp + 7) / 8, bkv, g.classes), 256, 0, s>>>(
+      kk, n, kr, g.classes, stride, b_k, kp, ks, km, kflag);
+  rc = psa_check_launch("xl_slice_kernel<k>");
+  if (rc) return rc;
+
+  XlMaps maps;
+  memset(&maps, 0, sizeof(maps));
+  rc = xl_encode(&maps.qs, qs, static_cast<uint64_t>(bhq) * g.classes * kXlSlices * g.rq_pad,
+                 kXlQRows);
+  if (rc) return rc;
+  rc = xl_encode(&maps.ks, ks, static_cast<uint64_t>(bkv) * g.classes * kXlSlices * g.kp, kXlKeys);
+  if (rc) return rc;
+  XlParams p{};
+  p.n = n;
+  p.hq = hq;
+  p.hkv = hkv;
+  p.classes = g.classes;
+  p.stride = stride;
+  p.b_q = b_q;
+  p.b_k = b_k;
+  p.n_q = static_cast<int>(n / b_q);
+  p.n_k = static_cast<int>(n / b_k);
+  p.r_total = q_total;
+  p.rq_pad = g.rq_pad;
+  p.kp = g.kp;
+  p.n_tiles = g.n_tiles;
+  p.per = g.per;
+  p.bpt = g.bpt;
+  p.sqrt_d = sqrt(static_cast<double>(D));
+  p.inv_sqrt_d = 1.0 / p.sqrt_d;
+  p.scale = 1.0 / sqrt(static_cast<double>(D));
+  p.q = qq;
+  p.k = kk;
+  p.qmeta = qm;
+  p.kmeta = km;
+  p.qflag = qflag;
+  p.kflag = kflag;
+  p.M = M;
+  p.Mc = Mc;
+  p.mstat = mstat;
+  p.lstat = lstat;
+  const size_t smem = sizeof(XlSmem<D>);
+  auto kern = xl_stats_kernel<D, QR, KR, MODE>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  kern<<<dim3(g.rq_pad / kXlQRows, bhq, g.classes), kXlThreads, smem, s>>>(maps, p, qr, kr);
+  return psa_check_launch("xl_stats_kernel");
+}
+
+int xl_sampled_max(const void* q, const void* k, int64_t batch, int hq, int hkv, int64_t n, int d,
+                   int b_q, int b_k, const int32_t* q_rows, const int32_t* k_rows, int s_q,
+                   int s_k, const XlGeometry& g, void* ws, double* M, double* mstat,
+                   double* lstat, cudaStream_t s) {
+  const int n_q = static_cast<int>(n / b_q), n_k = static_cast<int>(n / b_k);
+  XlTableRows qr{q_rows}, kr{k_rows};
+  if (d == 128)
+    return xl_launch<128, kXlMax>(q, k, batch, hq, hkv, n, b_q, b_k, 1, g, qr, kr, n_q * s_q,
+                                  n_k * s_k, ws, M, nullptr, mstat, lstat, s);
+  return xl_launch<64, kXlMax>(q, k, batch, hq, hkv, n, b_q, b_k, 1, g, qr, kr, n_q * s_q,
+                               n_k * s_k, ws, M, nullptr, mstat, lstat, s);
+}
+
+int xl_antidiag(const void* q, const void* k, int64_t batch, int hq, int hkv, int64_t n, int d,
+                int b_q, int b_k, int stride, const XlGeometry& g, void* ws, double* E,
+                double* Mc, double* mstat, double* lstat, cudaStream_t s) {
+  const int n_q = static_cast<int>(n / b_q), n_k = static_cast<int>(n / b_k);
+  XlQueryClass qr{};
+  qr.n_blocks = n_q;
+  XlKeyClass kr{};
+  kr.n_blocks = n_k;
+  if (d == 128)
+    return xl_launch<128, kXlAntidiag>(q, k, batch, hq, hkv, n, b_q, b_k, stride, g, qr, kr, 0, 0,
+                                       ws, E, Mc, mstat, lstat, s);
+  return xl_launch<64, kXlAntidiag>(q, k, batch, hq, hkv, n, b_q, b_k, stride, g, qr, kr, 0, 0,
+                                    ws, E, Mc, mstat, lstat, s);
+}
+
+const int32_t* xl_qflags(const XlGeometry& g, const void* ws) {
+  return reinterpret_cast<const int32_t*>(static_cast<const uint8_t*>(ws) + g.off_flags);
+}
+
+}  // namespace psa

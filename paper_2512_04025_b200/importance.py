@@ -44,9 +44,17 @@ def sample_tables(layout: BlockLayout, cfg: SamplerConfig, device) -> tuple:
     return hit
 
 
+def _flags(fp64_only: bool) -> int:
+    return _lib.PSA_IMP_FP64_ONLY if fp64_only else 0
+
+
 def importance_scores(q4: torch.Tensor, k4: torch.Tensor, layout: BlockLayout,
-                      cfg: SamplerConfig, reducer: str = "max") -> torch.Tensor:
-    """fp64 scores [B, Hq, n_q, n_k] from bf16 [B, H, N, d] device tensors."""
+                      cfg: SamplerConfig, reducer: str = "max",
+                      fp64_only: bool = False) -> torch.Tensor:
+    """fp64 scores [B, Hq, n_q, n_k] from bf16 [B, H, N, d] device tensors.
+
+    Logits are exact (int8-sliced tensor cores, psa_xlogits.cu); ``fp64_only`` forces the fp64
+    DMMA kernel instead (same values; used to cross-check the two paths)."""
     if reducer not in ("max", "mean"):
         raise ValidationError(f"reducer must be 'max' or 'mean', got {reducer!r}")
     cfg.validate(layout)
@@ -59,14 +67,15 @@ def importance_scores(q4: torch.Tensor, k4: torch.Tensor, layout: BlockLayout,
     dev = q4.device
     q_rows, k_rows = sample_tables(layout, cfg, dev)
     lib = _lib.load()
-    ws_bytes = lib.psa_importance_workspace_bytes(B * Hq, layout.n_q, cfg.s_q, layout.n_k)
+    ws_bytes = lib.psa_importance_workspace_bytes(B * Hq, B * Hkv, layout.n_q, cfg.s_q,
+                                                  layout.n_k, cfg.s_k)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     scores = torch.empty(B, Hq, layout.n_q, layout.n_k, dtype=torch.float64, device=dev)
     rc = lib.psa_importance_sampled(q4.data_ptr(), k4.data_ptr(), B, Hq, Hkv, n, d,
                                     layout.q_block, layout.k_block, q_rows.data_ptr(),
                                     k_rows.data_ptr(), cfg.s_q, cfg.s_k,
-                                    0 if reducer == "max" else 1, scores.data_ptr(),
-                                    ws.data_ptr(), stream_handle(dev))
+                                    0 if reducer == "max" else 1, _flags(fp64_only),
+                                    scores.data_ptr(), ws.data_ptr(), stream_handle(dev))
     _lib.check(rc, "psa_importance_sampled")
     return scores
 
@@ -95,7 +104,7 @@ def antidiagonal_selection(b_q: int, b_k: int, stride: int) -> torch.Tensor:
 
 
 def antidiagonal_scores(q4: torch.Tensor, k4: torch.Tensor, layout: BlockLayout,
-                        stride: int) -> torch.Tensor:
+                        stride: int, fp64_only: bool = False) -> torch.Tensor:
     """fp64 antidiagonal scores [B, Hq, n_q, n_k] from bf16 [B, H, N, d] device tensors."""
     if stride is None or int(stride) < 1 or layout.k_block % int(stride):
         raise ValidationError(f"stride {stride} must divide k_block {layout.k_block}")
@@ -109,12 +118,14 @@ def antidiagonal_scores(q4: torch.Tensor, k4: torch.Tensor, layout: BlockLayout,
         raise ValidationError(f"query heads {Hq} not a multiple of kv heads {Hkv}")
     dev = q4.device
     lib = _lib.load()
-    ws = torch.empty(lib.psa_antidiag_workspace_bytes(B * Hq, n, layout.k_block, stride),
+    ws = torch.empty(lib.psa_antidiag_workspace_bytes(B * Hq, B * Hkv, n, layout.q_block,
+                                                      layout.k_block, stride),
                      dtype=torch.uint8, device=dev)
     scores = torch.empty(B, Hq, layout.n_q, layout.n_k, dtype=torch.float64, device=dev)
     rc = lib.psa_importance_antidiagonal(q4.data_ptr(), k4.data_ptr(), B, Hq, Hkv, n, d,
                                          layout.q_block, layout.k_block, stride,
-                                         scores.data_ptr(), ws.data_ptr(), stream_handle(dev))
+                                         _flags(fp64_only), scores.data_ptr(), ws.data_ptr(),
+                                         stream_handle(dev))
     _lib.check(rc, "psa_importance_antidiagonal")
     return scores
 

@@ -316,3 +316,52 @@ def test_staged_host_path_bit_identical(hq, hkv, causal, per_group):
     assert host.level_counts == dev.plan.level_counts.cpu().tolist()
     assert host.skipped_rows() == dev.skipped_rows()
     assert host.sparsity().rho_bar == dev.sparsity().rho_bar
+
+
+# ------------------------------------------------------------------ exact int8-sliced logits
+def _with_tiny(x, rng, rows, per_row):
+    """Scale `per_row` random entries of the given rows by 2^-20 (elements below the int8 slice
+    grid: exercises the exact tiny-element correction, or the fp64 fallback past 4 per row)."""
+    x = x.copy()
+    for r in rows:
+        cols = rng.choice(x.shape[-1], per_row, replace=False)
+        x[..., r, cols] *= 2.0 ** -20
+    return bf16_round(x)
+
+
+@pytest.mark.parametrize("kind,n,d,b,sk_or_stride", [
+    ("sampled", 4096, 128, 64, 8), ("sampled", 3840, 128, 120, 8), ("sampled", 2048, 64, 64, 7),
+    ("antidiag", 4096, 128, 64, 8), ("antidiag", 3840, 128, 120, 4), ("antidiag", 1920, 64, 120, 8)])
+@pytest.mark.parametrize("tiny", [0, 2, 6])
+def test_int8_exact_logits_match_fp64_path(kind, n, d, b, sk_or_stride, tiny):
+    """The int8 tensor-core logits (psa_xlogits.cu) reproduce the fp64 DMMA path: scores agree to
+    a few ulps (only the softmax-denominator summation order differs), level maps exactly, and
+    both match the oracle at 1e-12. tiny=2: exact corrections; tiny=6: fp64 fallback heads."""
+    from paper_2512_04025_b200.importance import antidiagonal_scores, importance_scores
+    from paper_2512_04025_b200.mask import assign_levels_device
+    psa = _psa()
+    rng = np.random.default_rng(17 + tiny)
+    q, k, v = gaussian_qkv(23, 3, n, d)
+    if tiny:
+        q[1] = _with_tiny(q[1], rng, rng.choice(n, 64, replace=False), tiny)
+        k[2] = _with_tiny(k[2], rng, rng.choice(n, 64, replace=False), tiny)
+    lay = psa.make_layout(n, d, b, b, 4)
+    q4, k4 = to_dev(q)[None], to_dev(k)[None]
+    if kind == "sampled":
+        cfg = psa.SamplerConfig(8, sk_or_stride, 0)
+        fast = importance_scores(q4, k4, lay, cfg, "max")
+        slow = importance_scores(q4, k4, lay, cfg, "max", fp64_only=True)
+    else:
+        fast = antidiagonal_scores(q4, k4, lay, sk_or_stride)
+        slow = antidiagonal_scores(q4, k4, lay, sk_or_stride, fp64_only=True)
+    np.testing.assert_allclose(fast.cpu().numpy(), slow.cpu().numpy(), rtol=1e-14, atol=0)
+    rule = psa.LevelThresholds(TAUS_CFG1)
+    pf = assign_levels_device(fast, mode="threshold", rule=rule, levels=4, b_q=b, b_k=b, hkv=3)
+    ps = assign_levels_device(slow, mode="threshold", rule=rule, levels=4, b_q=b, b_k=b, hkv=3)
+    assert torch.equal(pf.level_map, ps.level_map)
+    olay = orc.Layout(n, d, b, b, 4)
+    f = fast.cpu().numpy()[0]
+    for h in range(3):
+        exp = (orc.importance_sampled(q[h], k[h], olay, 8, sk_or_stride, 0, "max")
+               if kind == "sampled" else orc.importance_antidiagonal(q[h], k[h], olay, sk_or_stride))
+        np.testing.assert_allclose(f[h], exp, rtol=1e-12, atol=0)
