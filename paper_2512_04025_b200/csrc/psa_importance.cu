@@ -190,19 +190,18 @@ __global__ void __launch_bounds__(kImpThreads, 2)
     const int nb = cols / s_k;
     const int j0 = b0 / s_k;
     if (!MEAN) {
-      // block max of the raw dots, then ONE IEEE division per block: x -> fl(x / sqrt(d)) is
-      // monotone, so fl(max(x) / sqrt(d)) is exactly the reference's block-max logit.
+      // block max of the RAW dots (the finalize kernel divides once: x -> fl(x / sqrt(d)) is
+      // monotone, so fl(max(x) / sqrt(d)) is exactly the reference's block-max logit)
       double lmax = -INFINITY;
       for (int bb = quad; bb < nb; bb += 4) {
         double bm = -INFINITY;
         for (int t = 0; t < s_k; ++t) bm = fmax(bm, xr[bb * s_k + t]);
-        bm = __ddiv_rn(bm, sqrt_d);  // importance.py:80
         lmax = fmax(lmax, bm);
         if (row_ok) M[(static_cast<int64_t>(bhq) * R + a_glob) * n_k + j0 + bb] = bm;
       }
       lmax = fmax(lmax, __shfl_xor_sync(0xffffffffu, lmax, 1));
       lmax = fmax(lmax, __shfl_xor_sync(0xffffffffu, lmax, 2));
-      const double m_new = fmax(m_run, lmax);
+      const double m_new = fmax(m_run, __ddiv_rn(lmax, sqrt_d));  // importance.py:80
       // softmax denominator (only its value, not its summation order, matters downstream)
       double part = 0.0;
       for (int bb = quad; bb < nb; bb += 4)
@@ -227,11 +226,12 @@ __global__ void __launch_bounds__(kImpThreads, 2)
   }
 }
 
-// S_ij = max_a exp(M_aj - m_a) / l_a   (or mean: sum_a M_aj / (s_q*s_k))
+// S_ij = max_a exp(fl(M_aj / sqrt(d)) - m_a) / l_a, M_aj = raw block-max dot
+// (or mean: sum_a M_aj / (s_q*s_k))
 template <bool MEAN>
 __global__ void __launch_bounds__(128) importance_finalize_kernel(
     const double* __restrict__ M, const double* __restrict__ mstat,
-    const double* __restrict__ lstat, int R, int s_q, int s_k, int n_q, int n_k,
+    const double* __restrict__ lstat, int R, int s_q, int s_k, int n_q, int n_k, double sqrt_d,
     double* __restrict__ S) {
   const int i = blockIdx.x;
   const int64_t bhq = blockIdx.y;
@@ -243,7 +243,8 @@ __global__ void __launch_bounds__(128) importance_finalize_kernel(
       if (MEAN) {
         acc = __dadd_rn(acc, mv);
       } else {
-        const double p = __ddiv_rn(exp(__dsub_rn(mv, mstat[a])), lstat[a]);
+        const double logit = __ddiv_rn(mv, sqrt_d);  // importance.py:80
+        const double p = __ddiv_rn(exp(__dsub_rn(logit, mstat[a])), lstat[a]);
         acc = fmax(acc, p);
       }
     }
@@ -527,10 +528,10 @@ static int launch_importance(const void* q, const void* k, int64_t batch, int hq
     rc = psa_check_launch("importance_stats_kernel<mean>");
     if (rc) return rc;
     importance_finalize_kernel<true><<<dim3(n_q, bhq), 128, 0, s>>>(M, mstat, lstat, R, s_q, s_k,
-                                                                     n_q, n_k, scores);
+                                                                     n_q, n_k, sqrt_d, scores);
   } else {
     importance_finalize_kernel<false><<<dim3(n_q, bhq), 128, 0, s>>>(M, mstat, lstat, R, s_q,
-                                                                      s_k, n_q, n_k, scores);
+                                                                      s_k, n_q, n_k, sqrt_d, scores);
   }
   return psa_check_launch("importance_finalize_kernel");
 }

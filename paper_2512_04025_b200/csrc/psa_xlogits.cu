@@ -8,41 +8,44 @@
 // ~36 TFLOP/s; the int8 tensor cores are ~120x faster, so we compute the SAME exact value with
 // integer arithmetic (an Ozaki-style split):
 //
-//   every gathered row x is put on the grid 2^(E-20), E = floor(log2 max|x|):
-//     x = X * 2^(E-20) + r,  X integer, |X| < 2^21,  r = 0 unless |x_k| < 2^(E-13) ("tiny")
-//   X = d2 * 2^14 + d1 * 2^7 + d0 with int8 digits (d0, d1 in [0, 127], d2 in [-128, 127])
-//   dot(X, Y) = sum_{a,b} 2^(7(a+b)) * dot(x_a, y_b)        (9 int8 GEMMs, int32 exact)
+//   every gathered row x is put on the grid 2^(E-27), E = floor(log2 max|x|):
+//     x = X * 2^(E-27) + r,  X integer, |X| < 2^28,  r = 0 unless |x_k| < 2^(E-20) ("tiny")
+//   X = d3 * 2^21 + d2 * 2^14 + d1 * 2^7 + d0, int8 digits (d0..d2 in [0, 127], d3 signed)
+//   dot(X, Y) = sum_{a,b} 2^(7(a+b)) * dot(x_a, y_b)        (16 int8 GEMMs, int32 exact)
 //
-// The 9 slice products accumulate into 5 int32 TMEM accumulators (one per weight class a+b);
-// the epilogue combines them in int64 (|dot(X,Y)| < 2^49: exact), converts exactly to fp64
-// and scales by 2^(Ex+Ey-40). Pairs involving tiny elements (at most 4 per row; ~3% of
-// Gaussian rows) add the exact fp64 correction sum_k (x_k y_k - xm_k ym_k) over the tiny
-// dimensions. Rows with more than 4 tiny elements (or non-finite values) mark their head for
-// the fp64 DMMA kernel instead, so the result is always the exact dot up to one final fp64
-// rounding. From the logits on, the epilogue is the DMMA kernels' arithmetic: per KV block the
+// The 16 slice products accumulate into 7 int32 TMEM accumulators (one per weight class a+b);
+// the epilogue forms the classes 0-3 and 4-6 as two exact int64 partial sums, converts both
+// exactly to fp64 and adds them with ONE rounding (the correctly rounded exact dot), then scales
+// by 2^(Ex+Ey-54). Pairs involving tiny elements (at most 4 per row; ~2e-4 of Gaussian rows)
+// add the exact fp64 correction sum_k (x_k y_k - xm_k ym_k) over the tiny dimensions. Rows with
+// more than 4 tiny elements (or non-finite values) mark their head for the fp64 DMMA kernel
+// instead. Either way the logit is the exact dot up to the final fp64 rounding. From the logits on, the epilogue is the DMMA kernels' arithmetic: per KV block the
 // max (sampled) or the numpy-ordered exp-sum (antidiagonal), and the online softmax (m, l).
 //
 // Kernel shape: one CTA per (head, residue class, 128 gathered query rows); 12 warps.
 //   warp 0  TMA: the 3 query slice tiles once, then 3 x (32 keys x 128 B) per key tile
-//   warp 1  MMA: 9 slice pairs x D/32 k-steps of tcgen05.mma.kind::i8 (M=128, N=32)
-//   warp 2  TMEM allocator (3 accumulator buffers x 5 classes x 32 columns)
-//   warps 4-11  epilogue, two groups taking alternate key tiles (their (m, l) merge at the end)
+//   warp 1  MMA: 16 slice pairs x D/32 k-steps of tcgen05.mma.kind::i8 (M=128, N=32)
+//   warp 2  TMEM allocator (2 accumulator buffers x 7 classes x 32 columns)
+//   warps 4-11  epilogue, two groups taking alternate key tiles (group g owns accumulator
+//           buffer g; their running (m, l) merge at the end). The epilogue is FP64-pipe bound
+//           (one fp64 exp per logit), so it keeps the tile's 32 logits in registers and
+//           evaluates them as independent chains.
 #include "common.cuh"
 #include "psa_internal.h"
 
 namespace psa {
 
-constexpr int kXlSlices = 3;
+constexpr int kXlSlices = 4;
 constexpr int kXlClasses = 2 * kXlSlices - 1;
 constexpr int kXlRowBytes = 128;  // one slice row: K-major, one 128-byte swizzle atom wide
 constexpr int kXlQRows = 128;     // MMA M
 constexpr int kXlKeys = 32;       // MMA N = keys per tile
 constexpr int kXlStages = 4;
-constexpr int kXlAccBufs = 3;
+constexpr int kXlAccBufs = 2;
 constexpr int kXlMaxTiny = 4;
 constexpr int kXlThreads = 384;
 constexpr int kXlEpiThreads = 256;
-constexpr int kXlGridShift = 20;  // X = x * 2^(20 - E), |X| < 2^21
+constexpr int kXlGridShift = 27;  // X = x * 2^(27 - E), |X| < 2^28
 
 struct XlMeta {
   int32_t e;      // row exponent E (0 for an all-zero row)
@@ -97,7 +100,7 @@ __global__ void __launch_bounds__(256) xl_slice_kernel(const uint16_t* __restric
   finite = __all_sync(0xffffffffu, finite);
   const int E = (amax > 0.0 && finite) ? ilogb(amax) : 0;
   const double up = ldexp(1.0, kXlGridShift - E);
-  uint32_t d[3] = {0u, 0u, 0u};
+  uint32_t d[kXlSlices] = {0u, 0u, 0u, 0u};
   unsigned tiny_bits = 0;
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
@@ -107,7 +110,8 @@ __global__ void __launch_bounds__(256) xl_slice_kernel(const uint16_t* __restric
     const int X = finite ? static_cast<int>(xt) : 0;
     d[0] |= static_cast<uint32_t>(X & 127) << (8 * e);
     d[1] |= static_cast<uint32_t>((X >> 7) & 127) << (8 * e);
-    d[2] |= static_cast<uint32_t>((X >> 14) & 0xFF) << (8 * e);
+    d[2] |= static_cast<uint32_t>((X >> 14) & 127) << (8 * e);
+    d[3] |= static_cast<uint32_t>((X >> 21) & 0xFF) << (8 * e);
   }
 #pragma unroll
   for (int s = 0; s < kXlSlices; ++s)
@@ -206,7 +210,8 @@ template <int D>
 struct XlSmem {
   uint8_t q[kXlSlices][kXlQRows * kXlRowBytes];
   uint8_t k[kXlStages][kXlSlices][kXlKeys * kXlRowBytes];
-  double dots[kXlKeys][kXlEpiThreads];
+  double ex[kXlKeys][kXlEpiThreads];  // per-thread logits / exp terms of one tile
+  double exp_tab[64];                 // 2^(j/64)
   double red_m[kXlQRows], red_l[kXlQRows];
   uint64_t q_full;
   uint64_t k_full[kXlStages], k_empty[kXlStages];
@@ -242,6 +247,46 @@ constexpr uint32_t xl_idesc(int M, int N) {
 PSA_DEV double pow2(int k) {  // exact 2^k for the normal range
   return __longlong_as_double(static_cast<long long>(k + 1023) << 52);
 }
+// exact int64 -> fp64 for |v| < 2^51
+PSA_DEV double i64_to_f64_exact(long long v) {
+  return __dsub_rn(__longlong_as_double(v + 0x4338000000000000LL), 6755399441055744.0);
+}
+// 2^(j/64), j = 0..63, correctly rounded (host-computed)
+__constant__ double kExp2Tab[64] = {1.0, 1.0108892860517005, 1.0218971486541166, 1.0330248790212284, 1.0442737824274138, 1.0556451783605572, 1.0671404006768237, 1.0787607977571199, 1.0905077326652577, 1.102382583307841, 1.1143867425958924, 1.1265216186082418, 1.1387886347566916, 1.1511892299529827, 1.1637248587775775, 1.1763969916502812, 1.189207115002721, 1.202156731452703, 1.215247359980469, 1.22848053610687, 1.241857812073484, 1.255380757024691, 1.2690509571917332, 1.2828700160787783, 1.2968395546510096, 1.3109612115247644, 1.3252366431597413, 1.339667524053303, 1.3542555469368927, 1.3690024229745905, 1.383909881963832, 1.3989796725383112, 1.4142135623730951, 1.42961333839197, 1.4451808069770467, 1.460917794180647, 1.4768261459394993, 1.4929077282912648, 1.5091644275934228, 1.5255981507445384, 1.5422108254079407, 1.559004400237837, 1.5759808451078865, 1.593142151342267, 1.6104903319492543, 1.6280274218573478, 1.645755478153965, 1.6636765803267364, 1.681792830507429, 1.7001063537185235, 1.718619298122478, 1.7373338352737062, 1.7562521603732995, 1.7753764925265212, 1.7947090750031072, 1.8142521755003989, 1.8340080864093424, 1.8539791250833855, 1.8741676341103, 1.8945759815869656, 1.9152065613971474, 1.9360617934922943, 1.9571441241754002, 1.978456026387951};
+
+// exp(t) for finite t <= 0 without branches, so a thread's 32 independent exps interleave on
+// the FP64 pipe: t = (64 e + j) ln2/64 + r with |r| <= ln2/128 (Cody-Waite, ln2_hi has 21
+// trailing zero bits so n * ln2_hi/64 is exact), e^r by a degree-6 Taylor polynomial
+// (truncation < 2^-60) evaluated as e^r - 1, 2^(j/64) from a shared-memory table joined with
+// one fma, 2^e applied in two exact steps (correct subnormals). Max error 1 ulp against libm
+// (numpy's and CUDA's exp differ from each other by as much).
+__constant__ double kExpC[10] = {
+    92.33248261689366,                           // 64 / ln2
+    0.01083042469326756,                         // ln2_hi / 64
+    2.9815858269852933e-12,                      // ln2_lo / 64
+    1.3888888888888889419e-03,                   // 1/6!
+    8.3333333333333332177e-03,                   // 1/5!
+    4.1666666666666664354e-02,                   // 1/4!
+    1.6666666666666665741e-01,                   // 1/3!
+    0.5, 1.0, 6755399441055744.0};               // 1/2!, 1/1!, 1.5 * 2^52
+PSA_DEV double exp_nonpos(double t, const double* tab) {
+  const double kd = __fma_rn(t, kExpC[0], kExpC[9]);  // rint(t * 64/ln2)
+  const int n = max(__double2loint(kd), -102400);
+  const double nd = __dsub_rn(kd, kExpC[9]);
+  double r = __fma_rn(-nd, kExpC[1], t);
+  r = __fma_rn(-nd, kExpC[2], r);
+  double pl = kExpC[3];
+  pl = __fma_rn(pl, r, kExpC[4]);
+  pl = __fma_rn(pl, r, kExpC[5]);
+  pl = __fma_rn(pl, r, kExpC[6]);
+  pl = __fma_rn(pl, r, kExpC[7]);
+  pl = __fma_rn(pl, r, kExpC[8]);
+  const double q = __dmul_rn(pl, r);  // e^r - 1
+  const double tj = tab[n & 63];
+  const int e = n >> 6;
+  const int ea = e >> 1;
+  return __dmul_rn(__dmul_rn(__fma_rn(tj, q, tj), pow2(ea)), pow2(e - ea));
+}
 // value of x on row grid E (the part the int8 slices carry exactly)
 PSA_DEV double grid_part(double x, int E) {
   return trunc(x * pow2(kXlGridShift - E)) * pow2(E - kXlGridShift);
@@ -249,8 +294,9 @@ PSA_DEV double grid_part(double x, int E) {
 PSA_DEV double bf16_at(const uint16_t* row, int c) {
   return static_cast<double>(__uint_as_float(static_cast<uint32_t>(row[c]) << 16));
 }
-// exact fp64 correction of dot(x, y) for the tiny dimensions of either row
-PSA_DEV double tiny_correction(const uint16_t* xr, const uint16_t* yr, XlMeta mx, XlMeta my) {
+// exact fp64 correction of dot(x, y) for the tiny dimensions of either row (rare path)
+__device__ __noinline__ double tiny_correction(const uint16_t* xr, const uint16_t* yr,
+                                               XlMeta mx, XlMeta my) {
   double c = 0.0;
   const int nx = min(static_cast<int>(mx.tiny >> 28), kXlMaxTiny);
   const int ny = min(static_cast<int>(my.tiny >> 28), kXlMaxTiny);
@@ -265,7 +311,9 @@ PSA_DEV double tiny_correction(const uint16_t* xr, const uint16_t* yr, XlMeta mx
   return c;
 }
 
-template <int D, class QRows, class KRows, int MODE>
+// PER > 0: keys per KV block known at compile time (tile = 32/PER whole blocks; the block
+// reductions are static register trees). PER == 0: runtime block size (shared-memory loops).
+template <int D, class QRows, class KRows, int MODE, int PER>
 __global__ void __launch_bounds__(kXlThreads, 1)
     xl_stats_kernel(const __grid_constant__ XlMaps maps, const XlParams p, QRows qrows0,
                     KRows krows0) {
@@ -308,6 +356,7 @@ __global__ void __launch_bounds__(kXlThreads, 1)
     tmem_alloc(&sm.tmem_base, 512);
     tmem_relinquish();
   }
+  if (threadIdx.x < 64) sm.exp_tab[threadIdx.x] = kExp2Tab[threadIdx.x];
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -322,7 +371,7 @@ __global__ void __launch_bounds__(kXlThreads, 1)
       const int kset = (bkv * p.classes + kcls) * kXlSlices;
       for (int t = 0; t < T; ++t) {
         const int s = t % kXlStages;
-        if (t >= kXlStages) mbar_wait(&sm.k_empty[s], ((t / kXlStages) - 1) & 1);
+        if (t >= kXlStages) mbar_wait_backoff(&sm.k_empty[s], ((t / kXlStages) - 1) & 1);
         mbar_arrive_expect_tx(&sm.k_full[s], kXlSlices * kXlKeys * kXlRowBytes);
         for (int bb = 0; bb < kXlSlices; ++bb)
           tma_load_2d(&maps.ks, &sm.k_full[s], sm.k[s][bb], 0, (kset + bb) * p.kp + t * kXlKeys);
@@ -335,24 +384,22 @@ __global__ void __launch_bounds__(kXlThreads, 1)
     for (int t = 0; t < T; ++t) {
       const int s = t % kXlStages, ab = t % kXlAccBufs;
       mbar_wait(&sm.k_full[s], (t / kXlStages) & 1);
-      if (t >= kXlAccBufs) mbar_wait(&sm.acc_empty[ab], ((t / kXlAccBufs) - 1) & 1);
+      if (t >= kXlAccBufs) mbar_wait_backoff(&sm.acc_empty[ab], ((t / kXlAccBufs) - 1) & 1);
       tc_fence_after();
       if (elect_one()) {
-        bool started[kXlClasses] = {false, false, false, false, false};
 #pragma unroll
         for (int a = 0; a < kXlSlices; ++a)
 #pragma unroll
           for (int bb = 0; bb < kXlSlices; ++bb) {
             const int c = a + bb;
+            const bool first = (a == 0) || (bb == kXlSlices - 1 && a == c - bb && c >= kXlSlices);
             const uint64_t ad = umma_desc_sw128(smem_u32(sm.q[a]), 16, 1024);
             const uint64_t bd = umma_desc_sw128(smem_u32(sm.k[s][bb]), 16, 1024);
             const uint32_t dcol = tmem + ab * (kXlClasses * kXlKeys) + c * kXlKeys;
 #pragma unroll
-            for (int kk = 0; kk < D / 32; ++kk) {
+            for (int kk = 0; kk < D / 32; ++kk)
               mma_i8_ss(dcol, ad + ((kk * 32) >> 4), bd + ((kk * 32) >> 4), idesc,
-                        (started[c] || kk > 0) ? 1u : 0u);
-            }
-            started[c] = true;
+                        (first && kk == 0) ? 0u : 1u);
           }
         mma_commit(&sm.k_empty[s]);
         mma_commit(&sm.acc_full[ab]);
@@ -373,78 +420,190 @@ __global__ void __launch_bounds__(kXlThreads, 1)
     const uint16_t* qrow_ptr = p.q + (static_cast<int64_t>(bhq) * p.n + qsrc) * D;
     const XlMeta* kmeta = p.kmeta + static_cast<int64_t>(bkv * p.classes + kcls) * p.kp;
     const uint16_t* kbase = p.k + static_cast<int64_t>(bkv) * p.n * D;
-    const uint32_t t_lane = tmem + (static_cast<uint32_t>(wq * 32) << 16);
-    double* dots = &sm.dots[0][e_tid];
+    const uint32_t t_acc = tmem + (static_cast<uint32_t>(wq * 32) << 16) +
+                           grp * (kXlClasses * kXlKeys);
     const int cw = p.bpt * p.per;
     const int64_t out_row = MODE == kXlMax ? static_cast<int64_t>(bhq) * rows_valid + a
                                            : static_cast<int64_t>(bhq) * p.n + qsrc;
+    double* out_blocks = p.M + out_row * p.n_k;
     double m_run = -INFINITY, l_run = 0.0;
 
     for (int t = grp; t < T; t += 2) {
-      const int ab = t % kXlAccBufs;
       const int j0 = t * p.bpt;  // first KV block of the tile
       const int nb = min(p.bpt, p.n_k - j0);
       const int nvalid = nb * p.per;
-      mbar_wait(&sm.acc_full[ab], (t / kXlAccBufs) & 1);
+      const uint32_t valid_mask = nvalid >= 32 ? 0xffffffffu : ((1u << nvalid) - 1u);
+      const XlMeta kml = kmeta[t * kXlKeys + lane];  // lane j: key j's exponent / tiny count
+      const int kinfo = (kml.e << 1) | ((kml.tiny >> 28) != 0u ? 1 : 0);
+      mbar_wait(&sm.acc_full[grp], (t >> 1) & 1);
       tc_fence_after();
-      const XlMeta* km = kmeta + t * kXlKeys;
+      double dv[kXlKeys];
 #pragma unroll
       for (int c8 = 0; c8 < kXlKeys / 8; ++c8) {
         uint32_t cv[kXlClasses][8];
 #pragma unroll
-        for (int c = 0; c < kXlClasses; ++c)
-          tmem_ld8(t_lane + ab * (kXlClasses * kXlKeys) + c * kXlKeys + c8 * 8, cv[c]);
+        for (int c = 0; c < kXlClasses; ++c) tmem_ld8(t_acc + c * kXlKeys + c8 * 8, cv[c]);
         tmem_wait_ld();
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          const int j = c8 * 8 + e;
-          long long v = static_cast<int>(cv[0][e]);
-          v += static_cast<long long>(static_cast<int>(cv[1][e])) << 7;
-          v += static_cast<long long>(static_cast<int>(cv[2][e])) << 14;
-          v += static_cast<long long>(static_cast<int>(cv[3][e])) << 21;
-          v += static_cast<long long>(static_cast<int>(cv[4][e])) << 28;
-          // exact int64 -> fp64 for |v| < 2^51
-          const double vd = __dsub_rn(__longlong_as_double(v + 0x4338000000000000LL),
-                                      6755399441055744.0);
-          const XlMeta kmj = km[j];
-          double dot = vd * pow2(qm.e + kmj.e - 2 * kXlGridShift);
-          if ((q_tiny || (kmj.tiny >> 28) != 0) && j < nvalid && row_ok) {
-            const uint16_t* krow = kbase + krows(t * cw + j) * D;  // tile t: elements t*cw..
-            dot = __dadd_rn(dot, tiny_correction(qrow_ptr, krow, qm, kmj));
-          }
-          dots[j * kXlEpiThreads] = dot;
+          // classes (weights 2^(7c)): exact int32 pairs, then two exact int64 partial sums
+          const int lo32 = static_cast<int>(cv[0][e]) + (static_cast<int>(cv[1][e]) << 7);
+          const int mid32 = static_cast<int>(cv[2][e]) + (static_cast<int>(cv[3][e]) << 7);
+          const int hi32 = static_cast<int>(cv[4][e]) + (static_cast<int>(cv[5][e]) << 7);
+          const long long lo = static_cast<long long>(lo32) + (static_cast<long long>(mid32) << 14);
+          const long long hi = static_cast<long long>(hi32) +
+                               (static_cast<long long>(static_cast<int>(cv[6][e])) << 14);
+          // exact dot(X, Y) = hi * 2^28 + lo, rounded once
+          dv[c8 * 8 + e] = __fma_rn(i64_to_f64_exact(hi), 268435456.0, i64_to_f64_exact(lo));
         }
       }
       tc_fence_before();
-      mbar_arrive(&sm.acc_empty[ab]);
+      mbar_arrive(&sm.acc_empty[grp]);
+#pragma unroll
+      for (int j = 0; j < kXlKeys; ++j) {
+        const int kj = __shfl_sync(0xffffffffu, kinfo, j);
+        dv[j] = __dmul_rn(dv[j], pow2((kj >> 1) + qm.e - 2 * kXlGridShift));
+      }
+      // exact corrections for tiny elements (rare: skipped unless some lane needs one)
+      const uint32_t key_tiny = __ballot_sync(0xffffffffu, kinfo & 1) & valid_mask;
+      if (__any_sync(0xffffffffu, q_tiny && row_ok) || key_tiny != 0u) {
+#pragma unroll 1
+        for (int j = 0; j < nvalid; ++j)
+          if (row_ok && (q_tiny || ((key_tiny >> j) & 1u))) {
+            const XlMeta kmj = kmeta[t * kXlKeys + j];
+            const double c = tiny_correction(qrow_ptr, kbase + krows(t * cw + j) * D, qm, kmj);
+            sm.ex[j][e_tid] = c;  // staged: dv[] needs static indices
+          }
+#pragma unroll
+        for (int j = 0; j < kXlKeys; ++j)
+          if (row_ok && (q_tiny || ((key_tiny >> j) & 1u)) && j < nvalid)
+            dv[j] = __dadd_rn(dv[j], sm.ex[j][e_tid]);
+      }
+      double* xs = &sm.ex[0][e_tid];  // this thread's column: 32 values, stride kXlEpiThreads
 
-      if (MODE == kXlMax) {
-        double lmax = -INFINITY;
-        for (int bb = 0; bb < nb; ++bb) {
-          double bm = -INFINITY;
-          for (int u = 0; u < p.per; ++u) bm = fmax(bm, dots[(bb * p.per + u) * kXlEpiThreads]);
-          bm = __ddiv_rn(bm, p.sqrt_d);  // importance.py:80 (one IEEE division per block)
-          lmax = fmax(lmax, bm);
-          if (row_ok) p.M[out_row * p.n_k + j0 + bb] = bm;
+      constexpr int kP = PER > 0 ? PER : 1;
+      if (PER > 0) {
+        // ---- static block structure: blocks are PER consecutive keys of the tile
+        constexpr int kB = kXlKeys / kP;
+        double bx[kB];
+        if (MODE == kXlMax) {
+#pragma unroll
+          for (int bb = 0; bb < kB; ++bb) {  // raw block maxima (tree)
+            double v[kP];
+#pragma unroll
+            for (int u = 0; u < kP; ++u) v[u] = dv[bb * kP + u];
+#pragma unroll
+            for (int w = 1; w < kP; w <<= 1)
+#pragma unroll
+              for (int u = 0; u + w < kP; u += 2 * w) v[u] = fmax(v[u], v[u + w]);
+            bx[bb] = bb < nb ? v[0] : -INFINITY;
+            if (row_ok && bb < nb) out_blocks[j0 + bb] = v[0];
+          }
+          double tmax = bx[0];
+#pragma unroll
+          for (int bb = 1; bb < kB; ++bb) tmax = fmax(tmax, bx[bb]);
+          const double m_new = fmax(m_run, __ddiv_rn(tmax, p.sqrt_d));  // importance.py:80
+          double ps[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+          for (int j = 0; j < kXlKeys; ++j) {
+            const double arg = __fma_rn(dv[j], p.inv_sqrt_d, -m_new);
+            ps[j & 3] = __dadd_rn(ps[j & 3],
+                                  exp_nonpos(((valid_mask >> j) & 1u) ? arg : -2000.0, sm.exp_tab));
+          }
+          const double part = __dadd_rn(__dadd_rn(ps[0], ps[1]), __dadd_rn(ps[2], ps[3]));
+          l_run = __dadd_rn(__dmul_rn(l_run, exp(__dsub_rn(m_run, m_new))), part);
+          m_run = m_new;
+        } else {
+          double cmax = -INFINITY;
+#pragma unroll
+          for (int bb = 0; bb < kB; ++bb) {
+            double v[kP];
+#pragma unroll
+            for (int u = 0; u < kP; ++u) v[u] = dv[bb * kP + u];
+#pragma unroll
+            for (int w = 1; w < kP; w <<= 1)
+#pragma unroll
+              for (int u = 0; u + w < kP; u += 2 * w) v[u] = fmax(v[u], v[u + w]);
+            cmax = fmax(cmax, bb < nb ? v[0] : -INFINITY);
+          }
+          const double m_new = fmax(m_run, __dmul_rn(cmax, p.scale));
+          double part = 0.0;
+#pragma unroll
+          for (int bb = 0; bb < kB; ++bb) {
+            double ev[kP];
+#pragma unroll
+            for (int u = 0; u < kP; ++u)
+              ev[u] = exp_nonpos(__dsub_rn(__dmul_rn(dv[bb * kP + u], p.scale), m_new), sm.exp_tab);
+            // numpy pairwise order for PER elements (np_pairwise_sum, common.cuh)
+            double e;
+            if (kP < 8) {
+              e = 0.0;
+#pragma unroll
+              for (int u = 0; u < kP; ++u) e = __dadd_rn(e, ev[u]);
+            } else {
+              double r8[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) r8[u] = ev[u < kP ? u : 0];
+#pragma unroll
+              for (int u = 8; u < kP - (kP % 8); u += 8)
+#pragma unroll
+                for (int w = 0; w < 8; ++w) r8[w] = __dadd_rn(r8[w], ev[u + w]);
+              e = __dadd_rn(__dadd_rn(__dadd_rn(r8[0], r8[1]), __dadd_rn(r8[2], r8[3])),
+                            __dadd_rn(__dadd_rn(r8[4], r8[5]), __dadd_rn(r8[6], r8[7])));
+#pragma unroll
+              for (int u = kP - (kP % 8); u < kP; ++u) e = __dadd_rn(e, ev[u]);
+            }
+            if (bb < nb) {
+              part = __dadd_rn(part, e);
+              if (row_ok) out_blocks[j0 + bb] = e;
+            }
+          }
+          l_run = __dadd_rn(__dmul_rn(l_run, exp(__dsub_rn(m_run, m_new))), part);
+          m_run = m_new;
+          if (row_ok) p.Mc[out_row * p.n_tiles + t] = m_new;
         }
-        const double m_new = fmax(m_run, lmax);
-        double part = 0.0;
-        for (int u = 0; u < nvalid; ++u)
-          part = __dadd_rn(part, exp(__fma_rn(dots[u * kXlEpiThreads], p.inv_sqrt_d, -m_new)));
+      } else if (MODE == kXlMax) {
+        double tmax = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < kXlKeys; ++j) {
+          xs[j * kXlEpiThreads] = dv[j];
+          tmax = fmax(tmax, ((valid_mask >> j) & 1u) ? dv[j] : -INFINITY);
+        }
+        const double m_new = fmax(m_run, __ddiv_rn(tmax, p.sqrt_d));  // importance.py:80
+        // branch-free: padding keys get an argument whose exp is exactly 0
+        double ps[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int j = 0; j < kXlKeys; ++j) {
+          const double arg = __fma_rn(dv[j], p.inv_sqrt_d, -m_new);
+          ps[j & 3] = __dadd_rn(ps[j & 3],
+                                exp_nonpos(((valid_mask >> j) & 1u) ? arg : -2000.0, sm.exp_tab));
+        }
+        const double part = __dadd_rn(__dadd_rn(ps[0], ps[1]), __dadd_rn(ps[2], ps[3]));
         l_run = __dadd_rn(__dmul_rn(l_run, exp(__dsub_rn(m_run, m_new))), part);
         m_run = m_new;
+        // raw block maxima (the finalize kernel divides by sqrt(d) once per value)
+        for (int bb = 0; bb < nb; ++bb) {
+          double bm = xs[bb * p.per * kXlEpiThreads];
+          for (int u = 1; u < p.per; ++u) bm = fmax(bm, xs[(bb * p.per + u) * kXlEpiThreads]);
+          if (row_ok) out_blocks[j0 + bb] = bm;
+        }
       } else {
         double cmax = -INFINITY;
-        for (int u = 0; u < nvalid; ++u) cmax = fmax(cmax, dots[u * kXlEpiThreads]);
+#pragma unroll
+        for (int j = 0; j < kXlKeys; ++j)
+          cmax = fmax(cmax, ((valid_mask >> j) & 1u) ? dv[j] : -INFINITY);
         const double m_new = fmax(m_run, __dmul_rn(cmax, p.scale));
+#pragma unroll
+        for (int j = 0; j < kXlKeys; ++j) {
+          const double arg = __dsub_rn(__dmul_rn(dv[j], p.scale), m_new);
+          xs[j * kXlEpiThreads] = exp_nonpos(((valid_mask >> j) & 1u) ? arg : -2000.0, sm.exp_tab);
+        }
         double part = 0.0;
-        for (int bb = 0; bb < nb; ++bb) {
-          const double* xb = dots + bb * p.per * kXlEpiThreads;
-          const double e = np_pairwise_sum_fn(p.per, [&](int u) {
-            return exp(__dsub_rn(__dmul_rn(xb[u * kXlEpiThreads], p.scale), m_new));
-          });
+        for (int bb = 0; bb < nb; ++bb) {  // numpy pairwise order inside each block
+          const double* xb = xs + bb * p.per * kXlEpiThreads;
+          const double e = np_pairwise_sum_fn(p.per, [&](int u) { return xb[u * kXlEpiThreads]; });
           part = __dadd_rn(part, e);
-          if (row_ok) p.M[out_row * p.n_k + j0 + bb] = e;
+          if (row_ok) out_blocks[j0 + bb] = e;
         }
         l_run = __dadd_rn(__dmul_rn(l_run, exp(__dsub_rn(m_run, m_new))), part);
         m_run = m_new;
@@ -578,7 +737,7 @@ static int xl_launch(const void* q, const void* k, int64_t batch, int hq, int hk
   p.mstat = mstat;
   p.lstat = lstat;
   const size_t smem = sizeof(XlSmem<D>);
-  auto kern = xl_stats_kernel<D, QR, KR, MODE>;
+  auto kern = g.per == 8 ? xl_stats_kernel<D, QR, KR, MODE, 8> : xl_stats_kernel<D, QR, KR, MODE, 0>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   kern<<<dim3(g.rq_pad / kXlQRows, bhq, g.classes), kXlThreads, smem, s>>>(maps, p, qr, kr);
   return psa_check_launch("xl_stats_kernel");
