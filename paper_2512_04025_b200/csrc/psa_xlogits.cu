@@ -212,7 +212,7 @@ struct XlSmem {
   uint8_t k[kXlStages][kXlSlices][kXlKeys * kXlRowBytes];
   double ex[kXlKeys][kXlEpiThreads];  // per-thread logits / exp terms of one tile
   double exp_tab[64];                 // 2^(j/64)
-  double red_m[kXlQRows], red_l[kXlQRows];
+  double red_m[kXlQRows], red_l[kXlQRows], red_x[kXlQRows];
   uint64_t q_full;
   uint64_t k_full[kXlStages], k_empty[kXlStages];
   uint64_t acc_full[kXlAccBufs], acc_empty[kXlAccBufs];
@@ -260,19 +260,39 @@ __constant__ double kExp2Tab[64] = {1.0, 1.0108892860517005, 1.0218971486541166,
 // (truncation < 2^-60) evaluated as e^r - 1, 2^(j/64) from a shared-memory table joined with
 // one fma, 2^e applied in two exact steps (correct subnormals). Max error 1 ulp against libm
 // (numpy's and CUDA's exp differ from each other by as much).
-__constant__ double kExpC[10] = {
+__constant__ double kExpC[9] = {
     92.33248261689366,                           // 64 / ln2
     0.01083042469326756,                         // ln2_hi / 64
     2.9815858269852933e-12,                      // ln2_lo / 64
-    1.3888888888888889419e-03,                   // 1/6!
     8.3333333333333332177e-03,                   // 1/5!
     4.1666666666666664354e-02,                   // 1/4!
     1.6666666666666665741e-01,                   // 1/3!
     0.5, 1.0, 6755399441055744.0};               // 1/2!, 1/1!, 1.5 * 2^52
-PSA_DEV double exp_nonpos(double t, const double* tab) {
-  const double kd = __fma_rn(t, kExpC[0], kExpC[9]);  // rint(t * 64/ln2)
-  const int n = max(__double2loint(kd), -102400);
-  const double nd = __dsub_rn(kd, kExpC[9]);
+// Fast path for t >= -708 (2^e applied by an exponent-field add: exact for normal results);
+// *slow (0/1) flags a t below that, which the caller recomputes with exp_nonpos_slow.
+PSA_DEV double exp_nonpos(double t, const double* tab, int* slow) {
+  const double kd = __fma_rn(t, kExpC[0], kExpC[8]);  // rint(t * 64/ln2)
+  const int n = __double2loint(kd);
+  const double nd = __dsub_rn(kd, kExpC[8]);
+  double r = __fma_rn(-nd, kExpC[1], t);
+  r = __fma_rn(-nd, kExpC[2], r);
+  double pl = kExpC[3];                       // degree 5: truncation < 0.3 ulp for |r| <= ln2/128
+  pl = __fma_rn(pl, r, kExpC[4]);
+  pl = __fma_rn(pl, r, kExpC[5]);
+  pl = __fma_rn(pl, r, kExpC[6]);
+  pl = __fma_rn(pl, r, kExpC[7]);
+  const double q = __dmul_rn(pl, r);  // e^r - 1
+  const double tj = tab[n & 63];
+  const double v = __fma_rn(tj, q, tj);  // in [1, 2)
+  *slow |= (n < -65344) ? 1 : 0;         // e = n >> 6 < -1021: subnormal / zero result
+  return __hiloint2double(__double2hiint(v) + ((n >> 6) << 20), __double2loint(v));
+}
+// exp(t) for any t <= 0 including -inf (two exact scaling steps: correct subnormals)
+PSA_DEV double exp_nonpos_slow(double t, const double* tab) {
+  t = fmax(t, -1100.0);
+  const double kd = __fma_rn(t, kExpC[0], kExpC[8]);
+  const int n = __double2loint(kd);
+  const double nd = __dsub_rn(kd, kExpC[8]);
   double r = __fma_rn(-nd, kExpC[1], t);
   r = __fma_rn(-nd, kExpC[2], r);
   double pl = kExpC[3];
@@ -280,12 +300,15 @@ PSA_DEV double exp_nonpos(double t, const double* tab) {
   pl = __fma_rn(pl, r, kExpC[5]);
   pl = __fma_rn(pl, r, kExpC[6]);
   pl = __fma_rn(pl, r, kExpC[7]);
-  pl = __fma_rn(pl, r, kExpC[8]);
-  const double q = __dmul_rn(pl, r);  // e^r - 1
+  const double q = __dmul_rn(pl, r);
   const double tj = tab[n & 63];
   const int e = n >> 6;
   const int ea = e >> 1;
   return __dmul_rn(__dmul_rn(__fma_rn(tj, q, tj), pow2(ea)), pow2(e - ea));
+}
+// exp(m_old - m_new) for the running-sum rescale; 0 before the first tile (m_old = -inf)
+PSA_DEV double rescale(double m_old, double m_new, const double* tab) {
+  return m_old == -INFINITY ? 0.0 : exp_nonpos_slow(__dsub_rn(m_old, m_new), tab);
 }
 // value of x on row grid E (the part the int8 slices carry exactly)
 PSA_DEV double grid_part(double x, int E) {
@@ -427,6 +450,7 @@ __global__ void __launch_bounds__(kXlThreads, 1)
                                            : static_cast<int64_t>(bhq) * p.n + qsrc;
     double* out_blocks = p.M + out_row * p.n_k;
     double m_run = -INFINITY, l_run = 0.0;
+    double rmax = -INFINITY;  // MAX mode: exact running max of the raw dot products
 
     for (int t = grp; t < T; t += 2) {
       const int j0 = t * p.bpt;  // first KV block of the tile
@@ -502,16 +526,29 @@ __global__ void __launch_bounds__(kXlThreads, 1)
           double tmax = bx[0];
 #pragma unroll
           for (int bb = 1; bb < kB; ++bb) tmax = fmax(tmax, bx[bb]);
-          const double m_new = fmax(m_run, __ddiv_rn(tmax, p.sqrt_d));  // importance.py:80
+          rmax = fmax(rmax, tmax);
+          // exps use an offset within an ulp of the running max logit (no division on the
+          // critical path); the exact max fl(max / sqrt(d)) is applied once per row at the end
+          const double m_new = fmax(m_run, __dmul_rn(tmax, p.inv_sqrt_d));
           double ps[4] = {0.0, 0.0, 0.0, 0.0};
+          int slow = 0;
 #pragma unroll
           for (int j = 0; j < kXlKeys; ++j) {
-            const double arg = __fma_rn(dv[j], p.inv_sqrt_d, -m_new);
-            ps[j & 3] = __dadd_rn(ps[j & 3],
-                                  exp_nonpos(((valid_mask >> j) & 1u) ? arg : -2000.0, sm.exp_tab));
+            const bool ok = (valid_mask >> j) & 1u;
+            const double e = exp_nonpos(ok ? __fma_rn(dv[j], p.inv_sqrt_d, -m_new) : 0.0,
+                                        sm.exp_tab, &slow);
+            ps[j & 3] = __dadd_rn(ps[j & 3], ok ? e : 0.0);
+          }
+          if (slow) {  // some term below e^-708: redo this tile's sum with exact subnormals
+            ps[0] = ps[1] = ps[2] = ps[3] = 0.0;
+#pragma unroll
+            for (int j = 0; j < kXlKeys; ++j)
+              if ((valid_mask >> j) & 1u)
+                ps[j & 3] = __dadd_rn(ps[j & 3], exp_nonpos_slow(__fma_rn(dv[j], p.inv_sqrt_d, -m_new),
+                                                                 sm.exp_tab));
           }
           const double part = __dadd_rn(__dadd_rn(ps[0], ps[1]), __dadd_rn(ps[2], ps[3]));
-          l_run = __dadd_rn(__dmul_rn(l_run, exp(__dsub_rn(m_run, m_new))), part);
+          l_run = __dadd_rn(__dmul_rn(l_run, rescale(m_run, m_new, sm.exp_tab)), part);
           m_run = m_new;
         } else {
           double cmax = -INFINITY;
@@ -531,9 +568,17 @@ __global__ void __launch_bounds__(kXlThreads, 1)
 #pragma unroll
           for (int bb = 0; bb < kB; ++bb) {
             double ev[kP];
+            int slow = 0;
 #pragma unroll
             for (int u = 0; u < kP; ++u)
-              ev[u] = exp_nonpos(__dsub_rn(__dmul_rn(dv[bb * kP + u], p.scale), m_new), sm.exp_tab);
+              ev[u] = exp_nonpos(__dsub_rn(__dmul_rn(dv[bb * kP + u], p.scale), m_new), sm.exp_tab,
+                                 &slow);
+            if (slow) {
+#pragma unroll
+              for (int u = 0; u < kP; ++u)
+                ev[u] = exp_nonpos_slow(__dsub_rn(__dmul_rn(dv[bb * kP + u], p.scale), m_new),
+                                        sm.exp_tab);
+            }
             // numpy pairwise order for PER elements (np_pairwise_sum, common.cuh)
             double e;
             if (kP < 8) {
@@ -558,7 +603,7 @@ __global__ void __launch_bounds__(kXlThreads, 1)
               if (row_ok) out_blocks[j0 + bb] = e;
             }
           }
-          l_run = __dadd_rn(__dmul_rn(l_run, exp(__dsub_rn(m_run, m_new))), part);
+          l_run = __dadd_rn(__dmul_rn(l_run, rescale(m_run, m_new, sm.exp_tab)), part);
           m_run = m_new;
           if (row_ok) p.Mc[out_row * p.n_tiles + t] = m_new;
         }
@@ -569,17 +614,18 @@ __global__ void __launch_bounds__(kXlThreads, 1)
           xs[j * kXlEpiThreads] = dv[j];
           tmax = fmax(tmax, ((valid_mask >> j) & 1u) ? dv[j] : -INFINITY);
         }
-        const double m_new = fmax(m_run, __ddiv_rn(tmax, p.sqrt_d));  // importance.py:80
+        rmax = fmax(rmax, tmax);
+        const double m_new = fmax(m_run, __dmul_rn(tmax, p.inv_sqrt_d));
         // branch-free: padding keys get an argument whose exp is exactly 0
         double ps[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int j = 0; j < kXlKeys; ++j) {
           const double arg = __fma_rn(dv[j], p.inv_sqrt_d, -m_new);
           ps[j & 3] = __dadd_rn(ps[j & 3],
-                                exp_nonpos(((valid_mask >> j) & 1u) ? arg : -2000.0, sm.exp_tab));
+                                exp_nonpos_slow(((valid_mask >> j) & 1u) ? arg : -2000.0, sm.exp_tab));
         }
         const double part = __dadd_rn(__dadd_rn(ps[0], ps[1]), __dadd_rn(ps[2], ps[3]));
-        l_run = __dadd_rn(__dmul_rn(l_run, exp(__dsub_rn(m_run, m_new))), part);
+        l_run = __dadd_rn(__dmul_rn(l_run, rescale(m_run, m_new, sm.exp_tab)), part);
         m_run = m_new;
         // raw block maxima (the finalize kernel divides by sqrt(d) once per value)
         for (int bb = 0; bb < nb; ++bb) {
@@ -596,7 +642,7 @@ __global__ void __launch_bounds__(kXlThreads, 1)
 #pragma unroll
         for (int j = 0; j < kXlKeys; ++j) {
           const double arg = __dsub_rn(__dmul_rn(dv[j], p.scale), m_new);
-          xs[j * kXlEpiThreads] = exp_nonpos(((valid_mask >> j) & 1u) ? arg : -2000.0, sm.exp_tab);
+          xs[j * kXlEpiThreads] = exp_nonpos_slow(((valid_mask >> j) & 1u) ? arg : -2000.0, sm.exp_tab);
         }
         double part = 0.0;
         for (int bb = 0; bb < nb; ++bb) {  // numpy pairwise order inside each block
@@ -605,22 +651,24 @@ __global__ void __launch_bounds__(kXlThreads, 1)
           part = __dadd_rn(part, e);
           if (row_ok) out_blocks[j0 + bb] = e;
         }
-        l_run = __dadd_rn(__dmul_rn(l_run, exp(__dsub_rn(m_run, m_new))), part);
+        l_run = __dadd_rn(__dmul_rn(l_run, rescale(m_run, m_new, sm.exp_tab)), part);
         m_run = m_new;
         if (row_ok) p.Mc[out_row * p.n_tiles + t] = m_new;
       }
     }
-    // merge the two groups' running (m, l)
+    // merge the two groups' running (m, l); MAX mode re-bases l on the exact max logit
     if (grp == 1) {
       sm.red_m[row] = m_run;
       sm.red_l[row] = l_run;
+      sm.red_x[row] = rmax;
     }
     named_bar_sync(1, kXlEpiThreads);
     if (grp == 0 && row_ok) {
       const double m1 = sm.red_m[row], l1 = sm.red_l[row];
-      const double m = fmax(m_run, m1);
+      const double m = MODE == kXlMax ? __ddiv_rn(fmax(rmax, sm.red_x[row]), p.sqrt_d)  // :80
+                                      : fmax(m_run, m1);
       const double l = __dadd_rn(__dmul_rn(l_run, exp(__dsub_rn(m_run, m))),
-                                 __dmul_rn(l1, exp(__dsub_rn(m1, m))));
+                                 m1 == -INFINITY ? 0.0 : __dmul_rn(l1, exp(__dsub_rn(m1, m))));
       p.mstat[out_row] = m;
       p.lstat[out_row] = l;
     }
