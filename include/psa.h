@@ -148,6 +148,15 @@ int psa_attn_fwd(const void* q, const void* k, const void* v, const void* k_pyr,
                  int b_k, int levels, const uint16_t* plan_csr, const int32_t* plan_info,
                  int causal, void* out, float* lse, int32_t* skipped_rows, void* stream);
 
+/*
+ * Token permutation.  Replaces apply_permutation (pkg/src/pyrattn/permute.py:131-137) for the
+ * space-filling-curve reorder of pipeline._run_head (pipeline.py:257-263, unpermute :312-313):
+ * dst[b][i] = src[b][index[i]] for b < bh, i < n; rows of row_bytes bytes (multiple of 4).
+ * index: DEVICE int64 [n] (a bijection; hilbert_order is generated by the Python layer).
+ */
+int psa_gather_rows(const void* src, int64_t bh, int64_t n, int row_bytes, const int64_t* index,
+                    void* dst, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

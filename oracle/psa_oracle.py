@@ -351,14 +351,66 @@ def causal_full_attention(q, k, v):
     return (p @ v) / den[:, None], mx + np.log(den)
 
 
+# --------------------------------------------------------------------------- permutation
+def _sgn(v):
+    return (v > 0) - (v < 0)
+
+
+def _gilbert(x, y, ax, ay, bx, by):
+    """permute.py:46-90 — generalized Hilbert walk, recursive as in the reference."""
+    w, h = abs(ax + ay), abs(bx + by)
+    dax, day, dbx, dby = _sgn(ax), _sgn(ay), _sgn(bx), _sgn(by)
+    if h == 1:
+        return [(x + t * dax, y + t * day) for t in range(w)]
+    if w == 1:
+        return [(x + t * dbx, y + t * dby) for t in range(h)]
+    ax2, ay2, bx2, by2 = ax // 2, ay // 2, bx // 2, by // 2
+    w2, h2 = abs(ax2 + ay2), abs(bx2 + by2)
+    if 2 * w > 3 * h:
+        if (w2 % 2) and w > 2:
+            ax2, ay2 = ax2 + dax, ay2 + day
+        return (_gilbert(x, y, ax2, ay2, bx, by)
+                + _gilbert(x + ax2, y + ay2, ax - ax2, ay - ay2, bx, by))
+    if (h2 % 2) and h > 2:
+        bx2, by2 = bx2 + dbx, by2 + dby
+    return (_gilbert(x, y, bx2, by2, ax2, ay2)
+            + _gilbert(x + bx2, y + by2, ax, ay, bx - bx2, by - by2)
+            + _gilbert(x + (ax - dax) + (bx2 - dbx), y + (ay - day) + (by2 - dby),
+                       -bx2, -by2, -(ax - ax2), -(ay - ay2)))
+
+
+def hilbert_order(grid):
+    """permute.py:97-128 — flat token order along the 2D curve / 3D serpentine of 2D curves."""
+    def walk(n0, n1):
+        if n0 >= n1:
+            return _gilbert(0, 0, n0, 0, 0, n1)
+        return [(x, y) for (y, x) in _gilbert(0, 0, n1, 0, 0, n0)]
+    grid = [int(g) for g in grid]
+    if len(grid) == 2:
+        return np.array([x * grid[1] + y for (x, y) in walk(*grid)], dtype=np.int64)
+    n0, n1, n2 = grid
+    plane, flat = walk(n1, n2), []
+    for s in range(n0):
+        if s:
+            plane = plane[::-1]
+        flat.extend(s * n1 * n2 + x * n2 + y for (x, y) in plane)
+    return np.array(flat, dtype=np.int64)
+
+
 # --------------------------------------------------------------------------- composition
 def run_head(q, k, v, lay, *, estimator="sampled-max", s_q=None, s_k=None, seed=None,
              stride=None, mask="threshold", thresholds=None, cutpoints=None, tau=None,
-             sim_thresholds=None, causal=False, executor="streaming", rows_of=None):
-    """pipeline.py:256-314 stage order without permutation, scheduler and dense oracle.
+             sim_thresholds=None, causal=False, executor="streaming", rows_of=None,
+             grid=None, unpermute=False):
+    """pipeline.py:256-314 stage order (with the optional curve permutation) without the
+    scheduler and dense oracle. With ``unpermute`` both out and lse return in input order.
 
     Returns dict(scores, mask, caps, out, lse, skipped, report)."""
     q, k, v = (np.asarray(x, np.float64) for x in (q, k, v))
+    perm = None
+    if grid is not None:
+        perm = hilbert_order(grid)
+        q, k, v = q[perm], k[perm], v[perm]
     kl, vl = build_pyramid(k, v, lay)
     if estimator == "antidiagonal":
         scores = importance_antidiagonal(q, k, lay, stride)
@@ -381,6 +433,10 @@ def run_head(q, k, v, lay, *, estimator="sampled-max", s_q=None, s_k=None, seed=
         out, lse, skipped = psa_streaming(q, kl, vl, m, lay, causal)
     else:
         out, lse, skipped = psa_materialized(q, kl, vl, m, lay, causal, rows_of=rows_of)
+    if perm is not None and unpermute:
+        inv = np.empty_like(perm)
+        inv[perm] = np.arange(perm.size)
+        out, lse = out[inv], lse[inv]
     return {"scores": scores, "mask": m, "caps": caps, "out": out, "lse": lse,
             "skipped": skipped, "report": sparsity_report(m, lay.levels), "pyramid": (kl, vl)}
 

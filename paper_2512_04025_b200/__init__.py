@@ -15,6 +15,7 @@ from .layout import (PRESET_CUTPOINTS, BlockLayout, LevelThresholds, QuantileCut
                      SamplerConfig, SimThresholds, make_layout)
 from .mask import (MaskPlan, SparsityReport, assign_quantile, assign_threshold, binary_mask,
                    causal_premask, combine_mask, report_from_counts, sparsity_report)
+from .permute import Permutation, apply_permutation, hilbert_order, invert_permutation
 from .pipeline import PSAResult, RunConfig, psa_attention, psa_forward_4d
 from .pyramid import PyramidKV, build_pyramid, level_cap_from_similarity
 
@@ -22,6 +23,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "AttentionOutput", "BlockLayout", "LN2", "LevelThresholds", "MaskPlan", "NumericError",
+    "Permutation", "apply_permutation", "hilbert_order", "invert_permutation",
     "PRESET_CUTPOINTS", "PSAResult", "PyramidKV", "QuantileCutpoints", "RunConfig",
     "SamplerConfig", "SimThresholds", "SparsityReport", "TensorFileError", "ValidationError",
     "assign_quantile", "assign_threshold", "binary_mask", "build_pyramid",

@@ -4,8 +4,9 @@ pkg/src/pyrattn/pipeline.py:256-314) run for every (batch, head) at once on the 
   pyramid (K1) -> importance (K2, non-causal) -> level assignment (K3) [-> similarity cap]
   [-> causal pre-pass] -> multi-level attention (K4)
 
-The dense oracle, the Python tile scheduler and the Hilbert permutation of the reference run
-are not part of this operator. ``RunConfig`` keeps the reference's flat key
+The reference's optional space-filling-curve permutation (``grid``/``unpermute``) runs as
+row gathers in libpsa; the dense oracle of the reference run is not part of this operator
+(see DESIGN.md). ``RunConfig`` keeps the reference's flat key
 names and validation (pipeline.py:38-137) so existing JSON configs drive the GPU path.
 """
 
@@ -24,6 +25,7 @@ from .importance import antidiagonal_scores, importance_scores
 from .layout import (PRESET_CUTPOINTS, LevelThresholds, QuantileCutpoints, SamplerConfig,
                      SimThresholds, make_layout)
 from .mask import MaskPlan, assign_levels_device
+from .permute import gather_rows, hilbert_order
 from .pyramid import PyramidKV, build_pyramid, similarity_caps
 
 ESTIMATORS = ("sampled-max", "sampled-mean", "antidiagonal")
@@ -169,9 +171,13 @@ def psa_forward_4d(q4, k4, v4, cfg: RunConfig, keep_scores: bool = False,
     optional preallocated device outputs)."""
     lay = cfg.layout()
     lay.check_gpu()
-    if cfg.grid is not None:
-        raise ValidationError("[stage: permutation] the Hilbert token permutation is not part "
-                              "of the sm_100a operator yet; permute Q/K/V before the call")
+    perm = None
+    if cfg.grid is not None:  # pipeline.py:257-263: curve order applied to Q, K and V
+        perm = _stage("permutation", hilbert_order, cfg.grid)
+        order, _ = perm.on(q4.device)
+        q4, k4, v4 = (gather_rows(x, order) for x in (q4, k4, v4))
+        final_out, final_lse = out, lse
+        out = lse = None
     mode, rule = _mask_rule(cfg, lay.levels)
     B, Hq = q4.shape[:2]
     Hkv = k4.shape[1]
@@ -188,6 +194,19 @@ def psa_forward_4d(q4, k4, v4, cfg: RunConfig, keep_scores: bool = False,
     plan = _stage("mask", assign_levels_device, scores, mode=mode, rule=rule, levels=lay.levels,
                   b_q=lay.q_block, b_k=lay.k_block, hkv=Hkv, caps=caps, causal=cfg.causal)
     out, lse, skipped = _stage("executor", attention_forward, q4, pyr, plan, cfg.causal, out, lse)
+    if perm is not None:
+        if cfg.unpermute:  # pipeline.py:312-313: back to the caller's token order
+            _, inverse = perm.on(q4.device)
+            out = gather_rows(out, inverse, final_out)
+            lse = gather_rows(lse.unsqueeze(-1), inverse,
+                              None if final_lse is None else final_lse.unsqueeze(-1)).squeeze(-1)
+        else:
+            if final_out is not None:
+                final_out.copy_(out)
+                out = final_out
+            if final_lse is not None:
+                final_lse.copy_(lse)
+                lse = final_lse
     return PSAResult(out=out, lse=lse, plan=plan, skipped=skipped,
                      scores=scores if keep_scores else None, pyramid=pyr)
 

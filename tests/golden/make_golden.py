@@ -44,9 +44,14 @@ def qkv(seed, n, d, kind="gaussian"):
 
 def case(name, n, d, bq, bk, H, *, seed, kind="gaussian", estimator="sampled-max", s_q=8,
          s_k=8, mask="threshold", thresholds=None, cutpoints=None, tau=None, sim=None,
-         causal=False, stride=None, keep_pyramid=False):
+         causal=False, stride=None, keep_pyramid=False, grid=None, unpermute=False):
     q, k, v = qkv(seed, n, d, kind)
     lay = ref.make_layout(n, d, bq, bk, H)
+    q_in, k_in, v_in = q, k, v
+    perm = None
+    if grid is not None:  # pipeline.py:257-263
+        perm = ref.hilbert_order(grid)
+        q, k, v = (ref.apply_permutation(x, perm) for x in (q, k, v))
     pyr = ref.build_pyramid(k, v, lay)
     if estimator == "antidiagonal":
         scores = ref.importance_antidiagonal(q, k, lay, stride)
@@ -67,19 +72,25 @@ def case(name, n, d, bq, bk, H, *, seed, kind="gaussian", estimator="sampled-max
     if causal:
         m = ref.causal_premask(m, lay)
     att = ref.psa_streaming(q, pyr, m, causal=causal)
+    out, lse = att.out, att.row_log_normalizers
+    if perm is not None and unpermute:  # pipeline.py:312-313 (lse follows out's row order)
+        inv = ref.invert_permutation(perm)
+        out = ref.apply_permutation(out, inv)
+        lse = lse[inv.order]
     rep = ref.sparsity_report(m, levels=H)
     levels_k = [np.concatenate([pyr.k(j, h) for j in range(lay.n_k)]) for h in range(1, H + 1)]
     levels_v = [np.concatenate([pyr.v(j, h) for j in range(lay.n_k)]) for h in range(1, H + 1)]
     payload = dict(
-        q=bits(q), k=bits(k), v=bits(v),
+        q=bits(q_in), k=bits(k_in), v=bits(v_in),
         layout=np.array([n, d, bq, bk, H]), scores=scores, mask=m,
         caps=caps if caps is not None else np.zeros(0, np.int64),
-        out=att.out, lse=att.row_log_normalizers, skipped=np.array(att.skipped_rows),
+        out=out, lse=lse, skipped=np.array(att.skipped_rows),
         level_counts=np.array(rep.level_counts), rho_bar=np.array(rep.rho_bar),
         kv_coverage=np.array(rep.kv_coverage),
         config=np.array(repr(dict(estimator=estimator, s_q=s_q, s_k=s_k, seed=0, mask=mask,
                                   thresholds=thresholds, cutpoints=cutpoints, tau=tau,
-                                  sim_thresholds=sim, causal=causal, stride=stride))),
+                                  sim_thresholds=sim, causal=causal, stride=stride, grid=grid,
+                                  unpermute=unpermute))),
     )
     for h in range(2, H + 1 if keep_pyramid else 2):
         payload[f"k_level{h}"] = levels_k[h - 1]
@@ -90,7 +101,16 @@ def case(name, n, d, bq, bk, H, *, seed, kind="gaussian", estimator="sampled-max
 
 TAUS = (0.164713, 0.282366, 0.376488, 0.95)
 
+def hilbert_fixture():
+    grids = [(4, 4), (8, 2), (2, 16), (16, 16), (64, 32), (3, 5, 6), (2, 3, 4), (5, 7, 9),
+             (1, 8, 8), (21, 45, 80)]
+    payload = {f"g{i}": np.array(g) for i, g in enumerate(grids)}
+    payload.update({f"o{i}": ref.hilbert_order(g).order for i, g in enumerate(grids)})
+    np.savez_compressed(HERE / "hilbert_orders.npz", **payload)
+
+
 if __name__ == "__main__":
+    hilbert_fixture()
     case("cfg1_small", 1024, 64, 64, 64, 4, seed=1, thresholds=TAUS, keep_pyramid=True)
     case("wan_b120", 960, 128, 120, 120, 4, seed=2, thresholds=(0.1634, 0.2803, 0.3738, 0.95),
          keep_pyramid=True)
@@ -109,6 +129,10 @@ if __name__ == "__main__":
          stride=8, thresholds=TAUS, sim=(0.75, 0.70, 0.70), causal=True)
     case("antidiag_stride4_b120", 960, 128, 120, 120, 4, seed=11, estimator="antidiagonal",
          stride=4, thresholds=(0.1634, 0.2803, 0.3738, 0.95))
+    # space-filling-curve token order (pipeline.py:257-263, 312-313): 2D Hilbert and 3D serpentine
+    case("hilbert2d_corr", 1024, 64, 64, 64, 4, seed=13, kind="correlated", thresholds=TAUS,
+         grid=(32, 32), unpermute=True)
+    case("hilbert3d_permuted_out", 960, 64, 64, 64, 4, seed=14, thresholds=TAUS, grid=(6, 10, 16))
     # stride does not divide q_block: residue classes of unequal size
     case("antidiag_ragged", 960, 64, 60, 48, 4, seed=12, estimator="antidiagonal", stride=8,
          thresholds=TAUS)

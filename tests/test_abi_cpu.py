@@ -18,7 +18,7 @@ def _declared():
 def test_header_declares_expected_entry_points():
     names = _declared()
     for n in ("psa_pyramid_build", "psa_similarity_caps", "psa_importance_sampled",
-              "psa_importance_antidiagonal", "psa_antidiag_workspace_bytes",
+              "psa_importance_antidiagonal", "psa_antidiag_workspace_bytes", "psa_gather_rows",
               "psa_assign_levels", "psa_mask_to_plan", "psa_attn_fwd", "psa_last_error"):
         assert n in names
 
@@ -48,6 +48,8 @@ def test_argument_errors_map_to_validation_error():
     assert lib.psa_importance_workspace_bytes(2, 2, 10, 8, 10, 40) == 8 * (2 * 80 * 10 + 2 * 2 * 80)
     # s_k = 8: plus the int8 slices of the exact tensor-core path
     assert lib.psa_importance_workspace_bytes(2, 2, 10, 8, 10, 8) > 8 * (2 * 80 * 10 + 2 * 2 * 80)
+    rc = lib.psa_gather_rows(1, 1, 16, 6, 1, 2, None)  # row_bytes must be a multiple of 4
+    assert rc == _lib.PSA_EINVAL
     # antidiagonal: stride must divide k_block, k_block/stride <= 64
     rc = lib.psa_importance_antidiagonal(1, 1, 1, 1, 1, 1024, 128, 64, 64, 3, 0, 1, 1, None)
     assert rc == _lib.PSA_EINVAL and "stride" in lib.psa_last_error().decode()

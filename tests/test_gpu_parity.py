@@ -365,3 +365,21 @@ def test_int8_exact_logits_match_fp64_path(kind, n, d, b, sk_or_stride, tiny):
         exp = (orc.importance_sampled(q[h], k[h], olay, 8, sk_or_stride, 0, "max")
                if kind == "sampled" else orc.importance_antidiagonal(q[h], k[h], olay, sk_or_stride))
         np.testing.assert_allclose(f[h], exp, rtol=1e-12, atol=0)
+
+
+# ------------------------------------------------------------------ token permutation
+@pytest.mark.parametrize("grid,d", [((32, 32), 64), ((6, 10, 16), 128), ((21, 45, 8), 128)])
+def test_apply_permutation_exact(grid, d):
+    """psa_gather_rows == numpy fancy indexing (permute.py:131-137), bit for bit; the inverse
+    permutation restores the input."""
+    psa = _psa()
+    n = int(np.prod(grid))
+    x = torch.randn(2, 3, n, d, dtype=torch.bfloat16, device="cuda")
+    p = psa.hilbert_order(grid)
+    y = psa.apply_permutation(x, p)
+    ref = x.cpu()[:, :, p.order]
+    assert torch.equal(y.cpu().view(torch.int16), ref.view(torch.int16))
+    back = psa.apply_permutation(y, psa.invert_permutation(p))
+    assert torch.equal(back.view(torch.int16), x.view(torch.int16))
+    single = psa.apply_permutation(x[0, 0], p)  # (n, d) form
+    assert torch.equal(single.cpu().view(torch.int16), ref[0, 0].view(torch.int16))

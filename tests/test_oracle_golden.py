@@ -18,7 +18,8 @@ def test_oracle_matches_reference_golden(name):
     r = orc.run_head(g["q"], g["k"], g["v"], lay, estimator=c["estimator"], s_q=c["s_q"],
                      s_k=c["s_k"], seed=c["seed"], stride=c["stride"], mask=c["mask"],
                      thresholds=c["thresholds"], cutpoints=c["cutpoints"], tau=c["tau"],
-                     sim_thresholds=c["sim_thresholds"], causal=c["causal"])
+                     sim_thresholds=c["sim_thresholds"], causal=c["causal"],
+                     grid=c.get("grid"), unpermute=c.get("unpermute", False))
     # importance: same numpy ops in the same order -> identical bits
     assert np.array_equal(r["scores"], g["scores"])
     assert np.array_equal(r["mask"], g["mask"])
@@ -103,3 +104,24 @@ def test_mixed_levels_budget():
     m[0, :3], m[0, 3:5], m[0, 5:9] = 1, 2, 3
     rep = orc.sparsity_report(m, 3)
     assert rep["rho_bar"] == 0.25 and rep["kv_coverage"] == 0.45
+
+
+def test_hilbert_orders_match_reference():
+    """Curve orders (permute.py:97-128): the oracle restatement and the product's host-side
+    generator both equal the reference's, including the Wan 21x45x80 latent grid."""
+    import paper_2512_04025_b200 as psa
+    from helpers import GOLDEN_DIR
+    z = np.load(GOLDEN_DIR / "hilbert_orders.npz")
+    n = len([k for k in z.files if k.startswith("g")])
+    for i in range(n):
+        grid = tuple(int(g) for g in z[f"g{i}"])
+        assert np.array_equal(orc.hilbert_order(grid), z[f"o{i}"]), grid
+        p = psa.hilbert_order(grid)
+        assert np.array_equal(p.order.numpy(), z[f"o{i}"]), grid
+        assert np.array_equal(p.order.numpy()[p.inverse.numpy()], np.arange(len(p)))
+    with pytest.raises(psa.ValidationError):
+        psa.hilbert_order((6, 8))           # 2D axes must be powers of two
+    with pytest.raises(psa.ValidationError):
+        psa.hilbert_order((2, 2, 2, 2))
+    inv = psa.invert_permutation(psa.hilbert_order((4, 4)))
+    assert np.array_equal(inv.order.numpy(), psa.hilbert_order((4, 4)).inverse.numpy())
