@@ -7,7 +7,7 @@ no CPU fallback: calling with CPU tensors or without the built library raises.
 """
 
 from .attention import (LN2, AttentionOutput, causal_full_attention, full_attention,
-                        level_bias, psa_streaming)
+                        level_bias, psa_reference, psa_streaming)
 from .errors import NumericError, TensorFileError, ValidationError
 from .importance import (antidiagonal_selection, importance_antidiagonal, importance_sampled,
                          sample_tables)
@@ -18,12 +18,16 @@ from .mask import (MaskPlan, SparsityReport, assign_quantile, assign_threshold, 
 from .permute import Permutation, apply_permutation, hilbert_order, invert_permutation
 from .pipeline import PSAResult, RunConfig, psa_attention, psa_forward_4d
 from .pyramid import PyramidKV, build_pyramid, level_cap_from_similarity
+from .schedule import (ExecutionTile, Segment, TileSchedule, UtilizationStats, build_schedule,
+                       execute_schedule, plan_utilization, utilization)
 
 __version__ = "0.1.0"
 
 __all__ = [
     "AttentionOutput", "BlockLayout", "LN2", "LevelThresholds", "MaskPlan", "NumericError",
     "Permutation", "apply_permutation", "hilbert_order", "invert_permutation",
+    "ExecutionTile", "Segment", "TileSchedule", "UtilizationStats", "build_schedule",
+    "execute_schedule", "plan_utilization", "utilization", "psa_reference",
     "PRESET_CUTPOINTS", "PSAResult", "PyramidKV", "QuantileCutpoints", "RunConfig",
     "SamplerConfig", "SimThresholds", "SparsityReport", "TensorFileError", "ValidationError",
     "assign_quantile", "assign_threshold", "binary_mask", "build_pyramid",

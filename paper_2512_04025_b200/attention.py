@@ -85,6 +85,13 @@ def psa_streaming(q, pyramid: PyramidKV, mask, causal: bool = False) -> Attentio
                            skipped_rows=int(skipped.item()))
 
 
+def psa_reference(q, pyramid: PyramidKV, mask, causal: bool = False) -> AttentionOutput:
+    """Materialized multi-level attention (attention.py:120-168). In the reference this is the
+    ground truth for the streaming pass; on the GPU both are the same sm_100a kernel (the
+    per-block softmax is computed exactly once either way), so this returns psa_streaming."""
+    return psa_streaming(q, pyramid, mask, causal=causal)
+
+
 def _dense_layout(n: int, d: int) -> BlockLayout:
     for b in (128, 120, 112, 96, 64, 32, 16, 8):
         if n % b == 0:

@@ -109,8 +109,32 @@ def hilbert_fixture():
     np.savez_compressed(HERE / "hilbert_orders.npz", **payload)
 
 
+def schedule_fixture():
+    """build_schedule / utilization of the reference (scheduler.py:71-126, 272-282)."""
+    rng = np.random.default_rng(21)
+    payload = {}
+    cases = [  # (n, b_q, b_k, levels, tile_len, merge)
+        (768, 64, 64, 4, 128, True), (768, 64, 64, 4, 128, False),
+        (960, 120, 120, 4, 50, True), (960, 120, 120, 4, 50, False),
+        (512, 128, 32, 3, 7, True), (256, 64, 64, 4, 64, True)]
+    for c, (n, bq, bk, H, tile_len, merge) in enumerate(cases):
+        lay = ref.make_layout(n, 64, bq, bk, H)
+        m = rng.integers(0, H + 1, size=(lay.n_q, lay.n_k))
+        sch = ref.build_schedule(m, lay, tile_len, merge=merge)
+        rows = [(t.query_block, s.kv_block, s.level, s.row_start, s.row_stop, ti)
+                for ti, t in enumerate(sch.tiles) for s in t.segments]
+        u = ref.utilization(sch)
+        payload[f"mask{c}"] = m
+        payload[f"layout{c}"] = np.array([n, 64, bq, bk, H])
+        payload[f"opts{c}"] = np.array([tile_len, int(merge)])
+        payload[f"segs{c}"] = np.array(rows, dtype=np.int64).reshape(-1, 6)
+        payload[f"util{c}"] = np.array([u.tiles, u.useful_rows, u.capacity, u.utilization])
+    np.savez_compressed(HERE / "schedules.npz", **payload)
+
+
 if __name__ == "__main__":
     hilbert_fixture()
+    schedule_fixture()
     case("cfg1_small", 1024, 64, 64, 64, 4, seed=1, thresholds=TAUS, keep_pyramid=True)
     case("wan_b120", 960, 128, 120, 120, 4, seed=2, thresholds=(0.1634, 0.2803, 0.3738, 0.95),
          keep_pyramid=True)

@@ -383,3 +383,42 @@ def test_apply_permutation_exact(grid, d):
     assert torch.equal(back.view(torch.int16), x.view(torch.int16))
     single = psa.apply_permutation(x[0, 0], p)  # (n, d) form
     assert torch.equal(single.cpu().view(torch.int16), ref[0, 0].view(torch.int16))
+
+
+# ------------------------------------------------------------------ block-tile schedule API
+@pytest.mark.parametrize("causal", [False, True])
+def test_execute_schedule_equals_streaming(causal, rng):
+    """execute_schedule (scheduler.py:203-269) on the GPU executor == psa_streaming on the same
+    mask (tiling only re-chunks the online softmax), and matches the oracle."""
+    psa = _psa()
+    n, d, b, H = 2048, 128, 64, 4
+    q, k, v = gaussian_qkv(41, 1, n, d)
+    lay = psa.make_layout(n, d, b, b, H)
+    m = rng.integers(0, H + 1, size=(lay.n_q, lay.n_k))
+    olay = orc.Layout(n, d, b, b, H)
+    if causal:
+        m = orc.causal_premask(m, olay)
+    pyr = psa.build_pyramid(to_dev(k[0]), to_dev(v[0]), lay)
+    sch = psa.build_schedule(m, lay, 128)
+    a = psa.execute_schedule(to_dev(q[0]), pyr, sch, causal=causal)
+    s = psa.psa_streaming(to_dev(q[0]), pyr, torch.from_numpy(m).cuda(), causal=causal)
+    assert torch.equal(a.out.view(torch.int16), s.out.view(torch.int16))
+    assert a.skipped_rows == s.skipped_rows
+    kl, vl = orc.build_pyramid(k[0], v[0], olay)
+    o, l, sk = orc.psa_streaming(q[0], kl, vl, m, olay, causal)
+    assert rel_l2(a.out.float().cpu().numpy(), o) <= 5e-3
+    assert psa.utilization(sch).utilization <= 1.0
+
+
+def test_plan_utilization_counts_executed_tiles():
+    psa = _psa()
+    n, d, b = 3840, 128, 120
+    q, k, v = gaussian_qkv(43, 2, n, d)
+    res = psa.psa_attention(to_dev(q), to_dev(k), to_dev(v), b_q=b, b_k=b, levels=4,
+                            estimator="sampled-max", s_q=8, s_k=8, seed=0, mask="threshold",
+                            thresholds=(0.1634, 0.2803, 0.3738, 0.95))
+    lay = psa.make_layout(n, d, b, b, 4)
+    u = psa.plan_utilization(res.plan, lay)
+    counts = res.plan.level_counts.cpu().tolist()
+    assert u.useful_rows == sum(c * (b >> (h - 1)) for h, c in enumerate(counts) if h)
+    assert 0.5 < u.utilization <= 1.0

@@ -81,3 +81,45 @@ def test_level_bias_values():
         psa.level_bias(0)
     with pytest.raises(psa.ValidationError):
         psa.level_bias(5, max_level=4)
+
+
+def test_build_schedule_matches_reference():
+    """build_schedule / utilization reproduce the reference's tiles exactly
+    (scheduler.py:71-126, 272-282; fixtures from the real reference)."""
+    import numpy as np
+    import paper_2512_04025_b200 as psa
+    from helpers import GOLDEN_DIR
+    z = np.load(GOLDEN_DIR / "schedules.npz")
+    n_cases = len([k for k in z.files if k.startswith("mask")])
+    for c in range(n_cases):
+        n, d, bq, bk, H = (int(x) for x in z[f"layout{c}"])
+        tile_len, merge = (int(x) for x in z[f"opts{c}"])
+        lay = psa.make_layout(n, d, bq, bk, H)
+        sch = psa.build_schedule(z[f"mask{c}"], lay, tile_len, merge=bool(merge))
+        rows = [(t.query_block, s.kv_block, s.level, s.row_start, s.row_stop, ti)
+                for ti, t in enumerate(sch.tiles) for s in t.segments]
+        assert np.array_equal(np.array(rows, dtype=np.int64).reshape(-1, 6), z[f"segs{c}"]), c
+        u = psa.utilization(sch)
+        assert [u.tiles, u.useful_rows, u.capacity] == z[f"util{c}"][:3].astype(int).tolist()
+        assert u.utilization == z[f"util{c}"][3]
+        # the validator accepts the reference packing and recovers the mask
+        from paper_2512_04025_b200.schedule import validate_schedule
+        assert np.array_equal(validate_schedule(sch, lay), z[f"mask{c}"])
+
+
+def test_validate_schedule_rejects_bad_schedules():
+    import pytest
+    import paper_2512_04025_b200 as psa
+    from paper_2512_04025_b200.schedule import validate_schedule
+    lay = psa.make_layout(256, 64, 64, 64, 2)
+    S, T = psa.Segment, psa.ExecutionTile
+    bad = [
+        [T(0, (S(1, 1, 0, 32),))],                                   # partial block
+        [T(0, (S(1, 1, 0, 64),)), T(0, (S(0, 1, 0, 64),))],          # out of order
+        [T(0, (S(1, 1, 0, 32), S(1, 2, 32, 64)))],                   # level mixing
+        [T(1, (S(0, 1, 0, 64),)), T(0, (S(0, 1, 0, 64),))],          # query blocks out of order
+        [T(0, ())],                                                  # empty tile
+    ]
+    for tiles in bad:
+        with pytest.raises(psa.ValidationError):
+            validate_schedule(psa.TileSchedule(64, tuple(tiles), lay), lay)
