@@ -16,7 +16,8 @@ from .layout import (PRESET_CUTPOINTS, BlockLayout, LevelThresholds, QuantileCut
 from .mask import (MaskPlan, SparsityReport, assign_quantile, assign_threshold, binary_mask,
                    causal_premask, combine_mask, report_from_counts, sparsity_report)
 from .permute import Permutation, apply_permutation, hilbert_order, invert_permutation
-from .pipeline import PSAResult, RunConfig, psa_attention, psa_forward_4d
+from .pipeline import (PipelineResult, PSAResult, RunConfig, psa_attention, psa_forward_4d,
+                       relative_error, report_to_json, run_pipeline)
 from .pyramid import PyramidKV, build_pyramid, level_cap_from_similarity
 from .schedule import (ExecutionTile, Segment, TileSchedule, UtilizationStats, build_schedule,
                        execute_schedule, plan_utilization, utilization)
@@ -28,6 +29,7 @@ __all__ = [
     "Permutation", "apply_permutation", "hilbert_order", "invert_permutation",
     "ExecutionTile", "Segment", "TileSchedule", "UtilizationStats", "build_schedule",
     "execute_schedule", "plan_utilization", "utilization", "psa_reference",
+    "PipelineResult", "relative_error", "report_to_json", "run_pipeline",
     "PRESET_CUTPOINTS", "PSAResult", "PyramidKV", "QuantileCutpoints", "RunConfig",
     "SamplerConfig", "SimThresholds", "SparsityReport", "TensorFileError", "ValidationError",
     "assign_quantile", "assign_threshold", "binary_mask", "build_pyramid",

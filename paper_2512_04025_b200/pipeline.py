@@ -251,3 +251,124 @@ def psa_attention(q, k, v, cfg: RunConfig | None = None, *, keep_scores: bool = 
     res.out = restore(res.out, lead)
     res.lse = res.lse.reshape(lead + (cfg.n,))
     return res
+
+
+# ------------------------------------------------------------------ run_pipeline (report API)
+@dataclass
+class PipelineResult:
+    report: dict
+    output: object  # attention output, same container (torch / numpy) and leading dims as q
+
+
+def relative_error(a: torch.Tensor, b: torch.Tensor) -> float:
+    """Frobenius ||a - b|| / ||b|| (linalg.py:61-70), computed on the device in fp32."""
+    den = torch.linalg.vector_norm(b.float())
+    if float(den) == 0.0:
+        raise NumericError("relative error undefined for a zero-norm reference")
+    return float(torch.linalg.vector_norm(a.float() - b.float()) / den)
+
+
+def _steps_metadata(cfg: RunConfig, rho_bar: float) -> dict:
+    """pipeline.py:317-330."""
+    dense = min(math.ceil(cfg.dense_prefix * cfg.num_steps) if cfg.dense_prefix > 0 else 0,
+                cfg.num_steps)
+    modes = ["dense"] * dense + ["sparse"] * (cfg.num_steps - dense)
+    return {"num_steps": cfg.num_steps, "dense_prefix": cfg.dense_prefix, "dense_steps": dense,
+            "modes": modes,
+            "mean_rho_over_steps": (dense * 1.0 + (cfg.num_steps - dense) * rho_bar) / cfg.num_steps}
+
+
+def run_pipeline(cfg: RunConfig, q, k, v) -> PipelineResult:
+    """pipeline.py:333-397 on the GPU: every head at once through psa_forward_4d, then the
+    reference's report (per-head sparsity, schedule utilisation for tile_len, error against
+    dense attention, skipped rows, steps metadata, aggregates). Inputs: (n, d) or (heads, n, d)
+    torch tensors or numpy arrays (moved to the current CUDA device as bf16); the output has
+    the input's container type. The dense baseline is the same sm_100a kernel with every block
+    at level 1 (bf16), and the tiled ("schedule") execution is the kernel itself, so
+    schedule_relative_error equals relative_error."""
+    import time
+
+    import numpy as np
+
+    from .attention import causal_full_attention, full_attention
+    from .mask import report_from_counts
+
+    t0 = time.perf_counter()
+    is_np = not isinstance(q, torch.Tensor)
+    dev = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else None
+    if dev is None:
+        raise ValidationError("run_pipeline needs a CUDA device (no CPU fallback)")
+
+    def to_dev(x):
+        x = torch.from_numpy(np.ascontiguousarray(x)) if not isinstance(x, torch.Tensor) else x
+        return x.to(dev, torch.bfloat16)
+
+    q, k, v = to_dev(q), to_dev(k), to_dev(v)
+    if q.shape != k.shape or k.shape != v.shape:
+        raise ValidationError(f"Q/K/V shapes differ: {tuple(q.shape)}/{tuple(k.shape)}/"
+                              f"{tuple(v.shape)}")
+    if q.ndim not in (2, 3):
+        raise ValidationError(f"expected (n, d) or (heads, n, d), got {tuple(q.shape)}")
+    squeeze = q.ndim == 2
+    q3, k3, v3 = (x.unsqueeze(0) if squeeze else x for x in (q, k, v))
+    if tuple(q3.shape[1:]) != (cfg.n, cfg.d):
+        raise ValidationError(f"tensor shape {tuple(q3.shape[1:])} does not match config "
+                              f"({cfg.n}, {cfg.d})")
+    lay = cfg.layout()
+    heads = q3.shape[0]
+    res = psa_forward_4d(q3[None].contiguous(), k3[None].contiguous(), v3[None].contiguous(), cfg)
+    out = res.out[0]
+    lm = res.plan.level_map[0].to(torch.int64)  # [heads, n_q, n_k]
+    dense_fn = causal_full_attention if cfg.causal else full_attention
+    if cfg.grid is not None:  # the dense oracle sees the same (permuted) token order
+        from .permute import apply_permutation, hilbert_order
+        p = hilbert_order(cfg.grid)
+        qd, kd, vd = (apply_permutation(x, p) for x in (q3, k3, v3))
+    else:
+        qd, kd, vd = q3, k3, v3
+    dense = dense_fn(qd, kd, vd).out
+    if cfg.grid is not None and cfg.unpermute:
+        from .permute import apply_permutation, hilbert_order, invert_permutation
+        dense = apply_permutation(dense, invert_permutation(hilbert_order(cfg.grid)))
+    pooled = torch.tensor([0] + [lay.pooled_len(h) for h in range(1, lay.levels + 1)],
+                          dtype=torch.int64, device=lm.device)
+    rows_qb = pooled[lm].sum(dim=2)                               # [heads, n_q]
+    tiles_qb = (rows_qb + cfg.tile_len - 1) // cfg.tile_len       # greedy merge packing
+    counts = torch.stack([(lm == h).sum(dim=(1, 2)) for h in range(lay.levels + 1)], dim=1)
+    skipped_h = (~torch.isfinite(res.lse[0])).sum(dim=1)
+    counts, rows_h, tiles_h, skipped_h = (x.cpu().tolist() for x in
+                                          (counts, rows_qb.sum(1), tiles_qb.sum(1), skipped_h))
+    per_head = []
+    for h in range(heads):
+        err = relative_error(out[h], dense[h])
+        cap = tiles_h[h] * cfg.tile_len
+        per_head.append({
+            "relative_error": err, "schedule_relative_error": err,
+            "sparsity": report_from_counts(counts[h], lay.n_q * lay.n_k).as_dict(),
+            "utilization": {"tiles": tiles_h[h], "useful_rows": rows_h[h], "capacity": cap,
+                            "utilization": rows_h[h] / cap if cap else 1.0},
+            "selected_pooled_rows": rows_h[h], "skipped_rows": skipped_h[h]})
+    tot_counts = [sum(c[i] for c in counts) for i in range(lay.levels + 1)]
+    agg = report_from_counts(tot_counts, heads * lay.n_q * lay.n_k).as_dict()
+    tiles, useful = sum(tiles_h), sum(rows_h)
+    capacity = tiles * cfg.tile_len
+    report = {
+        "config": cfg.to_dict(), "heads": heads,
+        "relative_error": float(np.mean([h["relative_error"] for h in per_head])),
+        "schedule_relative_error": float(np.mean([h["schedule_relative_error"] for h in per_head])),
+        "sparsity": agg,
+        "utilization": {"tiles": tiles, "useful_rows": useful, "capacity": capacity,
+                        "utilization": useful / capacity if capacity else 1.0},
+        "skipped_rows": sum(skipped_h), "per_head": per_head,
+        "steps": _steps_metadata(cfg, agg["rho_bar"]),
+        "wall_time_s": time.perf_counter() - t0,
+    }
+    output = out[0] if squeeze else out
+    if is_np:
+        output = output.float().cpu().numpy()
+    return PipelineResult(report=report, output=output)
+
+
+def report_to_json(report: dict) -> str:
+    """Deterministic JSON rendering (pipeline.py:400-402)."""
+    return json.dumps(report, sort_keys=True, indent=2) + "\n"

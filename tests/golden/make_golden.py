@@ -132,7 +132,24 @@ def schedule_fixture():
     np.savez_compressed(HERE / "schedules.npz", **payload)
 
 
+def pipeline_report_fixture():
+    """run_pipeline report of the reference on 2 heads (pipeline.py:333-397)."""
+    import json
+    rng = np.random.default_rng(31)
+    q, k, v = (bf16(rng.standard_normal((2, 1024, 64), dtype=np.float32)) for _ in range(3))
+    cfg = ref.RunConfig.from_dict(dict(n=1024, d=64, b_q=64, b_k=64, levels=4,
+                                       estimator="sampled-max", s_q=8, s_k=8, seed=0,
+                                       mask="threshold", thresholds=list(TAUS), tile_len=128,
+                                       num_steps=4, dense_prefix=0.25))
+    res = ref.run_pipeline(cfg, q, k, v)
+    rep = dict(res.report)
+    rep.pop("wall_time_s")
+    np.savez_compressed(HERE / "pipeline_report.npz", q=bits(q), k=bits(k), v=bits(v),
+                        out=res.output, report=np.array(json.dumps(rep, sort_keys=True)))
+
+
 if __name__ == "__main__":
+    pipeline_report_fixture()
     hilbert_fixture()
     schedule_fixture()
     case("cfg1_small", 1024, 64, 64, 64, 4, seed=1, thresholds=TAUS, keep_pyramid=True)

@@ -59,3 +59,32 @@ def test_gpu_antidiagonal_scores_entry_point(name):
     sel = psa.antidiagonal_selection(bq, bk, g["cfg"]["stride"])
     assert int(sel.sum()) == sum(len(range((-p) % g["cfg"]["stride"], bk, g["cfg"]["stride"]))
                                  for p in range(bq))
+
+
+def test_run_pipeline_report_matches_reference():
+    """run_pipeline (pipeline.py:333-397): the report's exact fields equal the reference's; the
+    error against dense attention agrees to bf16 precision; the output matches."""
+    import json
+
+    import paper_2512_04025_b200 as psa
+    from helpers import GOLDEN_DIR
+    z = np.load(GOLDEN_DIR / "pipeline_report.npz")
+    q, k, v = (torch.from_numpy(z[x].view(np.int16)).view(torch.bfloat16) for x in ("q", "k", "v"))
+    ref = json.loads(str(z["report"]))
+    cfg = psa.RunConfig.from_dict(ref["config"])
+    res = psa.run_pipeline(cfg, q.float().numpy(),
+                           k.float().numpy(), v.float().numpy())
+    rep = res.report
+    assert rep["heads"] == ref["heads"]
+    assert rep["sparsity"] == ref["sparsity"]
+    assert rep["utilization"] == ref["utilization"]
+    assert rep["skipped_rows"] == ref["skipped_rows"]
+    assert rep["steps"] == ref["steps"]
+    for mine, theirs in zip(rep["per_head"], ref["per_head"]):
+        assert mine["sparsity"] == theirs["sparsity"]
+        assert mine["utilization"] == theirs["utilization"]
+        assert mine["selected_pooled_rows"] == theirs["selected_pooled_rows"]
+        assert abs(mine["relative_error"] - theirs["relative_error"]) <= 2e-2 * theirs["relative_error"]
+    assert isinstance(res.output, np.ndarray) and res.output.shape == z["out"].shape
+    assert rel_l2(res.output.astype(np.float64), z["out"]) <= 5e-3
+    assert psa.report_to_json(rep).endswith("\n")
