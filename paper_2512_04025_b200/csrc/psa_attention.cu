@@ -533,7 +533,7 @@ PSA_DEV void regs_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"
 template <uint32_t N>
 PSA_DEV void regs_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N)); }
 
-template <int D>
+template <int D, int POLY_FROM = kPPPolyFrom>
 __global__ void __launch_bounds__(kPPThreads, 1)
     psa_attn_pp_kernel(const __grid_constant__ AttnMaps maps, const AttnParams p,
                        const uint16_t* __restrict__ csr, const int32_t* __restrict__ info,
@@ -807,7 +807,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       for (int e = 0; e < 128; e += 4) {
         float2 a = fadd2(make_float2(y[e], y[e + 1]), negm);
         float2 c = fadd2(make_float2(y[e + 2], y[e + 3]), negm);
-        if (e >= kPPPolyFrom) {
+        if (e >= POLY_FROM) {
           a = ex2_poly2(a);
           c = ex2_poly2(c);
         } else {
@@ -854,6 +854,439 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     named_bar_sync(1, 2 * kTileRows);
     const float m0 = sm.red_m[0][row], m1 = sm.red_m[1][row];
     const float l0 = sm.red_l[0][row], l1 = sm.red_l[1][row];
+    const float m = fmaxf(m0, m1);
+    const float a0 = (cnt0 > 0 && m0 != -INFINITY) ? ex2_approx(m0 - m) : 0.f;
+    const float a1 = (cnt1 > 0 && m1 != -INFINITY) ? ex2_approx(m1 - m) : 0.f;
+    const float l_tot = l0 * a0 + l1 * a1;
+    if (cnt0 > 0) mbar_wait(&sm.o_done[0], (cnt0 - 1) & 1);
+    if (cnt1 > 0) mbar_wait(&sm.o_done[1], (cnt1 - 1) & 1);
+    tc_fence_after();
+    const bool valid = row < p.b_q;
+    const bool alive = l_tot > 0.f;
+    const float inv = alive ? 1.f / l_tot : 0.f;
+    const float w0 = a0 * inv, w1 = a1 * inv;
+    constexpr int OC = D / 2;  // output columns per lane
+    uint16_t* orow = out + (q_row0 + row) * D + L * OC;
+#pragma unroll
+    for (int c4 = 0; c4 < OC / 32; ++c4) {
+      uint32_t o0[32], o1[32];
+      const uint32_t col = L * OC + c4 * 32;
+      if (cnt0 > 0) {
+        tmem_ld32(t_lane + kO0 + col, o0);
+        tmem_ld_wait(o0);
+      }
+      if (cnt1 > 0) {
+        tmem_ld32(t_lane + kO0 + D + col, o1);
+        tmem_ld_wait(o1);
+      }
+      uint32_t pkd[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        float v0 = 0.f, v1 = 0.f;
+        if (cnt0 > 0) {
+          v0 = __uint_as_float(o0[2 * e]) * w0;
+          v1 = __uint_as_float(o0[2 * e + 1]) * w0;
+        }
+        if (cnt1 > 0) {
+          v0 = fmaf(__uint_as_float(o1[2 * e]), w1, v0);
+          v1 = fmaf(__uint_as_float(o1[2 * e + 1]), w1, v1);
+        }
+        pkd[e] = pack_bf16x2(v0, v1);
+      }
+      if (valid) {
+#pragma unroll
+        for (int v4 = 0; v4 < 4; ++v4)
+          *reinterpret_cast<uint4*>(orow + c4 * 32 + v4 * 8) =
+              make_uint4(pkd[v4 * 4], pkd[v4 * 4 + 1], pkd[v4 * 4 + 2], pkd[v4 * 4 + 3]);
+      }
+    }
+    if (L == 0) {
+      if (valid) lse[q_row0 + row] = alive ? (m + log2f(l_tot)) * 0.69314718055994530942f : -INFINITY;
+      const unsigned dead = __ballot_sync(0xffffffffu, valid && !alive);
+      if (lane == 0 && dead) atomicAdd(skipped, __popc(dead));
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ====================================================================== ping-pong, P in SMEM
+// psa_attn_pp_kernel with P written to shared memory instead of back into the lane's S columns:
+// a lane releases S right after tcgen05.ld, so the tensor core computes the lane's NEXT S(t+2)
+// while its softmax of tile t is still running (the TMEM-P variant must wait for PV(t) before
+// S(t+2) can overwrite P). PV reads P with a shared-memory descriptor (K-major, 128B swizzle).
+// SMEM at D=128: Q 32K + K 2x32K + V 2x32K + P 2x32K. The lanes' final (max, sum) exchange
+// reuses their P buffers.
+template <int D>
+struct PP2Cfg {
+  static constexpr int kKStages = D == 128 ? 2 : 3;
+  static constexpr int kVStages = D == 128 ? 2 : 3;
+  static constexpr int kTileBytes = kTileRows * D * 2;
+};
+
+template <int D>
+struct PP2Smem {
+  using C = PP2Cfg<D>;
+  uint8_t q[kTileRows * D * 2];
+  uint8_t k[C::kKStages][C::kTileBytes];
+  uint8_t v[C::kVStages][C::kTileBytes];
+  uint8_t p[2][kTileRows * kTileRows * 2];
+  float bias[kMetaRing][kTileRows];
+  uint32_t meta[kMetaRing][kChunks];
+  uint64_t q_full;
+  uint64_t k_full[C::kKStages], k_empty[C::kKStages];
+  uint64_t v_full[C::kVStages], v_empty[C::kVStages];
+  uint64_t meta_full[kMetaRing], meta_empty[kMetaRing];
+  uint64_t s_full[2], s_free[2], p_full[2], o_done[2];
+  uint32_t tmem_base;
+};
+
+template <int D, int POLY_FROM = kPPPolyFrom>
+__global__ void __launch_bounds__(kPPThreads, 1)
+    psa_attn_pp2_kernel(const __grid_constant__ AttnMaps maps, const AttnParams p,
+                       const uint16_t* __restrict__ csr, const int32_t* __restrict__ info,
+                       uint16_t* __restrict__ out, float* __restrict__ lse,
+                       int32_t* __restrict__ skipped) {
+  using C = PP2Cfg<D>;
+  constexpr int KST = C::kKStages, VST = C::kVStages;
+  constexpr uint32_t kO0 = 256;  // O_L at kO0 + L * D
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  auto& sm = *reinterpret_cast<PP2Smem<D>*>(smem_raw);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t unit = blockIdx.x;
+  const int bhq = static_cast<int>(unit / p.n_q);
+  const int i = static_cast<int>(unit % p.n_q);
+  const int b = bhq / p.hq, hh = bhq % p.hq;
+  const int64_t bhkv = static_cast<int64_t>(b) * p.hkv + hh / (p.hq / p.hkv);
+  const int n_ent = info[unit * 2 + 0];
+  const int T = info[unit * 2 + 1];
+  const int64_t q_row0 = static_cast<int64_t>(bhq) * p.n + static_cast<int64_t>(i) * p.b_q;
+
+  if (threadIdx.x == 0) {
+    if (smem_u32(smem_raw) & 1023u) __trap();
+    mbar_init(&sm.q_full, 1);
+    for (int s = 0; s < KST; ++s) {
+      mbar_init(&sm.k_full[s], 1);
+      mbar_init(&sm.k_empty[s], 1);
+    }
+    for (int s = 0; s < VST; ++s) {
+      mbar_init(&sm.v_full[s], 1);
+      mbar_init(&sm.v_empty[s], 1);
+    }
+    for (int s = 0; s < kMetaRing; ++s) {
+      mbar_init(&sm.meta_full[s], 1);
+      mbar_init(&sm.meta_empty[s], kTileRows);  // one lane (128 threads) consumes a tile
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&sm.s_full[s], 1);
+      mbar_init(&sm.s_free[s], 4);  // one arrive per warp of the lane
+      mbar_init(&sm.p_full[s], 4);
+      mbar_init(&sm.o_done[s], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&maps.q);
+    for (int h = 0; h < p.levels; ++h) {
+      tma_prefetch_desc(&maps.k[h]);
+      tma_prefetch_desc(&maps.v[h]);
+    }
+  }
+  if (warp == 2) {
+    tmem_alloc(&sm.tmem_base, 512);
+    tmem_relinquish();
+  }
+  {  // K/V rows past the last filled slot of a tile are read by the MMA: keep them finite
+    uint4* z = reinterpret_cast<uint4*>(&sm.k[0][0]);
+    const int nvec = (KST + VST) * C::kTileBytes / 16;
+    for (int t = threadIdx.x; t < nvec; t += kPPThreads) z[t] = make_uint4(0, 0, 0, 0);  // K, V
+    fence_proxy_async_smem();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp < 4) {
+    regs_dec<64>();
+    if (warp == 0) {
+      // ============================================================ K producer (+ Q)
+      if (T > 0) {
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&sm.q_full, kTileRows * D * 2);
+          for (int c = 0; c < D / 64; ++c)
+            tma_load_2d(&maps.q, &sm.q_full, sm.q + c * kTileRows * 128, c * 64,
+                        static_cast<int>(q_row0));
+        }
+        PlanCursor pc;
+        pc.init(csr + unit * p.n_k, n_ent, lane);
+        for (int t = 0; t < T; ++t) {
+          const int ks = t % KST;
+          const TileSeg sg = pc.next(p, bhkv, lane);
+          if (t >= KST) mbar_wait(&sm.k_empty[ks], ((t / KST) - 1) & 1);
+          if (lane == 0) mbar_arrive_expect_tx(&sm.k_full[ks], static_cast<uint32_t>(sg.total) * D * 2);
+          __syncwarp();
+          if (sg.fits)
+            for (int c = 0; c < D / 64; ++c)
+              tma_load_2d(&maps.k[sg.h - 1], &sm.k_full[ks],
+                          sm.k[ks] + c * kTileRows * 128 + sg.off * 128, c * 64, sg.row);
+        }
+      }
+    } else if (warp == 3) {
+      // ============================================================ V producer
+      if (T > 0) {
+        PlanCursor pc;
+        pc.init(csr + unit * p.n_k, n_ent, lane);
+        for (int t = 0; t < T; ++t) {
+          const int vs = t % VST;
+          const TileSeg sg = pc.next(p, bhkv, lane);
+          if (t >= VST) mbar_wait(&sm.v_empty[vs], ((t / VST) - 1) & 1);
+          if (lane == 0) mbar_arrive_expect_tx(&sm.v_full[vs], static_cast<uint32_t>(sg.total) * D * 2);
+          __syncwarp();
+          if (sg.fits)
+            for (int c = 0; c < D / 64; ++c)
+              tma_load_2d(&maps.v[sg.h - 1], &sm.v_full[vs],
+                          sm.v[vs] + c * kTileRows * 128 + sg.off * 128, c * 64, sg.row);
+        }
+      }
+    } else if (warp == 2) {
+      // ============================================================ bias/meta producer
+      if (T > 0) {
+        const int64_t q_lo = static_cast<int64_t>(i) * p.b_q;
+        PlanCursor pc;
+        pc.init(csr + unit * p.n_k, n_ent, lane);
+        for (int t = 0; t < T; ++t) {
+          const int ms = t % kMetaRing;
+          const TileSeg sg = pc.next(p, bhkv, lane);
+          if (t >= kMetaRing) mbar_wait(&sm.meta_empty[ms], ((t / kMetaRing) - 1) & 1);
+          {
+            int g = 0;
+            for (int q = 1; q < sg.nseg; ++q)
+              if (__shfl_sync(0xffffffffu, sg.off, q) <= 4 * lane) g = q;
+            const int goff = __shfl_sync(0xffffffffu, sg.off, g);
+            const int gL = __shfl_sync(0xffffffffu, sg.L, g);
+            const int gh = __shfl_sync(0xffffffffu, sg.h, g);
+            const int r0 = 4 * lane - goff;
+            const float bv = static_cast<float>(gh - 1);
+            float4 w = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+            if (4 * lane < sg.total) {
+              w.x = r0 + 0 < gL ? bv : -INFINITY;
+              w.y = r0 + 1 < gL ? bv : -INFINITY;
+              w.z = r0 + 2 < gL ? bv : -INFINITY;
+              w.w = r0 + 3 < gL ? bv : -INFINITY;
+            }
+            *reinterpret_cast<float4*>(&sm.bias[ms][4 * lane]) = w;
+          }
+          if (p.causal && sg.fits) {
+            const bool straddle = static_cast<int64_t>(sg.j + 1) * p.b_k - 1 > q_lo;
+            for (int c = 0; c < sg.sz / 8; ++c)
+              sm.meta[ms][sg.off / 8 + c] =
+                  (straddle ? 1u : 0u) | (static_cast<uint32_t>(sg.j * p.b_k + c * 8) << 1);
+          }
+          if (p.causal && lane < kChunks && 8 * lane >= sg.total) sm.meta[ms][lane] = 0u;
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.meta_full[ms]);
+        }
+      }
+    } else {
+      // ============================================================ MMA issuer (warp 1)
+      if (T > 0) {
+        constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128, false, false);
+        constexpr uint32_t idesc_o = umma_idesc_bf16(128, D, false, true);
+        const uint64_t q_desc0 = umma_desc_sw128(smem_u32(sm.q), 16, 1024);
+        auto issue_s = [&](int t) {
+          const int ks = t % KST, L = t & 1;
+          mbar_wait(&sm.k_full[ks], (t / KST) & 1);
+          if (t >= 2) mbar_wait(&sm.s_free[L], ((t >> 1) - 1) & 1);  // lane read S(t-2)
+          tc_fence_after();
+          const uint64_t k_desc0 = umma_desc_sw128(smem_u32(sm.k[ks]), 16, 1024);
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk) {
+              const uint32_t koff = ((kk >> 2) * kTileRows * 128 + (kk & 3) * 32) >> 4;
+              mma_bf16_ss(tmem + L * 128, q_desc0 + koff, k_desc0 + koff, idesc_s,
+                          kk > 0 ? 1u : 0u);
+            }
+            mma_commit(&sm.k_empty[ks]);
+            mma_commit(&sm.s_full[L]);
+          }
+          __syncwarp();
+        };
+        auto issue_pv = [&](int t) {
+          const int vs = t % VST, L = t & 1;
+          mbar_wait(&sm.v_full[vs], (t / VST) & 1);
+          mbar_wait(&sm.p_full[L], (t >> 1) & 1);
+          tc_fence_after();
+          const uint64_t v_desc0 = umma_desc_sw128(smem_u32(sm.v[vs]), kTileRows * 128, 1024);
+          const uint64_t p_desc0 = umma_desc_sw128(smem_u32(sm.p[L]), 16, 1024);
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < kTileRows / 16; ++kk) {
+              const uint32_t poff = ((kk >> 2) * kTileRows * 128 + (kk & 3) * 32) >> 4;
+              mma_bf16_ss(tmem + kO0 + L * D, p_desc0 + poff, v_desc0 + ((kk * 16 * 128) >> 4),
+                          idesc_o, (t >= 2 || kk > 0) ? 1u : 0u);
+            }
+            mma_commit(&sm.v_empty[vs]);
+            mma_commit(&sm.o_done[L]);
+          }
+          __syncwarp();
+        };
+        mbar_wait(&sm.q_full, 0);
+        tc_fence_after();
+        issue_s(0);
+        if (T > 1) issue_s(1);
+        for (int t = 0; t < T; ++t) {
+          if (t + 2 < T) issue_s(t + 2);  // as soon as lane (t&1) has read S(t)
+          issue_pv(t);
+        }
+      }
+    }
+  } else {
+    regs_inc<216>();
+    // ============================================================== softmax lanes
+    const int L = (warp - 4) >> 2;  // lane L takes KV tiles t = L, L + 2, ...
+    const int wq = warp & 3;
+    const int row = wq * 32 + lane;
+    const uint32_t t_lane = tmem + (static_cast<uint32_t>(wq * 32) << 16);
+    const uint32_t t_s = t_lane + L * 128;
+    const int qpos = i * p.b_q + row;
+    const float2 scale2 = make_float2(p.scale_log2, p.scale_log2);
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int t = L; t < T; t += 2) {
+      const int ms = t % kMetaRing;
+      mbar_wait(&sm.s_full[L], (t >> 1) & 1);
+      tc_fence_after();
+      uint32_t s[4][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld32(t_s + c * 32, s[c]);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld_wait(s[c]);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.s_free[L]);  // S_L may take tile t+2 now
+      // y = s * scale + bias_col (bias: level-1 in log2 units; -inf on pad columns)
+      mbar_wait(&sm.meta_full[ms], (t / kMetaRing) & 1);
+      float y[128];
+      const float4* bias4 = reinterpret_cast<const float4*>(&sm.bias[ms][0]);
+#pragma unroll
+      for (int q4 = 0; q4 < 32; ++q4) {
+        const float4 bv = bias4[q4];
+        const float* x = reinterpret_cast<const float*>(&s[q4 >> 3][(q4 & 7) * 4]);
+        const float2 a = ffma2(make_float2(x[0], x[1]), scale2, make_float2(bv.x, bv.y));
+        const float2 c = ffma2(make_float2(x[2], x[3]), scale2, make_float2(bv.z, bv.w));
+        y[q4 * 4 + 0] = a.x;
+        y[q4 * 4 + 1] = a.y;
+        y[q4 * 4 + 2] = c.x;
+        y[q4 * 4 + 3] = c.y;
+      }
+      if (p.causal) {  // token-level mask on straddling level-1 chunks (attention.py:88-108)
+#pragma unroll
+        for (int c = 0; c < kChunks; ++c) {
+          const uint32_t w = sm.meta[ms][c];
+          if (w & 1u) {
+            const int lim = qpos - static_cast<int>(w >> 1);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) y[c * 8 + e] = (e <= lim) ? y[c * 8 + e] : -INFINITY;
+          }
+        }
+      }
+      mbar_arrive(&sm.meta_empty[ms]);
+
+      float mx[4] = {fmax3(y[0], y[1], y[2]), fmax3(y[3], y[4], y[5]), fmax3(y[6], y[7], y[8]),
+                     fmax3(y[9], y[10], y[11])};
+#pragma unroll
+      for (int e = 12; e < 124; e += 8) {
+        mx[0] = fmax3(mx[0], y[e], y[e + 1]);
+        mx[1] = fmax3(mx[1], y[e + 2], y[e + 3]);
+        mx[2] = fmax3(mx[2], y[e + 4], y[e + 5]);
+        mx[3] = fmax3(mx[3], y[e + 6], y[e + 7]);
+      }
+      mx[0] = fmax3(mx[0], y[124], y[125]);
+      mx[1] = fmax3(mx[1], y[126], y[127]);
+      const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+      const float m_new = fmaxf(m_run, mt);
+      const bool resc = m_new > m_run + kRescaleThreshold;
+      float alpha = 1.f;
+      if (resc) {
+        alpha = ex2_approx(m_run - m_new);
+        m_run = m_new;
+      }
+      const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
+      const float2 negm = make_float2(-m_use, -m_use);
+      float2 ls0 = make_float2(0.f, 0.f), ls1 = make_float2(0.f, 0.f);
+      uint32_t pk[64];
+#pragma unroll
+      for (int e = 0; e < 128; e += 4) {
+        float2 a = fadd2(make_float2(y[e], y[e + 1]), negm);
+        float2 c = fadd2(make_float2(y[e + 2], y[e + 3]), negm);
+        if (e >= POLY_FROM) {
+          a = ex2_poly2(a);
+          c = ex2_poly2(c);
+        } else {
+          a.x = ex2_approx(a.x);
+          a.y = ex2_approx(a.y);
+          c.x = ex2_approx(c.x);
+          c.y = ex2_approx(c.y);
+        }
+        ls0 = fadd2(ls0, a);
+        ls1 = fadd2(ls1, c);
+        pk[e / 2] = pack_bf16x2(a.x, a.y);
+        pk[e / 2 + 1] = pack_bf16x2(c.x, c.y);
+      }
+      const float2 ls = fadd2(ls0, ls1);
+      l_run = l_run * alpha + (ls.x + ls.y);
+      // PV(t-2) done: P_L is free and O_L is stable
+      if (t >= 2) {
+        mbar_wait(&sm.o_done[L], ((t >> 1) - 1) & 1);
+        tc_fence_after();
+      }
+      if (t >= 2 && __any_sync(0xffffffffu, resc)) {
+#pragma unroll
+        for (int c4 = 0; c4 < D / 32; ++c4) {
+          uint32_t o[32];
+          tmem_ld32(t_lane + kO0 + L * D + c4 * 32, o);
+          tmem_ld_wait(o);
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+          tmem_st32(t_lane + kO0 + L * D + c4 * 32, o);
+        }
+      }
+      {  // P (bf16) -> shared memory, UMMA K-major 128B-swizzled: [key half][row][128 B]
+        uint8_t* prow = sm.p[L] + row * 128;
+        const int sw = row & 7;
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int ch = 0; ch < 8; ++ch)
+            *reinterpret_cast<uint4*>(prow + c * kTileRows * 128 + ((ch ^ sw) << 4)) =
+                make_uint4(pk[c * 32 + ch * 4], pk[c * 32 + ch * 4 + 1], pk[c * 32 + ch * 4 + 2],
+                           pk[c * 32 + ch * 4 + 3]);
+      }
+      tmem_st_wait();  // O rescale stores
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.p_full[L]);
+    }
+
+    // ---------------------------------------------------------------- merge + epilogue
+    const int cnt0 = (T + 1) >> 1, cnt1 = T >> 1;  // tiles of lane 0 / lane 1
+    const int cnt_me = L == 0 ? cnt0 : cnt1;
+    if (cnt_me > 0) mbar_wait(&sm.o_done[L], (cnt_me - 1) & 1);  // P_L no longer read
+    float* red = reinterpret_cast<float*>(sm.p[L]);
+    red[row] = m_run;
+    red[kTileRows + row] = l_run;
+    named_bar_sync(1, 2 * kTileRows);
+    const float* red0 = reinterpret_cast<const float*>(sm.p[0]);
+    const float* red1 = reinterpret_cast<const float*>(sm.p[1]);
+    const float m0 = red0[row], m1 = red1[row];
+    const float l0 = red0[kTileRows + row], l1 = red1[kTileRows + row];
     const float m = fmaxf(m0, m1);
     const float a0 = (cnt0 > 0 && m0 != -INFINITY) ? ex2_approx(m0 - m) : 0.f;
     const float a1 = (cnt1 > 0 && m1 != -INFINITY) ? ex2_approx(m1 - m) : 0.f;
@@ -993,10 +1426,30 @@ static int launch_attn(const void* q, const void* k, const void* v, const void* 
         maps, p, csr, info, static_cast<uint16_t*>(out), lse, skipped);
     return psa_check_launch("psa_attn_fwd_kernel");
   }
+  static const bool use_pp1 = [] {
+    const char* e = getenv("PSA_ATTN_KERNEL");
+    return e != nullptr && strcmp(e, "pp") == 0;
+  }();
+  if (!use_pp1) {
+    const size_t smem2 = sizeof(PP2Smem<D>);
+    auto kern2 = psa_attn_pp2_kernel<D>;
+    cudaFuncSetAttribute(kern2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem2));
+    kern2<<<static_cast<unsigned>(units), kPPThreads, smem2, s>>>(
+        maps, p, csr, info, static_cast<uint16_t*>(out), lse, skipped);
+    return psa_check_launch("psa_attn_pp2_kernel");
+  }
   const size_t smem = sizeof(PPSmem<D>);
-  cudaFuncSetAttribute(psa_attn_pp_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       static_cast<int>(smem));
-  psa_attn_pp_kernel<D><<<static_cast<unsigned>(units), kPPThreads, smem, s>>>(
+  static const int poly = [] {  // experiment knob: first softmax column on the FMA-pipe exp2
+    const char* e = getenv("PSA_PP_POLY");
+    return e != nullptr ? atoi(e) : kPPPolyFrom;
+  }();
+  auto kern = poly >= 128 ? psa_attn_pp_kernel<D, 128>
+            : poly >= 112 ? psa_attn_pp_kernel<D, 112>
+            : poly >= 96 ? psa_attn_pp_kernel<D, 96>
+            : poly >= 80 ? psa_attn_pp_kernel<D, 80> : psa_attn_pp_kernel<D, 64>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  kern<<<static_cast<unsigned>(units), kPPThreads, smem, s>>>(
       maps, p, csr, info, static_cast<uint16_t*>(out), lse, skipped);
   return psa_check_launch("psa_attn_pp_kernel");
 }
