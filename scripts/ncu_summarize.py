@@ -93,7 +93,7 @@ def main(tag: str) -> None:
                         "dram_gbs": ((rd or 0) + (wr or 0)) / t / 1e9 if t else None}
         (PROF / f"{tag}_{name}_ncu.json").write_text(json.dumps(m, indent=1) + "\n")
         print(name, m["summary"])
-        if name in ("attn", "psa_attn_fwd"):
+        if name.startswith("psa_attn") or name == "attn":
             cfg = sys.argv[2] if len(sys.argv) > 2 else "cfg3"
             (PROF / f"attention_ncu_summary_{cfg}.json").write_text(json.dumps(
                 {"source": f"profiles/{tag}_{name}_ncu.json", "kernel": m.get("kernel"),
