@@ -29,7 +29,7 @@ struct LevelRule {  // thresholds (mode 0) or quantile rank counts (mode 1)
 // Exact int8-sliced importance logits (psa_xlogits.cu).
 struct XlGeometry {
   bool ok;
-  int per, bpt, n_tiles, kp, rq_pad, classes;
+  int per, bpt, n_halves, n_tiles, kp, rq_pad, classes;  // bpt: KV blocks per 16-key half
   size_t off_ks, off_qm, off_km, off_flags, bytes;
 };
 XlGeometry xl_geometry(int64_t bhq, int64_t bkv, int n_q, int n_k, int classes, int rows_per_class,

@@ -43,8 +43,10 @@ constexpr int kXlKeys = 32;       // MMA N = keys per tile
 constexpr int kXlStages = 4;
 constexpr int kXlAccBufs = 2;
 constexpr int kXlMaxTiny = 4;
-constexpr int kXlThreads = 384;
-constexpr int kXlEpiThreads = 256;
+constexpr int kXlHalf = 16;         // keys per epilogue group and tile (half an MMA tile)
+constexpr int kXlGroups = 4;        // epilogue warpgroups: (accumulator buffer, half) pairs
+constexpr int kXlEpiThreads = kXlGroups * 128;
+constexpr int kXlThreads = 128 + kXlEpiThreads;
 constexpr int kXlGridShift = 27;  // X = x * 2^(27 - E), |X| < 2^28
 
 struct XlMeta {
@@ -185,7 +187,7 @@ enum XlMode { kXlMax = 0, kXlAntidiag = 1 };
 struct XlParams {
   int64_t n;
   int hq, hkv, classes, stride, b_q, b_k, n_q, n_k;
-  int r_total, rq_pad, kp, n_tiles, per, bpt;
+  int r_total, rq_pad, kp, n_tiles, n_chunks, per, bpt;  // bpt: KV blocks per 16-key half
   double sqrt_d, inv_sqrt_d, scale;
   const uint16_t* q;
   const uint16_t* k;
@@ -210,9 +212,9 @@ template <int D>
 struct XlSmem {
   uint8_t q[kXlSlices][kXlQRows * kXlRowBytes];
   uint8_t k[kXlStages][kXlSlices][kXlKeys * kXlRowBytes];
-  double ex[kXlKeys][kXlEpiThreads];  // per-thread logits / exp terms of one tile
+  double ex[kXlHalf][kXlEpiThreads];  // per-thread logits / exp terms of one half tile
   double exp_tab[64];                 // 2^(j/64)
-  double red_m[kXlQRows], red_l[kXlQRows], red_x[kXlQRows];
+  double red_m[kXlGroups][kXlQRows], red_l[kXlGroups][kXlQRows], red_x[kXlGroups][kXlQRows];
   uint64_t q_full;
   uint64_t k_full[kXlStages], k_empty[kXlStages];
   uint64_t acc_full[kXlAccBufs], acc_empty[kXlAccBufs];
@@ -367,7 +369,7 @@ __global__ void __launch_bounds__(kXlThreads, 1)
     }
     for (int s = 0; s < kXlAccBufs; ++s) {
       mbar_init(&sm.acc_full[s], 1);
-      mbar_init(&sm.acc_empty[s], kXlEpiThreads / 2);
+      mbar_init(&sm.acc_empty[s], 2 * 128);  // the two half-tile groups of the buffer
     }
     fence_barrier_init();
   }
@@ -430,8 +432,12 @@ __global__ void __launch_bounds__(kXlThreads, 1)
       __syncwarp();
     }
   } else if (warp >= 4) {
+    // ---- epilogue: group g takes accumulator buffer g >> 1 (tiles t = g >> 1 mod 2) and
+    // the 16-key half (g & 1) of each of those tiles; half index hx = 2 t + half holds the
+    // whole KV blocks [hx * bpt, hx * bpt + bpt) (keys packed 16 per half by the slicer)
     const int e_tid = threadIdx.x - 128;
     const int grp = (warp - 4) >> 2;
+    const int buf = grp >> 1, half = grp & 1;
     const int wq = warp & 3;
     const int row = wq * 32 + lane;
     const int a = qt * kXlQRows + row;  // gathered query row of this class
@@ -444,26 +450,28 @@ __global__ void __launch_bounds__(kXlThreads, 1)
     const XlMeta* kmeta = p.kmeta + static_cast<int64_t>(bkv * p.classes + kcls) * p.kp;
     const uint16_t* kbase = p.k + static_cast<int64_t>(bkv) * p.n * D;
     const uint32_t t_acc = tmem + (static_cast<uint32_t>(wq * 32) << 16) +
-                           grp * (kXlClasses * kXlKeys);
-    const int cw = p.bpt * p.per;
+                           buf * (kXlClasses * kXlKeys) + half * kXlHalf;
+    const int cw = p.bpt * p.per;  // valid keys of a half
     const int64_t out_row = MODE == kXlMax ? static_cast<int64_t>(bhq) * rows_valid + a
                                            : static_cast<int64_t>(bhq) * p.n + qsrc;
     double* out_blocks = p.M + out_row * p.n_k;
     double m_run = -INFINITY, l_run = 0.0;
     double rmax = -INFINITY;  // MAX mode: exact running max of the raw dot products
+    double* xs = &sm.ex[0][e_tid];  // this thread's column: 16 values, stride kXlEpiThreads
 
-    for (int t = grp; t < T; t += 2) {
-      const int j0 = t * p.bpt;  // first KV block of the tile
-      const int nb = min(p.bpt, p.n_k - j0);
+    for (int t = buf; t < T; t += 2) {
+      const int hx = 2 * t + half;
+      const int j0 = hx * p.bpt;  // first KV block of the half
+      const int nb = max(0, min(p.bpt, p.n_k - j0));
       const int nvalid = nb * p.per;
-      const uint32_t valid_mask = nvalid >= 32 ? 0xffffffffu : ((1u << nvalid) - 1u);
-      const XlMeta kml = kmeta[t * kXlKeys + lane];  // lane j: key j's exponent / tiny count
+      const uint32_t valid_mask = (1u << nvalid) - 1u;
+      const XlMeta kml = kmeta[t * kXlKeys + half * kXlHalf + (lane & (kXlHalf - 1))];
       const int kinfo = (kml.e << 1) | ((kml.tiny >> 28) != 0u ? 1 : 0);
-      mbar_wait(&sm.acc_full[grp], (t >> 1) & 1);
+      mbar_wait(&sm.acc_full[buf], (t >> 1) & 1);
       tc_fence_after();
-      double dv[kXlKeys];
+      double dv[kXlHalf];
 #pragma unroll
-      for (int c8 = 0; c8 < kXlKeys / 8; ++c8) {
+      for (int c8 = 0; c8 < kXlHalf / 8; ++c8) {
         uint32_t cv[kXlClasses][8];
 #pragma unroll
         for (int c = 0; c < kXlClasses; ++c) tmem_ld8(t_acc + c * kXlKeys + c8 * 8, cv[c]);
@@ -482,9 +490,10 @@ __global__ void __launch_bounds__(kXlThreads, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&sm.acc_empty[grp]);
+      mbar_arrive(&sm.acc_empty[buf]);
+      if (nb == 0) continue;  // odd half count: this half of the last tile holds no block
 #pragma unroll
-      for (int j = 0; j < kXlKeys; ++j) {
+      for (int j = 0; j < kXlHalf; ++j) {
         const int kj = __shfl_sync(0xffffffffu, kinfo, j);
         dv[j] = __dmul_rn(dv[j], pow2((kj >> 1) + qm.e - 2 * kXlGridShift));
       }
@@ -494,23 +503,22 @@ __global__ void __launch_bounds__(kXlThreads, 1)
 #pragma unroll 1
         for (int j = 0; j < nvalid; ++j)
           if (row_ok && (q_tiny || ((key_tiny >> j) & 1u))) {
-            const XlMeta kmj = kmeta[t * kXlKeys + j];
-            const double c = tiny_correction(qrow_ptr, kbase + krows(t * cw + j) * D, qm, kmj);
-            sm.ex[j][e_tid] = c;  // staged: dv[] needs static indices
+            const XlMeta kmj = kmeta[t * kXlKeys + half * kXlHalf + j];
+            const double c = tiny_correction(qrow_ptr, kbase + krows(hx * cw + j) * D, qm, kmj);
+            xs[j * kXlEpiThreads] = c;  // staged: dv[] needs static indices
           }
 #pragma unroll
-        for (int j = 0; j < kXlKeys; ++j)
+        for (int j = 0; j < kXlHalf; ++j)
           if (row_ok && (q_tiny || ((key_tiny >> j) & 1u)) && j < nvalid)
-            dv[j] = __dadd_rn(dv[j], sm.ex[j][e_tid]);
+            dv[j] = __dadd_rn(dv[j], xs[j * kXlEpiThreads]);
       }
-      double* xs = &sm.ex[0][e_tid];  // this thread's column: 32 values, stride kXlEpiThreads
 
       constexpr int kP = PER > 0 ? PER : 1;
       if (PER > 0) {
-        // ---- static block structure: blocks are PER consecutive keys of the tile
-        constexpr int kB = kXlKeys / kP;
-        double bx[kB];
+        // ---- static block structure: blocks are PER consecutive keys of the half
+        constexpr int kB = kXlHalf / kP;
         if (MODE == kXlMax) {
+          double hmax = -INFINITY;
 #pragma unroll
           for (int bb = 0; bb < kB; ++bb) {  // raw block maxima (tree)
             double v[kP];
@@ -520,29 +528,28 @@ __global__ void __launch_bounds__(kXlThreads, 1)
             for (int w = 1; w < kP; w <<= 1)
 #pragma unroll
               for (int u = 0; u + w < kP; u += 2 * w) v[u] = fmax(v[u], v[u + w]);
-            bx[bb] = bb < nb ? v[0] : -INFINITY;
-            if (row_ok && bb < nb) out_blocks[j0 + bb] = v[0];
+            if (bb < nb) {
+              hmax = fmax(hmax, v[0]);
+              if (row_ok) out_blocks[j0 + bb] = v[0];
+            }
           }
-          double tmax = bx[0];
-#pragma unroll
-          for (int bb = 1; bb < kB; ++bb) tmax = fmax(tmax, bx[bb]);
-          rmax = fmax(rmax, tmax);
+          rmax = fmax(rmax, hmax);
           // exps use an offset within an ulp of the running max logit (no division on the
           // critical path); the exact max fl(max / sqrt(d)) is applied once per row at the end
-          const double m_new = fmax(m_run, __dmul_rn(tmax, p.inv_sqrt_d));
+          const double m_new = fmax(m_run, __dmul_rn(hmax, p.inv_sqrt_d));
           double ps[4] = {0.0, 0.0, 0.0, 0.0};
           int slow = 0;
 #pragma unroll
-          for (int j = 0; j < kXlKeys; ++j) {
+          for (int j = 0; j < kXlHalf; ++j) {
             const bool ok = (valid_mask >> j) & 1u;
             const double e = exp_nonpos(ok ? __fma_rn(dv[j], p.inv_sqrt_d, -m_new) : 0.0,
                                         sm.exp_tab, &slow);
             ps[j & 3] = __dadd_rn(ps[j & 3], ok ? e : 0.0);
           }
-          if (slow) {  // some term below e^-708: redo this tile's sum with exact subnormals
+          if (slow) {  // some term below e^-708: redo this half's sum with exact subnormals
             ps[0] = ps[1] = ps[2] = ps[3] = 0.0;
 #pragma unroll
-            for (int j = 0; j < kXlKeys; ++j)
+            for (int j = 0; j < kXlHalf; ++j)
               if ((valid_mask >> j) & 1u)
                 ps[j & 3] = __dadd_rn(ps[j & 3], exp_nonpos_slow(__fma_rn(dv[j], p.inv_sqrt_d, -m_new),
                                                                  sm.exp_tab));
@@ -553,16 +560,8 @@ __global__ void __launch_bounds__(kXlThreads, 1)
         } else {
           double cmax = -INFINITY;
 #pragma unroll
-          for (int bb = 0; bb < kB; ++bb) {
-            double v[kP];
-#pragma unroll
-            for (int u = 0; u < kP; ++u) v[u] = dv[bb * kP + u];
-#pragma unroll
-            for (int w = 1; w < kP; w <<= 1)
-#pragma unroll
-              for (int u = 0; u + w < kP; u += 2 * w) v[u] = fmax(v[u], v[u + w]);
-            cmax = fmax(cmax, bb < nb ? v[0] : -INFINITY);
-          }
+          for (int j = 0; j < kXlHalf; ++j)
+            cmax = fmax(cmax, ((valid_mask >> j) & 1u) ? dv[j] : -INFINITY);
           const double m_new = fmax(m_run, __dmul_rn(cmax, p.scale));
           double part = 0.0;
 #pragma unroll
@@ -605,21 +604,20 @@ __global__ void __launch_bounds__(kXlThreads, 1)
           }
           l_run = __dadd_rn(__dmul_rn(l_run, rescale(m_run, m_new, sm.exp_tab)), part);
           m_run = m_new;
-          if (row_ok) p.Mc[out_row * p.n_tiles + t] = m_new;
+          if (row_ok) p.Mc[out_row * p.n_chunks + hx] = m_new;
         }
       } else if (MODE == kXlMax) {
-        double tmax = -INFINITY;
+        double hmax = -INFINITY;
 #pragma unroll
-        for (int j = 0; j < kXlKeys; ++j) {
+        for (int j = 0; j < kXlHalf; ++j) {
           xs[j * kXlEpiThreads] = dv[j];
-          tmax = fmax(tmax, ((valid_mask >> j) & 1u) ? dv[j] : -INFINITY);
+          hmax = fmax(hmax, ((valid_mask >> j) & 1u) ? dv[j] : -INFINITY);
         }
-        rmax = fmax(rmax, tmax);
-        const double m_new = fmax(m_run, __dmul_rn(tmax, p.inv_sqrt_d));
-        // branch-free: padding keys get an argument whose exp is exactly 0
+        rmax = fmax(rmax, hmax);
+        const double m_new = fmax(m_run, __dmul_rn(hmax, p.inv_sqrt_d));
         double ps[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-        for (int j = 0; j < kXlKeys; ++j) {
+        for (int j = 0; j < kXlHalf; ++j) {
           const double arg = __fma_rn(dv[j], p.inv_sqrt_d, -m_new);
           ps[j & 3] = __dadd_rn(ps[j & 3],
                                 exp_nonpos_slow(((valid_mask >> j) & 1u) ? arg : -2000.0, sm.exp_tab));
@@ -636,11 +634,11 @@ __global__ void __launch_bounds__(kXlThreads, 1)
       } else {
         double cmax = -INFINITY;
 #pragma unroll
-        for (int j = 0; j < kXlKeys; ++j)
+        for (int j = 0; j < kXlHalf; ++j)
           cmax = fmax(cmax, ((valid_mask >> j) & 1u) ? dv[j] : -INFINITY);
         const double m_new = fmax(m_run, __dmul_rn(cmax, p.scale));
 #pragma unroll
-        for (int j = 0; j < kXlKeys; ++j) {
+        for (int j = 0; j < kXlHalf; ++j) {
           const double arg = __dsub_rn(__dmul_rn(dv[j], p.scale), m_new);
           xs[j * kXlEpiThreads] = exp_nonpos_slow(((valid_mask >> j) & 1u) ? arg : -2000.0, sm.exp_tab);
         }
@@ -653,22 +651,28 @@ __global__ void __launch_bounds__(kXlThreads, 1)
         }
         l_run = __dadd_rn(__dmul_rn(l_run, rescale(m_run, m_new, sm.exp_tab)), part);
         m_run = m_new;
-        if (row_ok) p.Mc[out_row * p.n_tiles + t] = m_new;
+        if (row_ok) p.Mc[out_row * p.n_chunks + hx] = m_new;
       }
     }
-    // merge the two groups' running (m, l); MAX mode re-bases l on the exact max logit
-    if (grp == 1) {
-      sm.red_m[row] = m_run;
-      sm.red_l[row] = l_run;
-      sm.red_x[row] = rmax;
-    }
+    // merge the four groups' running (m, l); MAX mode re-bases l on the exact max logit
+    sm.red_m[grp][row] = m_run;
+    sm.red_l[grp][row] = l_run;
+    sm.red_x[grp][row] = rmax;
     named_bar_sync(1, kXlEpiThreads);
     if (grp == 0 && row_ok) {
-      const double m1 = sm.red_m[row], l1 = sm.red_l[row];
-      const double m = MODE == kXlMax ? __ddiv_rn(fmax(rmax, sm.red_x[row]), p.sqrt_d)  // :80
-                                      : fmax(m_run, m1);
-      const double l = __dadd_rn(__dmul_rn(l_run, exp(__dsub_rn(m_run, m))),
-                                 m1 == -INFINITY ? 0.0 : __dmul_rn(l1, exp(__dsub_rn(m1, m))));
+      double xm = -INFINITY, mm = -INFINITY;
+#pragma unroll
+      for (int g = 0; g < kXlGroups; ++g) {
+        xm = fmax(xm, sm.red_x[g][row]);
+        mm = fmax(mm, sm.red_m[g][row]);
+      }
+      const double m = MODE == kXlMax ? __ddiv_rn(xm, p.sqrt_d) : mm;  // importance.py:80
+      double l = 0.0;
+#pragma unroll
+      for (int g = 0; g < kXlGroups; ++g) {
+        const double mg = sm.red_m[g][row];
+        if (mg != -INFINITY) l = __dadd_rn(l, __dmul_rn(sm.red_l[g][row], exp(__dsub_rn(mg, m))));
+      }
       p.mstat[out_row] = m;
       p.lstat[out_row] = l;
     }
@@ -700,11 +704,12 @@ static int xl_encode(CUtensorMap* m, const void* base, uint64_t rows, uint32_t b
 XlGeometry xl_geometry(int64_t bhq, int64_t bkv, int n_q, int n_k, int classes, int rows_per_class,
                        int per) {
   XlGeometry g{};
-  g.ok = per >= 1 && per <= kXlKeys;
+  g.ok = per >= 1 && per <= kXlHalf;
   if (!g.ok) return g;
   g.per = per;
-  g.bpt = kXlKeys / per;
-  g.n_tiles = (n_k + g.bpt - 1) / g.bpt;
+  g.bpt = kXlHalf / per;  // whole KV blocks per 16-key half
+  g.n_halves = (n_k + g.bpt - 1) / g.bpt;
+  g.n_tiles = (g.n_halves + 1) / 2;
   g.kp = g.n_tiles * kXlKeys;
   g.rq_pad = (rows_per_class + kXlQRows - 1) / kXlQRows * kXlQRows;
   g.classes = classes;
@@ -742,7 +747,7 @@ static int xl_launch(const void* q, const void* k, int64_t batch, int hq, int hk
       qq, n, qr, g.classes, stride, b_q, qp, qs, qm, qflag);
   int rc = psa_check_launch("xl_slice_kernel<q>");
   if (rc) return rc;
-  XlPack kp{kXlKeys, g.bpt * g.per, k_total, g.kp};
+  XlPack kp{kXlHalf, g.bpt * g.per, k_total, g.kp};
   xl_slice_kernel<D, KR><<<dim3((g.kp + 7) / 8, bkv, g.classes), 256, 0, s>>>(
       kk, n, kr, g.classes, stride, b_k, kp, ks, km, kflag);
   rc = psa_check_launch("xl_slice_kernel<k>");
@@ -769,6 +774,7 @@ static int xl_launch(const void* q, const void* k, int64_t batch, int hq, int hk
   p.rq_pad = g.rq_pad;
   p.kp = g.kp;
   p.n_tiles = g.n_tiles;
+  p.n_chunks = g.n_halves;
   p.per = g.per;
   p.bpt = g.bpt;
   p.sqrt_d = sqrt(static_cast<double>(D));

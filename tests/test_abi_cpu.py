@@ -44,7 +44,7 @@ def test_argument_errors_map_to_validation_error():
         _lib.check(rc, "psa_pyramid_build")
     rc = lib.psa_attn_fwd(1, 1, 1, 1, 1, 1, 2, 1, 1024, 128, 256, 64, 2, 1, 1, 0, 1, 1, 1, None)
     assert rc == _lib.PSA_EINVAL and "q_block" in lib.psa_last_error().decode()
-    # s_k = 40 > 32: fp64 path only, workspace = block maxima + (m, l) per sampled row
+    # s_k = 40 > 16: fp64 path only, workspace = block maxima + (m, l) per sampled row
     assert lib.psa_importance_workspace_bytes(2, 2, 10, 8, 10, 40) == 8 * (2 * 80 * 10 + 2 * 2 * 80)
     # s_k = 8: plus the int8 slices of the exact tensor-core path
     assert lib.psa_importance_workspace_bytes(2, 2, 10, 8, 10, 8) > 8 * (2 * 80 * 10 + 2 * 2 * 80)
@@ -54,10 +54,10 @@ def test_argument_errors_map_to_validation_error():
     rc = lib.psa_importance_antidiagonal(1, 1, 1, 1, 1, 1024, 128, 64, 64, 3, 0, 1, 1, None)
     assert rc == _lib.PSA_EINVAL and "stride" in lib.psa_last_error().decode()
     assert lib.psa_antidiag_workspace_bytes(2, 2, 1024, 64, 64, 3) == 0
-    # n=1024, b_k=64, stride 2 -> per=32 (int8 path: one block per 32-key tile -> 16 chunks)
+    # n=1024, b_k=64, stride 4 -> per=16 (int8 path: one block per 16-key half -> 16 chunks)
     fp64 = 8 * 2 * 1024 * (16 + 16 + 2)
-    assert lib.psa_antidiag_workspace_bytes(2, 2, 1024, 64, 64, 2) > fp64
-    # stride 1 -> per=64 > 32: fp64 path only, 64-key chunks -> 16 chunks
+    assert lib.psa_antidiag_workspace_bytes(2, 2, 1024, 64, 64, 4) > fp64
+    # stride 1 -> per=64 > 16: fp64 path only, 64-key chunks -> 16 chunks
     assert lib.psa_antidiag_workspace_bytes(2, 2, 1024, 64, 64, 1) == fp64
 
 
