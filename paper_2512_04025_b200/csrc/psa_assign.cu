@@ -15,6 +15,8 @@
 // across a warp, then rounded half-to-even), which is what CPython's math.fsum returns; the
 // Neumaier recurrence is inherently sequential and runs on one thread with the same IEEE ops
 // in the same order, so identical scores give identical levels.
+#include <cub/block/block_radix_sort.cuh>
+
 #include "common.cuh"
 #include "psa_internal.h"
 
@@ -24,33 +26,6 @@ struct AssignParams {
   LevelRule rule;
   int n_q, n_k, hq, hkv, b_q, b_k, levels, causal, n_pad;
 };
-
-PSA_DEV bool sorts_before(double ka, int ia, double kb, int ib) {
-  return ka > kb || (ka == kb && ia < ib);
-}
-
-// Bitonic sort of (key, idx) pairs in shared memory into "descending key, ascending idx".
-PSA_DEV void bitonic_sort_desc(double* keys, int* idx, int n_pad) {
-  for (int k = 2; k <= n_pad; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int t = threadIdx.x; t < (n_pad >> 1); t += blockDim.x) {
-        const int i = 2 * j * (t / j) + (t % j);
-        const int l = i + j;
-        const double ki = keys[i], kl = keys[l];
-        const int ii = idx[i], il = idx[l];
-        const bool asc = (i & k) == 0;  // this run must end up in "sorts_before" order
-        const bool sw = asc ? sorts_before(kl, il, ki, ii) : sorts_before(ki, ii, kl, il);
-        if (sw) {
-          keys[i] = kl;
-          keys[l] = ki;
-          idx[i] = il;
-          idx[l] = ii;
-        }
-      }
-      __syncthreads();
-    }
-  }
-}
 
 // Extract `cnt` (<= 53) bits starting at bit `lo` of a 256-bit little-endian limb array.
 PSA_DEV uint64_t bits256(const uint32_t (&w)[8], int lo, int cnt) {
@@ -174,10 +149,18 @@ PSA_DEV void emit_plan_row(const int8_t* lvl, int n_k, int levels, int b_k, int6
   }
 }
 
+// Descending stable order of a row of n_k <= 128*IPT non-negative scores (numpy's stable argsort
+// of -s, mask.py:107-109): a CUB block radix sort of the fp64 bit patterns (monotone for
+// non-negative values; -0.0 is folded into +0.0 first, as the comparison-based sort treats
+// them as equal) with the column index as payload. Radix sort is stable, so equal scores keep
+// ascending column order; padding keys (0) follow every real score, zeros included.
+template <int IPT, int RB = 6>
 __global__ void __launch_bounds__(128) assign_levels_kernel(
     const double* __restrict__ S, const int8_t* __restrict__ caps, AssignParams p,
     int8_t* __restrict__ level_map, uint16_t* __restrict__ csr, int32_t* __restrict__ info,
     unsigned long long* __restrict__ level_counts) {
+  using Sort = cub::BlockRadixSort<unsigned long long, 128, IPT, int, RB>;
+  __shared__ typename Sort::TempStorage sort_tmp;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* keys = reinterpret_cast<double*>(smem_raw);
   int* idx = reinterpret_cast<int*>(keys + p.n_pad);
@@ -190,12 +173,25 @@ __global__ void __launch_bounds__(128) assign_levels_kernel(
   const int64_t bhq = blockIdx.y;
   const int64_t unit = bhq * p.n_q + i;
   const double* row = S + unit * p.n_k;
-  for (int t = threadIdx.x; t < p.n_pad; t += blockDim.x) {
-    keys[t] = t < p.n_k ? row[t] : -1.0;  // scores are >= 0: pads sort last
-    idx[t] = t;
+  {
+    unsigned long long kb[IPT];
+    int vb[IPT];
+#pragma unroll
+    for (int e = 0; e < IPT; ++e) {  // blocked arrangement: thread t holds [t*IPT, t*IPT+IPT)
+      const int t = threadIdx.x * IPT + e;
+      const double x = t < p.n_k ? row[t] : 0.0;
+      kb[e] = static_cast<unsigned long long>(__double_as_longlong(x == 0.0 ? 0.0 : x));
+      vb[e] = t;
+    }
+    Sort(sort_tmp).SortDescending(kb, vb, 0, 63);  // sign bit is 0: 63 key bits
+#pragma unroll
+    for (int e = 0; e < IPT; ++e) {
+      const int t = threadIdx.x * IPT + e;
+      keys[t] = __longlong_as_double(static_cast<long long>(kb[e]));
+      idx[t] = vb[e];
+    }
   }
   __syncthreads();
-  bitonic_sort_desc(keys, idx, p.n_pad);
 
   if (p.rule.mode == 0) {
     if (threadIdx.x < 32) {
@@ -328,16 +324,39 @@ extern "C" int psa_assign_levels(const double* scores, int64_t batch, int hq, in
   p.b_k = b_k;
   p.levels = levels;
   p.causal = causal;
-  int n_pad = 32;
-  while (n_pad < n_k) n_pad <<= 1;
+  static const int kIpt[] = {1, 2, 3, 4, 5, 6, 8, 10, 12, 16, 20, 24, 32};
+  int ipt = 32;
+  for (int v : kIpt)
+    if (128 * v >= n_k) {
+      ipt = v;
+      break;
+    }
+  const int n_pad = 128 * ipt;
   p.n_pad = n_pad;
   const size_t smem = static_cast<size_t>(n_pad) * (8 + 4 + 1) + n_k + 16;
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(assign_levels_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
   dim3 grid(n_q, static_cast<unsigned>(batch * hq));
-  assign_levels_kernel<<<grid, 128, smem, static_cast<cudaStream_t>(stream)>>>(
-      scores, caps, p, level_map, plan_csr, plan_info, level_counts);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  auto launch = [&](auto kern) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem));
+    kern<<<grid, 128, smem, st>>>(scores, caps, p, level_map, plan_csr, plan_info, level_counts);
+  };
+  switch (ipt) {
+    case 1: launch(assign_levels_kernel<1>); break;
+    case 2: launch(assign_levels_kernel<2>); break;
+    case 3: launch(assign_levels_kernel<3>); break;
+    case 4: launch(assign_levels_kernel<4>); break;
+    case 5: launch(assign_levels_kernel<5>); break;
+    case 6: launch(assign_levels_kernel<6>); break;
+    case 8: launch(assign_levels_kernel<8>); break;
+    case 10: launch(assign_levels_kernel<10>); break;
+    case 12: launch(assign_levels_kernel<12>); break;
+    case 16: launch(assign_levels_kernel<16>); break;
+    case 20: launch(assign_levels_kernel<20>); break;
+    case 24: launch(assign_levels_kernel<24>); break;
+    default: launch(assign_levels_kernel<32>); break;
+  }
   return psa_check_launch("assign_levels_kernel");
 }
 
