@@ -451,8 +451,11 @@ def run_e2e(psa, rc, q, k, v, args, stream, flops_all, world, device):
     out_h = torch.empty(q.shape, dtype=torch.bfloat16).pin_memory()
     lse_h = torch.empty(q.shape[:-1], dtype=torch.float32).pin_memory()
 
+    per_group = int(os.environ["PSA_E2E_GROUP"]) if os.environ.get("PSA_E2E_GROUP") else None
+
     def one():
-        return psa.psa_attention(hq, hk, hv, rc, device=device, out=out_h, lse=lse_h)
+        return psa.psa_attention(hq, hk, hv, rc, device=device, out=out_h, lse=lse_h,
+                                 kv_heads_per_group=per_group)
 
     for _ in range(2):
         one()
@@ -473,7 +476,18 @@ def run_e2e(psa, rc, q, k, v, args, stream, flops_all, world, device):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t[0])
+    # PCIe floor of the same step: the H2D of Q/K/V alone (pinned, one stream)
+    dq = [torch.empty_like(x, device=device) for x in (hq, hk, hv)]
+    a.record(stream)
+    for _ in range(steps):
+        for dst, src in zip(dq, (hq, hk, hv)):
+            dst.copy_(src, non_blocking=True)
+    b.record(stream)
+    torch.cuda.synchronize()
+    h2d_ms = a.elapsed_time(b) / steps
+    del dq
     return {"value": round(flops_all / (ms * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
+            "h2d_only_ms": round(h2d_ms, 3),
             "ms_per_step": round(ms, 3), "host_wall_ms_per_step": round(wall, 3), "steps": steps,
             "api": "psa_attention(pinned host q, k, v) -> host out, lse (staged H2D/compute/D2H)",
             "h2d_bytes_per_step": int(sum(x.numel() * x.element_size() for x in (hq, hk, hv))),

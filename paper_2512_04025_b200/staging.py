@@ -60,6 +60,19 @@ def _host_bhnd(x, name: str):
     return x4.contiguous(), lead
 
 
+def _group_sizes(n: int) -> list:
+    """KV-head group sizes for one batch entry: about six equal groups, then two smaller ones so
+    the compute and copy-out left after the last copy-in (the pipeline's tail) stay short."""
+    if n <= 4:
+        return [1] * n
+    base = max(1, round(n / 7))
+    tail = [max(1, base // 2), max(1, base // 4)]
+    body = n - sum(tail)
+    k = max(1, math.ceil(body / base))
+    per = [body // k + (1 if i < body % k else 0) for i in range(k)]
+    return per + tail
+
+
 def psa_attention_staged(q, k, v, cfg=None, *, device=None, kv_heads_per_group: int | None = None,
                          out: torch.Tensor | None = None, lse: torch.Tensor | None = None,
                          keep_level_map: bool = False, keep_scores: bool = False,
@@ -67,8 +80,9 @@ def psa_attention_staged(q, k, v, cfg=None, *, device=None, kv_heads_per_group: 
     """PSA forward of host tensors on ``device`` (default: the current CUDA device).
 
     ``out`` / ``lse``: optional preallocated (ideally pinned) host outputs of shapes
-    q.shape and q.shape[:-1]. ``kv_heads_per_group``: pipeline granularity (default: about
-    eight groups per call). Returns once the outputs are in host memory.
+    q.shape and q.shape[:-1]. ``kv_heads_per_group``: pipeline granularity (default: about six
+    equal groups followed by two smaller ones, which shortens the pipeline tail). Returns once
+    the outputs are in host memory.
     """
     from .pipeline import psa_forward_4d, resolve_config
 
@@ -91,8 +105,10 @@ def psa_attention_staged(q, k, v, cfg=None, *, device=None, kv_heads_per_group: 
     lay = cfg.layout()
     group = Hq // Hkv
     if kv_heads_per_group is None:
-        kv_heads_per_group = max(1, math.ceil(B * Hkv / 8))
-    g = max(1, min(Hkv, int(kv_heads_per_group)))
+        sizes = _group_sizes(Hkv) if B == 1 else [max(1, math.ceil(B * Hkv / 8))]
+    else:
+        sizes = [max(1, min(Hkv, int(kv_heads_per_group)))]
+    g = max(sizes)
 
     if out is None:
         out = torch.empty(q4.shape, dtype=torch.bfloat16, pin_memory=True)
@@ -105,7 +121,13 @@ def psa_attention_staged(q, k, v, cfg=None, *, device=None, kv_heads_per_group: 
     lmap = (torch.empty(B, Hq, lay.n_q, lay.n_k, dtype=torch.int8, pin_memory=True)
             if keep_level_map else None)
 
-    groups = [(b, h0, min(Hkv, h0 + g)) for b in range(B) for h0 in range(0, Hkv, g)]
+    groups = []
+    for b in range(B):
+        h0, gi = 0, 0
+        while h0 < Hkv:
+            step = sizes[min(gi, len(sizes) - 1)]
+            groups.append((b, h0, min(Hkv, h0 + step)))
+            h0, gi = h0 + step, gi + 1
     with torch.cuda.device(dev):
         cur = torch.cuda.current_stream(dev)
         s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
