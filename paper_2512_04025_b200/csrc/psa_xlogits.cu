@@ -249,6 +249,12 @@ constexpr uint32_t xl_idesc(int M, int N) {
 PSA_DEV double pow2(int k) {  // exact 2^k for the normal range
   return __longlong_as_double(static_cast<long long>(k + 1023) << 52);
 }
+// exact int32 -> fp64 without a conversion instruction: 1.5*2^52 + 2^31 + x has x in the low
+// word once the sign bit is flipped
+PSA_DEV double i32_to_f64(int x) {
+  return __dsub_rn(__hiloint2double(0x43380000, x ^ static_cast<int>(0x80000000u)),
+                   6755401588539392.0);  // 1.5 * 2^52 + 2^31
+}
 // exact int64 -> fp64 for |v| < 2^51
 PSA_DEV double i64_to_f64_exact(long long v) {
   return __dsub_rn(__longlong_as_double(v + 0x4338000000000000LL), 6755399441055744.0);
@@ -478,15 +484,15 @@ __global__ void __launch_bounds__(kXlThreads, 1)
         tmem_wait_ld();
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          // classes (weights 2^(7c)): exact int32 pairs, then two exact int64 partial sums
+          // classes (weights 2^(7c)): exact int32 pairs (|.| < 2^31), each converted exactly to
+          // fp64; the partial sums below 2^53 are exact, the last fma rounds the exact dot once
           const int lo32 = static_cast<int>(cv[0][e]) + (static_cast<int>(cv[1][e]) << 7);
           const int mid32 = static_cast<int>(cv[2][e]) + (static_cast<int>(cv[3][e]) << 7);
           const int hi32 = static_cast<int>(cv[4][e]) + (static_cast<int>(cv[5][e]) << 7);
-          const long long lo = static_cast<long long>(lo32) + (static_cast<long long>(mid32) << 14);
-          const long long hi = static_cast<long long>(hi32) +
-                               (static_cast<long long>(static_cast<int>(cv[6][e])) << 14);
-          // exact dot(X, Y) = hi * 2^28 + lo, rounded once
-          dv[c8 * 8 + e] = __fma_rn(i64_to_f64_exact(hi), 268435456.0, i64_to_f64_exact(lo));
+          const double lo = __fma_rn(i32_to_f64(mid32), 16384.0, i32_to_f64(lo32));
+          const double hi = __fma_rn(i32_to_f64(static_cast<int>(cv[6][e])), 16384.0,
+                                     i32_to_f64(hi32));
+          dv[c8 * 8 + e] = __fma_rn(hi, 268435456.0, lo);  // exact dot(X, Y) rounded once
         }
       }
       tc_fence_before();
