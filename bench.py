@@ -289,10 +289,18 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     cfg = CONFIGS[args.config]
+    # PSA_BENCH_DIST_BACKEND=gloo lets several ranks share one GPU to exercise the multi-rank
+    # logic (NCCL needs one GPU per rank); timings are still CUDA events, max over ranks.
+    backend = os.environ.get("PSA_BENCH_DIST_BACKEND", "nccl")
+    ngpu = max(1, torch.cuda.device_count())
+    device = torch.device(f"cuda:{local % ngpu}")
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    device = torch.device(f"cuda:{local}")
+        torch.cuda.set_device(device)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group(backend)
+    red_dev = device if backend == "nccl" else torch.device("cpu")
 
     if args.impl == "reference":
         return main_reference(args, cfg, rank, world, device)
@@ -310,8 +318,9 @@ def main():
     from paper_2512_04025_b200.parallel import shard_heads
     Hq, Hkv = cfg["Hq"], cfg["Hkv"]
     heads, kv_heads = shard_heads(Hq, Hkv, world, rank)
-    if not heads:
-        raise SystemExit("more ranks than kv heads")
+    has_work = bool(heads)  # more ranks than KV heads: the extra ranks idle but keep the barriers
+    if not has_work:
+        heads, kv_heads = [0], [0]  # placeholder tensors, never launched
     q, k, v = make_inputs(cfg, heads, kv_heads, device)
     rc = run_config(cfg)
     lay = rc.layout()
@@ -325,6 +334,11 @@ def main():
 
     def step(events=None):
         ev = events
+        if not has_work:
+            if ev:
+                for e in ev:
+                    e.record(stream)
+            return None, None
         if ev: ev[0].record(stream)
         pyr = build_pyramid(k, v, lay)
         caps = similarity_caps(k, lay, sim) if sim is not None else None
@@ -345,8 +359,12 @@ def main():
     for _ in range(max(args.warmup, 3)):
         plan, _ = step()
     torch.cuda.synchronize()
-    counts = plan.level_counts.cpu().tolist()
-    flops_local = flops_from_counts(counts, cfg, cfg["B"] * len(heads))
+    counts = plan.level_counts.cpu().tolist() if has_work else [0] * (lay.levels + 1)
+    flops_local = flops_from_counts(counts, cfg, cfg["B"] * len(heads)) if has_work else 0
+    if world > 1:  # whole-job level histogram
+        ct = torch.tensor(counts, dtype=torch.int64, device=red_dev)
+        dist.all_reduce(ct, op=dist.ReduceOp.SUM)
+        counts = ct.cpu().tolist()
     rho_bar = psa.report_from_counts(counts, sum(counts)).rho_bar
 
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
@@ -367,7 +385,7 @@ def main():
                                       for s in range(args.steps))
                 for i, name in enumerate(stage_names)}
     stats = torch.tensor([ms_total, float(flops_local), stage_ms["attention"]], dtype=torch.float64,
-                         device=device)
+                         device=red_dev)
     if world > 1:
         mx = stats.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
@@ -382,7 +400,7 @@ def main():
     # ---- end-to-end through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(psa, rc, q, k, v, args, stream, flops_all, world, device)
+        e2e = run_e2e(psa, rc, q, k, v, args, stream, flops_all, world, device, has_work, red_dev)
 
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
         if (ROOT / "MEASURED_PEAKS.json").exists() else {}
@@ -440,7 +458,8 @@ def main():
         dist.destroy_process_group()
 
 
-def run_e2e(psa, rc, q, k, v, args, stream, flops_all, world, device):
+def run_e2e(psa, rc, q, k, v, args, stream, flops_all, world, device, has_work=True,
+            red_dev=None):
     """Same metric through the public call a user makes with host data: psa.psa_attention on
     pinned host Q/K/V returns O and lse in pinned host memory. Every timed step includes the H2D
     of Q/K/V and the D2H of O/lse (the call pipelines head groups over copy-in / compute /
@@ -454,6 +473,8 @@ def run_e2e(psa, rc, q, k, v, args, stream, flops_all, world, device):
     per_group = int(os.environ["PSA_E2E_GROUP"]) if os.environ.get("PSA_E2E_GROUP") else None
 
     def one():
+        if not has_work:
+            return None
         return psa.psa_attention(hq, hk, hv, rc, device=device, out=out_h, lse=lse_h,
                                  kv_heads_per_group=per_group)
 
@@ -472,7 +493,7 @@ def run_e2e(psa, rc, q, k, v, args, stream, flops_all, world, device):
     torch.cuda.synchronize()
     wall = (time.perf_counter() - t0) * 1e3 / steps
     ms = a.elapsed_time(b) / steps
-    t = torch.tensor([ms], dtype=torch.float64, device=device)
+    t = torch.tensor([ms], dtype=torch.float64, device=red_dev or device)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t[0])
@@ -500,9 +521,12 @@ def main_reference(args, cfg, rank, world, device):
     the host cores, same config/metric/unit; rank 0 only. Nothing from the GPU package runs here:
     inputs are synthesised with torch's RNG (on the GPU when present, the same per-head streams as
     our arm) and the executed FLOPs come from the oracle's own level maps."""
-    if rank != 0:
-        return
     import torch
+    import torch.distributed as dist
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
     cores = os.cpu_count() or 1
     heads = list(range(min(cores, cfg["Hq"])))
     group = cfg["Hq"] // cfg["Hkv"]
@@ -526,6 +550,8 @@ def main_reference(args, cfg, rank, world, device):
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":
