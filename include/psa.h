@@ -114,7 +114,9 @@ int psa_importance_antidiagonal(const void* q, const void* k, int64_t batch, int
  * Outputs: level_map int8 [batch*hq, n_q, n_k];
  *   plan_csr uint16 [batch*hq*n_q, n_k]: per (head, query block) the selected blocks as
  *     (j | (level << 12)), level-major (level 1 first), ascending j within a level;
- *   plan_info int32 [batch*hq*n_q, 2]: (number of entries, number of 128-row KV tiles);
+ *   plan_info int32 [batch*hq*n_q, 2]: (number of entries, total slot rows R: every selected
+ *     pooled segment rounded up to a power of two >= 8 rows; an executor with T-row tiles runs
+ *     ceil(R / T) tiles — the segments pack perfectly in level-major order);
  *   level_counts uint64 [levels+1] (accumulated: caller zeroes it).
  */
 int psa_assign_levels(const double* scores, int64_t batch, int hq, int hkv, int n_q, int n_k,

@@ -143,7 +143,7 @@ PSA_DEV void emit_plan_row(const int8_t* lvl, int n_k, int levels, int b_k, int6
   }
   if (threadIdx.x == 0) {
     info[unit * 2 + 0] = base;
-    info[unit * 2 + 1] = static_cast<int32_t>((rows_total + 127) / 128);
+    info[unit * 2 + 1] = static_cast<int32_t>(rows_total);  // slot rows; tiles = ceil(rows / tile)
     if (level_counts && n_k - base)
       atomicAdd(level_counts, static_cast<unsigned long long>(n_k - base));
   }

@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   const int b = bhq / p.hq, hh = bhq % p.hq;
   const int64_t bhkv = static_cast<int64_t>(b) * p.hkv + hh / (p.hq / p.hkv);
   const int n_ent = info[unit * 2 + 0];
-  const int T = info[unit * 2 + 1];
+  const int T = (info[unit * 2 + 1] + kTileRows - 1) / kTileRows;  // 128-row KV tiles
   const int64_t q_row0 = static_cast<int64_t>(bhq) * p.n + static_cast<int64_t>(i) * p.b_q;
 
   // ---------------------------------------------------------------- setup
@@ -552,7 +552,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
   const int b = bhq / p.hq, hh = bhq % p.hq;
   const int64_t bhkv = static_cast<int64_t>(b) * p.hkv + hh / (p.hq / p.hkv);
   const int n_ent = info[unit * 2 + 0];
-  const int T = info[unit * 2 + 1];
+  const int T = (info[unit * 2 + 1] + kTileRows - 1) / kTileRows;  // 128-row KV tiles
   const int64_t q_row0 = static_cast<int64_t>(bhq) * p.n + static_cast<int64_t>(i) * p.b_q;
 
   if (threadIdx.x == 0) {
@@ -965,7 +965,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
   const int b = bhq / p.hq, hh = bhq % p.hq;
   const int64_t bhkv = static_cast<int64_t>(b) * p.hkv + hh / (p.hq / p.hkv);
   const int n_ent = info[unit * 2 + 0];
-  const int T = info[unit * 2 + 1];
+  const int T = (info[unit * 2 + 1] + kTileRows - 1) / kTileRows;  // 128-row KV tiles
   const int64_t q_row0 = static_cast<int64_t>(bhq) * p.n + static_cast<int64_t>(i) * p.b_q;
 
   if (threadIdx.x == 0) {

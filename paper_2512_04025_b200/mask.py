@@ -28,7 +28,7 @@ class MaskPlan:
 
     level_map: torch.Tensor      # int8 [B, Hq, n_q, n_k]
     csr: torch.Tensor            # uint16-as-int16 [B*Hq*n_q, n_k]: j | level << 12
-    info: torch.Tensor           # int32 [B*Hq*n_q, 2]: (entries, 128-row tiles)
+    info: torch.Tensor           # int32 [B*Hq*n_q, 2]: (entries, total power-of-two slot rows)
     level_counts: torch.Tensor   # int64 [levels+1] (device)
     levels: int
 

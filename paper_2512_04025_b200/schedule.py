@@ -199,7 +199,7 @@ def plan_utilization(plan, layout: BlockLayout, tile_rows: int = 128) -> Utiliza
     unused."""
     counts = [int(c) for c in plan.level_counts.cpu().tolist()]
     useful = sum(c * layout.pooled_len(h) for h, c in enumerate(counts) if h >= 1)
-    n_tiles = int(plan.info[:, 1].sum().item())
+    n_tiles = int(((plan.info[:, 1] + tile_rows - 1) // tile_rows).sum().item())
     capacity = n_tiles * tile_rows
     return UtilizationStats(tiles=n_tiles, useful_rows=useful, capacity=capacity,
                             utilization=useful / capacity if capacity else 1.0)
