@@ -36,6 +36,10 @@ CONFIGS = {
                  d=128, b_q=120, b_k=120, levels=4, taus=WAN_TAUS, causal=False),
     "cfg3": dict(desc="Wan2.1-14B 720p/81f: L=75600 H=40 d=128", B=1, Hq=40, Hkv=40, N=75600,
                  d=128, b_q=120, b_k=120, levels=4, taus=WAN_TAUS, causal=False),
+    "cfg5": dict(desc="compute-budget sweep 10-50% at L=32760 H=12 d=128 vs dense and binary "
+                      "(quantile cutpoints 0.6b,b,1.8b,1.8b -> rho_bar=b; binary = b at level 1)",
+                 B=1, Hq=12, Hkv=12, N=32760, d=128, b_q=120, b_k=120, levels=4, taus=WAN_TAUS,
+                 causal=False),
     "cfg4": dict(desc="Qwen2.5-VL-7B-style prefill: L=32768 Hq=28 Hkv=4 d=128 causal, "
                       "antidiagonal stride 8 + similarity cap (0.75,0.70,0.70)", B=1, Hq=28,
                  Hkv=4, N=32768, d=128, b_q=128, b_k=64, levels=4, taus=WAN_TAUS, causal=True,
@@ -304,6 +308,8 @@ def main():
 
     if args.impl == "reference":
         return main_reference(args, cfg, rank, world, device)
+    if args.config == "cfg5":
+        return main_sweep(args, cfg, rank, world, device, red_dev)
 
     import paper_2512_04025_b200 as psa
     from paper_2512_04025_b200 import _lib
@@ -452,6 +458,104 @@ def main():
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main_sweep(args, cfg, rank, world, device, red_dev):
+    """cfg5: PSA forward at budgets b = 0.1..0.5 (quantile cutpoints (0.6b, b, 1.8b, 1.8b), the
+    PSA-3 family: rho_bar = b), the binary block-sparse baseline at the same budgets (one level,
+    cutpoint b), and dense attention (this kernel with every block at level 1, and torch SDPA as
+    the external FlashAttention-style yardstick). Device time per full forward and per attention
+    launch; heads sharded over ranks like the other configs."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2512_04025_b200 as psa
+    from paper_2512_04025_b200 import _lib
+    from paper_2512_04025_b200.attention import attention_forward
+    from paper_2512_04025_b200.parallel import shard_heads
+    from paper_2512_04025_b200.pipeline import psa_forward_4d
+
+    _lib.load()
+    heads, kv_heads = shard_heads(cfg["Hq"], cfg["Hkv"], world, rank)
+    has_work = bool(heads)
+    if not has_work:
+        heads, kv_heads = [0], [0]
+    q, k, v = make_inputs(cfg, heads, kv_heads, device)
+    stream = torch.cuda.current_stream(device)
+    reps = max(1, args.steps)
+
+    def timed(fn):
+        for _ in range(max(args.warmup, 3)):
+            fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        a.record(stream)
+        for _ in range(reps):
+            if has_work:
+                fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([a.elapsed_time(b) / reps], dtype=torch.float64, device=red_dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t[0])
+
+    def base_cfg(**kw):
+        d = dict(n=cfg["N"], d=cfg["d"], b_q=cfg["b_q"], b_k=cfg["b_k"], levels=cfg["levels"],
+                 estimator="sampled-max", s_q=8, s_k=8, seed=0, tile_len=128)
+        d.update(kw)
+        return psa.RunConfig.from_dict(d)
+
+    rows = []
+    for beta in (0.1, 0.2, 0.3, 0.4, 0.5):
+        entry = {"budget": beta}
+        for name, rc in (("psa", base_cfg(mask="quantile",
+                                          cutpoints=[0.6 * beta, beta, 1.8 * beta, 1.8 * beta])),
+                         ("binary", base_cfg(mask="quantile", cutpoints=[beta]))):
+            res = psa_forward_4d(q, k, v, rc)
+            counts = res.plan.level_counts.cpu().tolist()
+            flops = flops_from_counts(counts, cfg, cfg["B"] * len(heads)) if has_work else 0
+            ft = torch.tensor([float(flops)], dtype=torch.float64, device=red_dev)
+            if world > 1:
+                dist.all_reduce(ft, op=dist.ReduceOp.SUM)
+            step_ms = timed(lambda rc=rc: psa_forward_4d(q, k, v, rc))
+            attn_ms = timed(lambda res=res: attention_forward(q, res.pyramid, res.plan, False))
+            entry[name] = {"ms_per_forward": round(step_ms, 4), "attention_ms": round(attn_ms, 4),
+                           "rho_bar": psa.report_from_counts(counts, sum(counts)).rho_bar,
+                           "executed_tflop": float(ft[0]) / 1e12,
+                           "attention_tflops": round(float(ft[0]) / (attn_ms * 1e-3) / 1e12, 2)}
+        rows.append(entry)
+    dense_flops = 4.0 * cfg["N"] * cfg["N"] * cfg["d"] * cfg["B"] * cfg["Hq"]
+    full_ms = timed(lambda: psa.full_attention(q, k, v))
+    sdpa_ms = timed(lambda: torch.nn.functional.scaled_dot_product_attention(q, k, v))
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    b02 = rows[1]["psa"]
+    line = {
+        "metric": "PSA fwd effective TFLOPS (and ms) at Wan2.1-14B 720p shape",
+        "value": round(b02["executed_tflop"] / (b02["ms_per_forward"] * 1e-3), 3),
+        "unit": "TFLOP/s", "n_gpus": world, "steps": reps, "warmup": max(args.warmup, 3),
+        "ms_per_step": b02["ms_per_forward"], "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic N(0,1) bf16 Q/K/V (seeded torch.Generator per head)",
+        "config": {"workload": f"cfg5: {cfg['desc']}", "L": cfg["N"], "Hq": cfg["Hq"],
+                   "d": cfg["d"], "b": cfg["b_q"], "value_at_budget": 0.2,
+                   "parallelism": f"heads sharded over {world} GPU(s)"},
+        "sweep": rows,
+        "dense": {"tflop": dense_flops / 1e12,
+                  "psa_kernel_all_level1_ms": round(full_ms, 4),
+                  "psa_kernel_all_level1_tflops": round(dense_flops / (full_ms * 1e-3) / 1e12, 2),
+                  "torch_sdpa_ms": round(sdpa_ms, 4),
+                  "torch_sdpa_tflops": round(dense_flops / (sdpa_ms * 1e-3) / 1e12, 2)},
+        "gpu_launches": None,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
