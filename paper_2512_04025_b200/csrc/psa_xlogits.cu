@@ -409,7 +409,14 @@ __global__ void __launch_bounds__(kXlThreads, 1)
       }
     }
   } else if (warp == 1) {
-    constexpr uint32_t idesc = xl_idesc(kXlQRows, kXlKeys);
+    // Class c = a + b accumulates at columns [c * 32, c * 32 + 32) of the buffer. For slice a of
+    // Q one MMA covers K slices b = 0..2 (N = 96, classes a..a+2) and one covers b = 3 (N = 32,
+    // class a+3, first writer of that class for a >= 1); slice 0 covers b = 0..3 in one N = 128
+    // MMA. 7 MMAs per K step instead of 16 pair MMAs: 2.3x fewer A-operand reads.
+    constexpr uint32_t idesc128 = xl_idesc(kXlQRows, 4 * kXlKeys);
+    constexpr uint32_t idesc96 = xl_idesc(kXlQRows, 3 * kXlKeys);
+    constexpr uint32_t idesc32 = xl_idesc(kXlQRows, kXlKeys);
+    static_assert(kXlSlices == 4, "class layout assumes 4 slices");
     mbar_wait(&sm.q_full, 0);
     tc_fence_after();
     for (int t = 0; t < T; ++t) {
@@ -418,20 +425,23 @@ __global__ void __launch_bounds__(kXlThreads, 1)
       if (t >= kXlAccBufs) mbar_wait_backoff(&sm.acc_empty[ab], ((t / kXlAccBufs) - 1) & 1);
       tc_fence_after();
       if (elect_one()) {
+        const uint32_t dbuf = tmem + ab * (kXlClasses * kXlKeys);
+        const uint64_t b0 = umma_desc_sw128(smem_u32(sm.k[s][0]), 16, 1024);
+        const uint64_t b3 = umma_desc_sw128(smem_u32(sm.k[s][3]), 16, 1024);
 #pragma unroll
-        for (int a = 0; a < kXlSlices; ++a)
+        for (int a = 0; a < kXlSlices; ++a) {
+          const uint64_t ad = umma_desc_sw128(smem_u32(sm.q[a]), 16, 1024);
 #pragma unroll
-          for (int bb = 0; bb < kXlSlices; ++bb) {
-            const int c = a + bb;
-            const bool first = (a == 0) || (bb == kXlSlices - 1 && a == c - bb && c >= kXlSlices);
-            const uint64_t ad = umma_desc_sw128(smem_u32(sm.q[a]), 16, 1024);
-            const uint64_t bd = umma_desc_sw128(smem_u32(sm.k[s][bb]), 16, 1024);
-            const uint32_t dcol = tmem + ab * (kXlClasses * kXlKeys) + c * kXlKeys;
-#pragma unroll
-            for (int kk = 0; kk < D / 32; ++kk)
-              mma_i8_ss(dcol, ad + ((kk * 32) >> 4), bd + ((kk * 32) >> 4), idesc,
-                        (first && kk == 0) ? 0u : 1u);
+          for (int kk = 0; kk < D / 32; ++kk) {
+            const uint32_t ko = (kk * 32) >> 4;
+            if (a == 0) {
+              mma_i8_ss(dbuf, ad + ko, b0 + ko, idesc128, kk == 0 ? 0u : 1u);
+            } else {
+              mma_i8_ss(dbuf + a * kXlKeys, ad + ko, b0 + ko, idesc96, 1u);
+              mma_i8_ss(dbuf + (a + 3) * kXlKeys, ad + ko, b3 + ko, idesc32, kk == 0 ? 0u : 1u);
+            }
           }
+        }
         mma_commit(&sm.k_empty[s]);
         mma_commit(&sm.acc_full[ab]);
       }
