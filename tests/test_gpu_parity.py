@@ -332,17 +332,20 @@ def _with_tiny(x, rng, rows, per_row):
 @pytest.mark.parametrize("kind,n,d,b,sk_or_stride", [
     ("sampled", 4096, 128, 64, 8), ("sampled", 3840, 128, 120, 8), ("sampled", 2048, 64, 64, 7),
     ("antidiag", 4096, 128, 64, 8), ("antidiag", 3840, 128, 120, 4), ("antidiag", 1920, 64, 120, 8)])
-@pytest.mark.parametrize("tiny", [0, 2, 6])
+@pytest.mark.parametrize("tiny", [0, 2, 6, -1])
 def test_int8_exact_logits_match_fp64_path(kind, n, d, b, sk_or_stride, tiny):
     """The int8 tensor-core logits (psa_xlogits.cu) reproduce the fp64 DMMA path: scores agree to
     a few ulps (only the softmax-denominator summation order differs), level maps exactly, and
-    both match the oracle at 1e-12. tiny=2: exact corrections; tiny=6: fp64 fallback heads."""
+    both match the oracle at 1e-12. tiny=2: exact corrections; tiny=6: fp64 fallback heads;
+    tiny=-1: one head with 32x larger queries (logits up to ~100: peaked softmax rows)."""
     from paper_2512_04025_b200.importance import antidiagonal_scores, importance_scores
     from paper_2512_04025_b200.mask import assign_levels_device
     psa = _psa()
     rng = np.random.default_rng(17 + tiny)
     q, k, v = gaussian_qkv(23, 3, n, d)
-    if tiny:
+    if tiny < 0:
+        q[1] = q[1] * 32.0  # power of two: still exact bf16
+    elif tiny:
         q[1] = _with_tiny(q[1], rng, rng.choice(n, 64, replace=False), tiny)
         k[2] = _with_tiny(k[2], rng, rng.choice(n, 64, replace=False), tiny)
     lay = psa.make_layout(n, d, b, b, 4)
