@@ -24,7 +24,8 @@
 //
 // Kernel shape: one CTA per (head, residue class, 128 gathered query rows); 12 warps.
 //   warp 0  TMA: the 3 query slice tiles once, then 3 x (32 keys x 128 B) per key tile
-//   warp 1  MMA: 16 slice pairs x D/32 k-steps of tcgen05.mma.kind::i8 (M=128, N=32)
+//   warp 1  MMA: per k-step, Q slice a x the 4 contiguous K slices as one N=128
+//           tcgen05.mma.kind::i8 into the class columns a..a+3 (4 MMAs instead of 16 pairs)
 //   warp 2  TMEM allocator (2 accumulator buffers x 7 classes x 32 columns)
 //   warps 4-11  epilogue, two groups taking alternate key tiles (group g owns accumulator
 //           buffer g; their running (m, l) merge at the end). The epilogue is FP64-pipe bound
@@ -228,6 +229,12 @@ PSA_DEV void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
                : "r"(taddr)
                : "memory");
 }
+PSA_DEV void tmem_zero16(uint32_t taddr) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, "
+      "%1, %1, %1, %1, %1};" ::"r"(taddr), "r"(0u)
+      : "memory");
+}
 PSA_DEV void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 PSA_DEV void mma_i8_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
@@ -392,6 +399,17 @@ __global__ void __launch_bounds__(kXlThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
+  if (warp >= 4 && warp < 8) {  // classes 4-6 start at zero (the MMAs only accumulate into them)
+    const uint32_t tl = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+    for (int ab = 0; ab < kXlAccBufs; ++ab)
+      for (int c = kXlSlices; c < kXlClasses; ++c)
+        for (int h2 = 0; h2 < kXlKeys / 16; ++h2)
+          tmem_zero16(tl + ab * (kXlClasses * kXlKeys) + c * kXlKeys + h2 * 16);
+    tmem_st_wait();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -409,13 +427,11 @@ __global__ void __launch_bounds__(kXlThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // Class c = a + b accumulates at columns [c * 32, c * 32 + 32) of the buffer. For slice a of
-    // Q one MMA covers K slices b = 0..2 (N = 96, classes a..a+2) and one covers b = 3 (N = 32,
-    // class a+3, first writer of that class for a >= 1); slice 0 covers b = 0..3 in one N = 128
-    // MMA. 7 MMAs per K step instead of 16 pair MMAs: 2.3x fewer A-operand reads.
+    // Class c = a + b accumulates at columns [c * 32, c * 32 + 32) of the buffer: slice a of Q
+    // against the 4 contiguous K slices is ONE N = 128 MMA into columns [a * 32, a * 32 + 128).
+    // Classes 0-3 are initialised by slice 0; classes 4-6 are zeroed by the epilogue after it
+    // reads them, so slices 1-3 only accumulate. 4 MMAs per K step.
     constexpr uint32_t idesc128 = xl_idesc(kXlQRows, 4 * kXlKeys);
-    constexpr uint32_t idesc96 = xl_idesc(kXlQRows, 3 * kXlKeys);
-    constexpr uint32_t idesc32 = xl_idesc(kXlQRows, kXlKeys);
     static_assert(kXlSlices == 4, "class layout assumes 4 slices");
     mbar_wait(&sm.q_full, 0);
     tc_fence_after();
@@ -427,19 +443,13 @@ __global__ void __launch_bounds__(kXlThreads, 1)
       if (elect_one()) {
         const uint32_t dbuf = tmem + ab * (kXlClasses * kXlKeys);
         const uint64_t b0 = umma_desc_sw128(smem_u32(sm.k[s][0]), 16, 1024);
-        const uint64_t b3 = umma_desc_sw128(smem_u32(sm.k[s][3]), 16, 1024);
 #pragma unroll
         for (int a = 0; a < kXlSlices; ++a) {
           const uint64_t ad = umma_desc_sw128(smem_u32(sm.q[a]), 16, 1024);
 #pragma unroll
           for (int kk = 0; kk < D / 32; ++kk) {
             const uint32_t ko = (kk * 32) >> 4;
-            if (a == 0) {
-              mma_i8_ss(dbuf, ad + ko, b0 + ko, idesc128, kk == 0 ? 0u : 1u);
-            } else {
-              mma_i8_ss(dbuf + a * kXlKeys, ad + ko, b0 + ko, idesc96, 1u);
-              mma_i8_ss(dbuf + (a + 3) * kXlKeys, ad + ko, b3 + ko, idesc32, kk == 0 ? 0u : 1u);
-            }
+            mma_i8_ss(dbuf + a * kXlKeys, ad + ko, b0 + ko, idesc128, (a > 0 || kk > 0) ? 1u : 0u);
           }
         }
         mma_commit(&sm.k_empty[s]);
@@ -505,6 +515,9 @@ __global__ void __launch_bounds__(kXlThreads, 1)
           dv[c8 * 8 + e] = __fma_rn(hi, 268435456.0, lo);  // exact dot(X, Y) rounded once
         }
       }
+#pragma unroll
+      for (int c = kXlSlices; c < kXlClasses; ++c) tmem_zero16(t_acc + c * kXlKeys);
+      tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&sm.acc_empty[buf]);
       if (nb == 0) continue;  // odd half count: this half of the last tile holds no block
