@@ -56,6 +56,17 @@ int psa_pyramid_build(const void* k, const void* v, int64_t bh, int64_t n, int d
                       int levels, void* k_pyr, void* v_pyr, int32_t* nonfinite, void* stream);
 
 /*
+ * Pyramid of token-permuted K/V.  Fuses apply_permutation (pkg/src/pyrattn/permute.py:131-137,
+ * as pipeline._run_head applies it before pooling, pipeline.py:257-263) into the pyramid build
+ * (blocks.py:93-109): row p of each head reads source row index[p].  Writes the permuted K/V
+ * (level 1) to k1/v1 [bh, n, d] and levels 2..H to k_pyr/v_pyr as psa_pyramid_build does.
+ * index: DEVICE int64 [n], a bijection.
+ */
+int psa_pyramid_build_gather(const void* k, const void* v, int64_t bh, int64_t n, int d, int b_k,
+                             int levels, const int64_t* index, void* k1, void* v1, void* k_pyr,
+                             void* v_pyr, int32_t* nonfinite, void* stream);
+
+/*
  * Similarity cap (Alg. 3).  Replaces level_cap_from_similarity / _strided_block_similarity
  * (pkg/src/pyrattn/mask.py:182-234).  sim_taus: HOST array of levels-1 thresholds.
  * caps: int8 [bh, n/b_k], each in 1..levels.
@@ -149,6 +160,17 @@ int psa_attn_fwd(const void* q, const void* k, const void* v, const void* k_pyr,
                  const void* v_pyr, int64_t batch, int hq, int hkv, int64_t n, int d, int b_q,
                  int b_k, int levels, const uint16_t* plan_csr, const int32_t* plan_info,
                  int causal, void* out, float* lse, int32_t* skipped_rows, void* stream);
+
+/*
+ * psa_attn_fwd with the unpermute of pipeline._run_head (pipeline.py:312-313) fused into the
+ * epilogue: O and lse of row i of each head are stored at row out_rows[i] (out_rows: DEVICE int64
+ * [n], the curve order; NULL = identity).  Only the default kernel has the scatter epilogue.
+ */
+int psa_attn_fwd_scatter(const void* q, const void* k, const void* v, const void* k_pyr,
+                         const void* v_pyr, int64_t batch, int hq, int hkv, int64_t n, int d,
+                         int b_q, int b_k, int levels, const uint16_t* plan_csr,
+                         const int32_t* plan_info, int causal, void* out, float* lse,
+                         int32_t* skipped_rows, const int64_t* out_rows, void* stream);
 
 /*
  * Token permutation.  Replaces apply_permutation (pkg/src/pyrattn/permute.py:131-137) for the

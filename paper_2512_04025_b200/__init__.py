@@ -18,7 +18,7 @@ from .mask import (MaskPlan, SparsityReport, assign_quantile, assign_threshold, 
 from .permute import Permutation, apply_permutation, hilbert_order, invert_permutation
 from .pipeline import (PipelineResult, PSAResult, RunConfig, psa_attention, psa_forward_4d,
                        relative_error, report_to_json, run_pipeline)
-from .pyramid import PyramidKV, build_pyramid, level_cap_from_similarity
+from .pyramid import PyramidKV, build_pyramid, build_pyramid_gather, level_cap_from_similarity
 from .schedule import (ExecutionTile, Segment, TileSchedule, UtilizationStats, build_schedule,
                        execute_schedule, plan_utilization, utilization)
 
@@ -32,7 +32,7 @@ __all__ = [
     "PipelineResult", "relative_error", "report_to_json", "run_pipeline",
     "PRESET_CUTPOINTS", "PSAResult", "PyramidKV", "QuantileCutpoints", "RunConfig",
     "SamplerConfig", "SimThresholds", "SparsityReport", "TensorFileError", "ValidationError",
-    "assign_quantile", "assign_threshold", "binary_mask", "build_pyramid",
+    "assign_quantile", "assign_threshold", "binary_mask", "build_pyramid", "build_pyramid_gather",
     "causal_full_attention", "causal_premask", "combine_mask", "full_attention",
     "antidiagonal_selection", "importance_antidiagonal", "importance_sampled", "level_bias",
     "level_cap_from_similarity", "make_layout",

@@ -43,6 +43,13 @@ _SIGNATURES = {
     "psa_attn_fwd": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int,
                              c_int, c_int64, c_int, c_int, c_int, c_int, c_void_p, c_void_p,
                              c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "psa_attn_fwd_scatter": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64,
+                                     c_int, c_int, c_int64, c_int, c_int, c_int, c_int, c_void_p,
+                                     c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
+                                     c_void_p]),
+    "psa_pyramid_build_gather": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int, c_int, c_int,
+                                         c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                         c_void_p, c_void_p]),
 }
 
 EXPORTED = tuple(_SIGNATURES)

@@ -44,8 +44,9 @@ def level_bias(level: int, max_level: int | None = None) -> float:
 
 def attention_forward(q4: torch.Tensor, pyr: PyramidKV, plan: MaskPlan, causal: bool,
                       out: torch.Tensor | None = None, lse: torch.Tensor | None = None,
-                      skipped: torch.Tensor | None = None):
-    """Launch psa_attn_fwd on device tensors; returns (out, lse, skipped-counter)."""
+                      skipped: torch.Tensor | None = None, out_rows: torch.Tensor | None = None):
+    """Launch psa_attn_fwd on device tensors; returns (out, lse, skipped-counter). ``out_rows``
+    (device int64 [n]): store O/lse row i of every head at row out_rows[i] (fused unpermute)."""
     lay = pyr.layout
     B, Hq, n, d = q4.shape
     Hkv = pyr.k_raw.shape[1]
@@ -57,11 +58,14 @@ def attention_forward(q4: torch.Tensor, pyr: PyramidKV, plan: MaskPlan, causal: 
     lse = torch.empty(B, Hq, n, dtype=torch.float32, device=dev) if lse is None else lse
     if skipped is None:
         skipped = torch.zeros(1, dtype=torch.int32, device=dev)
-    rc = _lib.load().psa_attn_fwd(
+    if out_rows is not None and (out_rows.numel() != n or out_rows.dtype != torch.int64
+                                 or out_rows.device != dev):
+        raise ValidationError(f"out_rows must be a device int64 tensor of {n} entries")
+    rc = _lib.load().psa_attn_fwd_scatter(
         q4.data_ptr(), pyr.k_raw.data_ptr(), pyr.v_raw.data_ptr(), _lib.ptr(pyr.k_pyr),
         _lib.ptr(pyr.v_pyr), B, Hq, Hkv, n, d, lay.q_block, lay.k_block, lay.levels,
         plan.csr.data_ptr(), plan.info.data_ptr(), int(causal), out.data_ptr(), lse.data_ptr(),
-        skipped.data_ptr(), stream_handle(dev))
+        skipped.data_ptr(), _lib.ptr(out_rows), stream_handle(dev))
     _lib.check(rc, "psa_attn_fwd")
     return out, lse, skipped
 

@@ -62,6 +62,7 @@ struct AttnParams {
   int64_t n;
   int hq, hkv, b_q, b_k, levels, n_q, n_k, causal;
   float scale_log2;
+  const int64_t* out_rows;  // optional scatter: O/lse row i of a head goes to row out_rows[i]
 };
 
 template <int D>
@@ -1299,7 +1300,11 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     const float inv = alive ? 1.f / l_tot : 0.f;
     const float w0 = a0 * inv, w1 = a1 * inv;
     constexpr int OC = D / 2;  // output columns per lane
-    uint16_t* orow = out + (q_row0 + row) * D + L * OC;
+    // unpermute (pipeline.py:312-313) fused into the store: row i of the head -> out_rows[i]
+    const int64_t o_row = p.out_rows == nullptr || !valid
+                              ? q_row0 + row
+                              : static_cast<int64_t>(bhq) * p.n + p.out_rows[i * p.b_q + row];
+    uint16_t* orow = out + o_row * D + L * OC;
 #pragma unroll
     for (int c4 = 0; c4 < OC / 32; ++c4) {
       uint32_t o0[32], o1[32];
@@ -1334,7 +1339,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       }
     }
     if (L == 0) {
-      if (valid) lse[q_row0 + row] = alive ? (m + log2f(l_tot)) * 0.69314718055994530942f : -INFINITY;
+      if (valid) lse[o_row] = alive ? (m + log2f(l_tot)) * 0.69314718055994530942f : -INFINITY;
       const unsigned dead = __ballot_sync(0xffffffffu, valid && !alive);
       if (lane == 0 && dead) atomicAdd(skipped, __popc(dead));
     }
@@ -1910,7 +1915,8 @@ template <int D>
 static int launch_attn(const void* q, const void* k, const void* v, const void* k_pyr,
                        const void* v_pyr, int64_t batch, int hq, int hkv, int64_t n, int b_q,
                        int b_k, int levels, const uint16_t* csr, const int32_t* info, int causal,
-                       void* out, float* lse, int32_t* skipped, cudaStream_t s) {
+                       void* out, float* lse, int32_t* skipped, const int64_t* out_rows,
+                       cudaStream_t s) {
   AttnMaps maps;
   memset(&maps, 0, sizeof(maps));
   AttnParams p{};
@@ -1924,6 +1930,7 @@ static int launch_attn(const void* q, const void* k, const void* v, const void* 
   p.n_k = static_cast<int>(n / b_k);
   p.causal = causal;
   p.scale_log2 = static_cast<float>(1.4426950408889634 / sqrt(static_cast<double>(D)));
+  p.out_rows = out_rows;
   const int64_t bhkv = batch * hkv;
   int rc = encode_2d(&maps.q, q, static_cast<uint64_t>(batch * hq * n), D, kTileRows);
   if (rc) return rc;
@@ -1946,6 +1953,9 @@ static int launch_attn(const void* q, const void* k, const void* v, const void* 
     const char* e = getenv("PSA_ATTN_KERNEL");
     return e != nullptr && strcmp(e, "v1") == 0;
   }();
+  if (out_rows != nullptr && getenv("PSA_ATTN_KERNEL") != nullptr &&
+      strcmp(getenv("PSA_ATTN_KERNEL"), "pp2") != 0)
+    return psa_fail(PSA_EINVAL, "the scatter epilogue exists only in the default (pp2) kernel");
   if (use_v1) {
     const size_t smem = sizeof(AttnSmem<D>);
     cudaFuncSetAttribute(psa_attn_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2014,11 +2024,12 @@ static int launch_attn(const void* q, const void* k, const void* v, const void* 
 
 using namespace psa;
 
-extern "C" int psa_attn_fwd(const void* q, const void* k, const void* v, const void* k_pyr,
-                            const void* v_pyr, int64_t batch, int hq, int hkv, int64_t n, int d,
-                            int b_q, int b_k, int levels, const uint16_t* plan_csr,
-                            const int32_t* plan_info, int causal, void* out, float* lse,
-                            int32_t* skipped_rows, void* stream) {
+extern "C" int psa_attn_fwd_scatter(const void* q, const void* k, const void* v,
+                                    const void* k_pyr, const void* v_pyr, int64_t batch, int hq,
+                                    int hkv, int64_t n, int d, int b_q, int b_k, int levels,
+                                    const uint16_t* plan_csr, const int32_t* plan_info, int causal,
+                                    void* out, float* lse, int32_t* skipped_rows,
+                                    const int64_t* out_rows, void* stream) {
   PSA_CHECK_ARG(q && k && v && plan_csr && plan_info && out && lse && skipped_rows,
                 "null pointer argument");
   PSA_CHECK_ARG(d == 64 || d == 128, "head_dim must be 64 or 128 for the sm_100a path");
@@ -2034,7 +2045,16 @@ extern "C" int psa_attn_fwd(const void* q, const void* k, const void* v, const v
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (d == 128)
     return launch_attn<128>(q, k, v, k_pyr, v_pyr, batch, hq, hkv, n, b_q, b_k, levels, plan_csr,
-                            plan_info, causal, out, lse, skipped_rows, s);
+                            plan_info, causal, out, lse, skipped_rows, out_rows, s);
   return launch_attn<64>(q, k, v, k_pyr, v_pyr, batch, hq, hkv, n, b_q, b_k, levels, plan_csr,
-                         plan_info, causal, out, lse, skipped_rows, s);
+                         plan_info, causal, out, lse, skipped_rows, out_rows, s);
+}
+
+extern "C" int psa_attn_fwd(const void* q, const void* k, const void* v, const void* k_pyr,
+                            const void* v_pyr, int64_t batch, int hq, int hkv, int64_t n, int d,
+                            int b_q, int b_k, int levels, const uint16_t* plan_csr,
+                            const int32_t* plan_info, int causal, void* out, float* lse,
+                            int32_t* skipped_rows, void* stream) {
+  return psa_attn_fwd_scatter(q, k, v, k_pyr, v_pyr, batch, hq, hkv, n, d, b_q, b_k, levels,
+                              plan_csr, plan_info, causal, out, lse, skipped_rows, nullptr, stream);
 }

@@ -21,14 +21,20 @@ namespace psa {
 // One thread: 4 consecutive columns (8 bytes) of one group of G = 2^LOGG raw rows,
 // for K (blockIdx.y == 0) or V (blockIdx.y == 1). A warp covers 128 contiguous columns
 // so every row access is a fully coalesced 256-byte segment.
-template <int LOGG>
+// GATHER: the token permutation of pipeline._run_head (pipeline.py:257-263) fused into the
+// loads: row p of a head reads source row index[p] and is also written to the permuted level 1
+// (k1/v1), so the permuted K/V and their pyramid cost one pass over K/V.
+template <int LOGG, bool GATHER>
 __global__ void __launch_bounds__(256) pyramid_kernel(const uint16_t* __restrict__ k,
                                                       const uint16_t* __restrict__ v,
                                                       int64_t groups, int d,
                                                       uint16_t* __restrict__ kp,
                                                       uint16_t* __restrict__ vp,
                                                       int64_t bh_rows /* bh*n */,
-                                                      int32_t* __restrict__ nonfinite) {
+                                                      int32_t* __restrict__ nonfinite,
+                                                      const int64_t* __restrict__ index, int64_t n,
+                                                      uint16_t* __restrict__ k1,
+                                                      uint16_t* __restrict__ v1) {
   constexpr int G = 1 << LOGG;
   const int tpg = d >> 2;  // threads per group
   const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -40,9 +46,20 @@ __global__ void __launch_bounds__(256) pyramid_kernel(const uint16_t* __restrict
 
   const int64_t row0 = g * G;
   uint2 raw[G];
+  if (GATHER) {  // G divides n: the group lies in one head
+    const int64_t head0 = row0 - row0 % n;
+    const int64_t p0 = row0 - head0;
 #pragma unroll
-  for (int r = 0; r < G; ++r)
-    raw[r] = __ldg(reinterpret_cast<const uint2*>(src + (row0 + r) * d + c4));
+    for (int r = 0; r < G; ++r)
+      raw[r] = __ldg(reinterpret_cast<const uint2*>(src + (head0 + __ldg(index + p0 + r)) * d + c4));
+    uint16_t* dst1 = blockIdx.y == 0 ? k1 : v1;
+#pragma unroll
+    for (int r = 0; r < G; ++r) *reinterpret_cast<uint2*>(dst1 + (row0 + r) * d + c4) = raw[r];
+  } else {
+#pragma unroll
+    for (int r = 0; r < G; ++r)
+      raw[r] = __ldg(reinterpret_cast<const uint2*>(src + (row0 + r) * d + c4));
+  }
 
   double stack[LOGG > 0 ? LOGG : 1][4];
   bool bad = false;
@@ -158,31 +175,44 @@ __global__ void __launch_bounds__(128) simcap_kernel(const uint16_t* __restrict_
 
 using namespace psa;
 
-extern "C" int psa_pyramid_build(const void* k, const void* v, int64_t bh, int64_t n, int d,
-                                 int b_k, int levels, void* k_pyr, void* v_pyr,
-                                 int32_t* nonfinite, void* stream) {
+static int pyramid_launch(const void* k, const void* v, int64_t bh, int64_t n, int d, int b_k,
+                          int levels, void* k_pyr, void* v_pyr, int32_t* nonfinite,
+                          const int64_t* index, void* k1, void* v1, void* stream) {
   PSA_CHECK_ARG(k && v, "K/V pointers must be non-null");
   PSA_CHECK_ARG(bh >= 1 && n >= 1, "bh and n must be positive");
   PSA_CHECK_ARG(d == 64 || d == 128, "head_dim must be 64 or 128 for the sm_100a path");
   PSA_CHECK_ARG(levels >= 1 && levels <= 8, "levels must lie in 1..8");
   PSA_CHECK_ARG(b_k >= 1 && n % b_k == 0, "seq_len not divisible by k_block");
   PSA_CHECK_ARG(b_k % (1 << (levels - 1)) == 0, "k_block not divisible by 2^(levels-1)");
-  if (levels == 1) return PSA_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const bool gather = index != nullptr;
+  if (gather) PSA_CHECK_ARG(k1 && v1, "permuted level-1 outputs must be non-null");
+  if (levels == 1) {
+    if (!gather) return PSA_OK;
+    int rc = psa_gather_rows(k, bh, n, d * 2, index, k1, stream);
+    return rc ? rc : psa_gather_rows(v, bh, n, d * 2, index, v1, stream);
+  }
   PSA_CHECK_ARG(k_pyr && v_pyr, "pyramid output pointers must be non-null");
   const int logg = levels - 1;
   const int64_t rows = bh * n;
   const int64_t groups = rows >> logg;
   const int64_t threads = groups * (d / 4);
   dim3 grid(static_cast<unsigned>((threads + 255) / 256), 2);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
   auto* kk = static_cast<const uint16_t*>(k);
   auto* vv = static_cast<const uint16_t*>(v);
   auto* kp = static_cast<uint16_t*>(k_pyr);
   auto* vp = static_cast<uint16_t*>(v_pyr);
+  auto* k1p = static_cast<uint16_t*>(k1);
+  auto* v1p = static_cast<uint16_t*>(v1);
   switch (logg) {
-#define PSA_PYR_CASE(L)                                                                   \
-  case L:                                                                                 \
-    pyramid_kernel<L><<<grid, 256, 0, s>>>(kk, vv, groups, d, kp, vp, rows, nonfinite); \
+#define PSA_PYR_CASE(L)                                                                        \
+  case L:                                                                                      \
+    if (gather)                                                                                \
+      pyramid_kernel<L, true><<<grid, 256, 0, s>>>(kk, vv, groups, d, kp, vp, rows, nonfinite, \
+                                                   index, n, k1p, v1p);                         \
+    else                                                                                       \
+      pyramid_kernel<L, false><<<grid, 256, 0, s>>>(kk, vv, groups, d, kp, vp, rows,           \
+                                                    nonfinite, nullptr, n, nullptr, nullptr);   \
     break;
     PSA_PYR_CASE(1)
     PSA_PYR_CASE(2)
@@ -196,6 +226,22 @@ extern "C" int psa_pyramid_build(const void* k, const void* v, int64_t bh, int64
       return psa_fail(PSA_EINVAL, "unsupported level count");
   }
   return psa_check_launch("pyramid_kernel");
+}
+
+extern "C" int psa_pyramid_build(const void* k, const void* v, int64_t bh, int64_t n, int d,
+                                 int b_k, int levels, void* k_pyr, void* v_pyr,
+                                 int32_t* nonfinite, void* stream) {
+  return pyramid_launch(k, v, bh, n, d, b_k, levels, k_pyr, v_pyr, nonfinite, nullptr, nullptr,
+                        nullptr, stream);
+}
+
+extern "C" int psa_pyramid_build_gather(const void* k, const void* v, int64_t bh, int64_t n,
+                                        int d, int b_k, int levels, const int64_t* index,
+                                        void* k1, void* v1, void* k_pyr, void* v_pyr,
+                                        int32_t* nonfinite, void* stream) {
+  PSA_CHECK_ARG(index != nullptr, "index must be non-null");
+  return pyramid_launch(k, v, bh, n, d, b_k, levels, k_pyr, v_pyr, nonfinite, index, k1, v1,
+                        stream);
 }
 
 extern "C" int psa_similarity_caps(const void* k, int64_t bh, int64_t n, int d, int b_k,

@@ -26,7 +26,7 @@ from .layout import (PRESET_CUTPOINTS, LevelThresholds, QuantileCutpoints, Sampl
                      SimThresholds, make_layout)
 from .mask import MaskPlan, assign_levels_device
 from .permute import gather_rows, hilbert_order
-from .pyramid import PyramidKV, build_pyramid, similarity_caps
+from .pyramid import PyramidKV, build_pyramid, build_pyramid_gather, similarity_caps
 
 ESTIMATORS = ("sampled-max", "sampled-mean", "antidiagonal")
 MASK_STRATEGIES = ("threshold", "quantile", "binary") + tuple(PRESET_CUTPOINTS)
@@ -171,17 +171,19 @@ def psa_forward_4d(q4, k4, v4, cfg: RunConfig, keep_scores: bool = False,
     optional preallocated device outputs)."""
     lay = cfg.layout()
     lay.check_gpu()
-    perm = None
+    perm = order = None
     if cfg.grid is not None:  # pipeline.py:257-263: curve order applied to Q, K and V
         perm = _stage("permutation", hilbert_order, cfg.grid)
         order, _ = perm.on(q4.device)
-        q4, k4, v4 = (gather_rows(x, order) for x in (q4, k4, v4))
-        final_out, final_lse = out, lse
-        out = lse = None
+        q4 = gather_rows(q4, order)
+        # K/V: the gather is fused into the pyramid kernel's loads (level 1 = permuted K/V)
+        pyr = _stage("pyramid", build_pyramid_gather, k4, v4, lay, order)
+        k4, v4 = pyr.k_raw, pyr.v_raw
+    else:
+        pyr = _stage("pyramid", build_pyramid, k4, v4, lay)
     mode, rule = _mask_rule(cfg, lay.levels)
     B, Hq = q4.shape[:2]
     Hkv = k4.shape[1]
-    pyr = _stage("pyramid", build_pyramid, k4, v4, lay)
     if cfg.estimator == "antidiagonal":  # pipeline._estimate (pipeline.py:239-244)
         scores = _stage("importance", antidiagonal_scores, q4, k4, lay, cfg.stride)
     else:
@@ -193,20 +195,10 @@ def psa_forward_4d(q4, k4, v4, cfg: RunConfig, keep_scores: bool = False,
         caps = _stage("similarity-cap", similarity_caps, k4, lay, SimThresholds(cfg.sim_thresholds))
     plan = _stage("mask", assign_levels_device, scores, mode=mode, rule=rule, levels=lay.levels,
                   b_q=lay.q_block, b_k=lay.k_block, hkv=Hkv, caps=caps, causal=cfg.causal)
-    out, lse, skipped = _stage("executor", attention_forward, q4, pyr, plan, cfg.causal, out, lse)
-    if perm is not None:
-        if cfg.unpermute:  # pipeline.py:312-313: back to the caller's token order
-            _, inverse = perm.on(q4.device)
-            out = gather_rows(out, inverse, final_out)
-            lse = gather_rows(lse.unsqueeze(-1), inverse,
-                              None if final_lse is None else final_lse.unsqueeze(-1)).squeeze(-1)
-        else:
-            if final_out is not None:
-                final_out.copy_(out)
-                out = final_out
-            if final_lse is not None:
-                final_lse.copy_(lse)
-                lse = final_lse
+    # pipeline.py:312-313 (back to the caller's token order) fused into the attention epilogue
+    scatter = order if perm is not None and cfg.unpermute else None
+    out, lse, skipped = _stage("executor", attention_forward, q4, pyr, plan, cfg.causal, out, lse,
+                               None, scatter)
     return PSAResult(out=out, lse=lse, plan=plan, skipped=skipped,
                      scores=scores if keep_scores else None, pyramid=pyr)
 

@@ -101,6 +101,30 @@ def build_pyramid(k: torch.Tensor, v: torch.Tensor, layout: BlockLayout,
     return PyramidKV(layout, k4, v4, kp, vp)
 
 
+def build_pyramid_gather(k4: torch.Tensor, v4: torch.Tensor, layout: BlockLayout,
+                         index: torch.Tensor) -> PyramidKV:
+    """Pyramid of the token-permuted K/V (pipeline.py:257-263 then blocks.py:93-109) in one pass:
+    the permutation is a gather in the pyramid kernel's loads (psa_pyramid_build_gather). The
+    returned PyramidKV's level 1 (``k_raw``/``v_raw``) is the permuted K/V."""
+    layout.check_gpu()
+    if k4.shape != v4.shape or k4.dim() != 4 or not (k4.is_contiguous() and v4.is_contiguous()):
+        raise ValidationError("K/V must be contiguous [B, H, N, d] tensors of one shape")
+    B, H, n, d = k4.shape
+    if index.numel() != n or index.dtype != torch.int64 or index.device != k4.device:
+        raise ValidationError(f"permutation must be a device int64 tensor of {n} entries")
+    k1, v1 = torch.empty_like(k4), torch.empty_like(v4)
+    kp = vp = None
+    if layout.levels > 1:
+        total = pyramid_elems(B * H, n, d, layout.levels)
+        kp = torch.empty(total, dtype=torch.bfloat16, device=k4.device)
+        vp = torch.empty(total, dtype=torch.bfloat16, device=k4.device)
+    rc = _lib.load().psa_pyramid_build_gather(
+        k4.data_ptr(), v4.data_ptr(), B * H, n, d, layout.k_block, layout.levels, index.data_ptr(),
+        k1.data_ptr(), v1.data_ptr(), _lib.ptr(kp), _lib.ptr(vp), None, stream_handle(k4.device))
+    _lib.check(rc, "psa_pyramid_build_gather")
+    return PyramidKV(layout, k1, v1, kp, vp)
+
+
 def similarity_caps(k4: torch.Tensor, layout: BlockLayout, sim: SimThresholds) -> torch.Tensor:
     """int8 caps [B, Hkv, n_k] from raw keys (device)."""
     if len(sim) != layout.levels - 1:

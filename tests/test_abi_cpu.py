@@ -19,7 +19,8 @@ def test_header_declares_expected_entry_points():
     names = _declared()
     for n in ("psa_pyramid_build", "psa_similarity_caps", "psa_importance_sampled",
               "psa_importance_antidiagonal", "psa_antidiag_workspace_bytes", "psa_gather_rows",
-              "psa_assign_levels", "psa_mask_to_plan", "psa_attn_fwd", "psa_last_error"):
+              "psa_assign_levels", "psa_mask_to_plan", "psa_attn_fwd", "psa_last_error",
+              "psa_pyramid_build_gather", "psa_attn_fwd_scatter"):
         assert n in names
 
 

@@ -388,6 +388,40 @@ def test_apply_permutation_exact(grid, d):
     assert torch.equal(single.cpu().view(torch.int16), ref[0, 0].view(torch.int16))
 
 
+@pytest.mark.parametrize("grid,d,b,levels", [((16, 16, 16), 128, 64, 4), ((21, 45, 8), 128, 120, 4),
+                                             ((32, 32), 64, 64, 1), ((6, 10, 16), 128, 96, 3)])
+def test_fused_permutation_pyramid_and_scatter(grid, d, b, levels):
+    """The permutation fused into the pyramid loads (psa_pyramid_build_gather) equals gather then
+    build_pyramid bit for bit (level 1 = the permuted K/V); the attention epilogue's scatter
+    (psa_attn_fwd_scatter) equals attention then the inverse gather, bit for bit."""
+    from paper_2512_04025_b200.attention import attention_forward
+    from paper_2512_04025_b200.mask import plan_from_mask
+    from paper_2512_04025_b200.pyramid import build_pyramid_gather
+    psa = _psa()
+    n = int(np.prod(grid))
+    torch.manual_seed(3)
+    q, k, v = (torch.randn(1, 2, n, d, dtype=torch.bfloat16, device="cuda") for _ in range(3))
+    lay = psa.make_layout(n, d, b, b, levels)
+    p = psa.hilbert_order(grid)
+    order, inverse = p.on(q.device)
+    fused = build_pyramid_gather(k, v, lay, order)
+    kg, vg = psa.apply_permutation(k, p), psa.apply_permutation(v, p)
+    plain = psa.build_pyramid(kg, vg, lay)
+    bits = lambda t: t.view(torch.int16)  # noqa: E731
+    assert torch.equal(bits(fused.k_raw), bits(kg)) and torch.equal(bits(fused.v_raw), bits(vg))
+    if levels > 1:
+        assert torch.equal(bits(fused.k_pyr), bits(plain.k_pyr))
+        assert torch.equal(bits(fused.v_pyr), bits(plain.v_pyr))
+    qg = psa.apply_permutation(q, p)
+    rng = np.random.default_rng(5)
+    mask = torch.from_numpy(rng.integers(0, levels + 1, size=(1, 2, lay.n_q, lay.n_k))).cuda()
+    plan = plan_from_mask(mask, lay, False, 1, 2)
+    out, lse, _ = attention_forward(qg, plain, plan, False)
+    out_s, lse_s, _ = attention_forward(qg, fused, plan, False, out_rows=order)
+    assert torch.equal(bits(out_s), bits(psa.apply_permutation(out, psa.invert_permutation(p))))
+    assert torch.equal(lse_s, lse[:, :, inverse])
+
+
 # ------------------------------------------------------------------ block-tile schedule API
 @pytest.mark.parametrize("causal", [False, True])
 def test_execute_schedule_equals_streaming(causal, rng):
