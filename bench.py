@@ -450,7 +450,7 @@ def main():
                    "parallelism": f"heads sharded over {world} GPU(s)",
                    "l2": "inputs (Q/K/V 2.3 GB at cfg3) exceed the 126 MB L2; no flush needed"},
         "stage_ms": {k_: round(v_, 4) for k_, v_ in stage_ms.items()},
-        "roofline": {"bound": "tensor", "kernel": "psa_attn_fwd_kernel", "achieved": round(achieved, 2),
+        "roofline": {"bound": "tensor", "kernel": "psa_attn_pp2_kernel", "achieved": round(achieved, 2),
                      "peak": peak_sus, "unit": "TFLOP/s", "frac": round(achieved / peak_sus, 4),
                      "peak_note": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)",
                      "frac_of_burst": round(achieved / peak_burst, 4), "traffic": traffic},
