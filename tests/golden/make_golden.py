@@ -148,7 +148,25 @@ def pipeline_report_fixture():
                         out=res.output, report=np.array(json.dumps(rep, sort_keys=True)))
 
 
+def psat_fixture():
+    """PSAT files written by the reference (tensorfile.py:28-41): bytes and the arrays read back."""
+    import tempfile
+    rng = np.random.default_rng(41)
+    arrays = [rng.standard_normal(7), rng.standard_normal((3, 5)) * 1e3,
+              rng.standard_normal((2, 4, 3)), np.array([[1.0, -0.0], [1e-40, 3.0e38]])]
+    payload = {}
+    with tempfile.TemporaryDirectory() as td:
+        for i, a in enumerate(arrays):
+            path = Path(td) / f"t{i}.psat"
+            ref.write_tensor(path, a)
+            payload[f"in{i}"] = a
+            payload[f"bytes{i}"] = np.frombuffer(path.read_bytes(), dtype=np.uint8)
+            payload[f"read{i}"] = ref.read_tensor(path)
+    np.savez_compressed(HERE / "psat_files.npz", **payload)
+
+
 if __name__ == "__main__":
+    psat_fixture()
     pipeline_report_fixture()
     hilbert_fixture()
     schedule_fixture()

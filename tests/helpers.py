@@ -51,7 +51,7 @@ def bf16_bits(x: np.ndarray) -> np.ndarray:
 
 
 GOLDEN_DIR = __import__("pathlib").Path(__file__).resolve().parent / "golden"
-GOLDEN_CASES = sorted(p.stem for p in GOLDEN_DIR.glob("*.npz") if p.stem not in ("hilbert_orders", "schedules", "pipeline_report"))
+GOLDEN_CASES = sorted(p.stem for p in GOLDEN_DIR.glob("*.npz") if p.stem not in ("hilbert_orders", "schedules", "pipeline_report", "psat_files"))
 
 
 def load_golden(name: str) -> dict:
