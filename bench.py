@@ -320,14 +320,21 @@ def main():
     from paper_2512_04025_b200.pyramid import build_pyramid, similarity_caps
 
     _lib.load()
-    # strong scaling: the workload's query heads are split evenly; KV heads follow (GQA groups)
-    from paper_2512_04025_b200.parallel import shard_heads
+    # strong scaling: the workload's query heads are split evenly (balanced contiguous ranges);
+    # each rank reads the KV heads its query heads use and runs uniform-GQA segments
+    from paper_2512_04025_b200.parallel import shard_heads, shard_segments
     Hq, Hkv = cfg["Hq"], cfg["Hkv"]
     heads, kv_heads = shard_heads(Hq, Hkv, world, rank)
-    has_work = bool(heads)  # more ranks than KV heads: the extra ranks idle but keep the barriers
+    has_work = bool(heads)  # more ranks than query heads: the extra ranks idle but keep barriers
     if not has_work:
         heads, kv_heads = [0], [0]  # placeholder tensors, never launched
     q, k, v = make_inputs(cfg, heads, kv_heads, device)
+    segs = []  # (q, k, v) views/copies per uniform-GQA call
+    for q_lo, q_hi, kv_lo, kv_hi in (shard_segments(Hq, Hkv, world, rank) if has_work else []):
+        qa, ka = q_lo - heads[0], kv_lo - kv_heads[0]
+        segs.append(tuple(x.contiguous() for x in (q[:, qa:qa + q_hi - q_lo],
+                                                   k[:, ka:ka + kv_hi - kv_lo],
+                                                   v[:, ka:ka + kv_hi - kv_lo])))
     rc = run_config(cfg)
     lay = rc.layout()
     sampler = SamplerConfig(8, 8, 0)
@@ -335,7 +342,7 @@ def main():
     stream = torch.cuda.current_stream(device)
 
     stage_names = ("pyramid", "importance", "assign", "attention")
-    launches_per_step = 1 + 2 + 1 + 1 + (1 if cfg["sim"] else 0)
+    launches_per_step = (1 + 2 + 1 + 1 + (1 if cfg["sim"] else 0)) * max(1, len(segs))
     sim = SimThresholds(cfg["sim"]) if cfg["sim"] else None
 
     def step(events=None):
@@ -346,26 +353,29 @@ def main():
                     e.record(stream)
             return None, None
         if ev: ev[0].record(stream)
-        pyr = build_pyramid(k, v, lay)
-        caps = similarity_caps(k, lay, sim) if sim is not None else None
+        pyrs = [build_pyramid(ks, vs, lay) for _, ks, vs in segs]
+        capss = [similarity_caps(ks, lay, sim) if sim is not None else None for _, ks, _ in segs]
         if ev: ev[1].record(stream)
         if cfg["estimator"] == "antidiagonal":
-            scores = antidiagonal_scores(q, k, lay, cfg["stride"])
+            scores = [antidiagonal_scores(qs, ks, lay, cfg["stride"]) for qs, ks, _ in segs]
         else:
-            scores = importance_scores(q, k, lay, sampler, "max")
+            scores = [importance_scores(qs, ks, lay, sampler, "max") for qs, ks, _ in segs]
         if ev: ev[2].record(stream)
-        plan = assign_levels_device(scores, mode="threshold", rule=rule, levels=lay.levels,
-                                    b_q=lay.q_block, b_k=lay.k_block, hkv=k.shape[1],
-                                    caps=caps, causal=cfg["causal"])
+        plans = [assign_levels_device(sc, mode="threshold", rule=rule, levels=lay.levels,
+                                      b_q=lay.q_block, b_k=lay.k_block, hkv=ks.shape[1],
+                                      caps=cp, causal=cfg["causal"])
+                 for sc, (_, ks, _), cp in zip(scores, segs, capss)]
         if ev: ev[3].record(stream)
-        out, lse, skipped = attention_forward(q, pyr, plan, cfg["causal"])
+        outs = [attention_forward(qs, pyr, plan, cfg["causal"])[0]
+                for (qs, _, _), pyr, plan in zip(segs, pyrs, plans)]
         if ev: ev[4].record(stream)
-        return plan, out
+        return plans, outs
 
     for _ in range(max(args.warmup, 3)):
-        plan, _ = step()
+        plans, _ = step()
     torch.cuda.synchronize()
-    counts = plan.level_counts.cpu().tolist() if has_work else [0] * (lay.levels + 1)
+    counts = (sum(p_.level_counts for p_ in plans).cpu().tolist() if has_work
+              else [0] * (lay.levels + 1))
     flops_local = flops_from_counts(counts, cfg, cfg["B"] * len(heads)) if has_work else 0
     if world > 1:  # whole-job level histogram
         ct = torch.tensor(counts, dtype=torch.int64, device=red_dev)
@@ -406,7 +416,7 @@ def main():
     # ---- end-to-end through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(psa, rc, q, k, v, args, stream, flops_all, world, device, has_work, red_dev)
+        e2e = run_e2e(psa, rc, segs, args, stream, flops_all, world, device, has_work, red_dev)
 
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
         if (ROOT / "MEASURED_PEAKS.json").exists() else {}
@@ -447,7 +457,7 @@ def main():
                    "mask": f"threshold taus={[round(t, 6) for t in cfg['taus']]}",
                    "rho_bar": rho_bar, "level_counts": counts, "causal": cfg["causal"],
                    "executed_tflop_per_step": flops_all / 1e12,
-                   "parallelism": f"heads sharded over {world} GPU(s)",
+                   "parallelism": f"query heads sharded over {world} GPU(s) (balanced ranges)",
                    "l2": "inputs (Q/K/V 2.3 GB at cfg3) exceed the 126 MB L2; no flush needed"},
         "stage_ms": {k_: round(v_, 4) for k_, v_ in stage_ms.items()},
         "roofline": {"bound": "tensor", "kernel": "psa_attn_pp2_kernel", "achieved": round(achieved, 2),
@@ -562,7 +572,7 @@ def main_sweep(args, cfg, rank, world, device, red_dev):
         dist.destroy_process_group()
 
 
-def run_e2e(psa, rc, q, k, v, args, stream, flops_all, world, device, has_work=True,
+def run_e2e(psa, rc, segs, args, stream, flops_all, world, device, has_work=True,
             red_dev=None):
     """Same metric through the public call a user makes with host data: psa.psa_attention on
     pinned host Q/K/V returns O and lse in pinned host memory. Every timed step includes the H2D
@@ -570,17 +580,16 @@ def run_e2e(psa, rc, q, k, v, args, stream, flops_all, world, device, has_work=T
     copy-out streams, staging.py)."""
     import torch
     import torch.distributed as dist
-    hq, hk, hv = (x.cpu().pin_memory() for x in (q, k, v))
-    out_h = torch.empty(q.shape, dtype=torch.bfloat16).pin_memory()
-    lse_h = torch.empty(q.shape[:-1], dtype=torch.float32).pin_memory()
+    host = [tuple(x.cpu().pin_memory() for x in sg) for sg in segs]
+    outs = [(torch.empty(hq.shape, dtype=torch.bfloat16).pin_memory(),
+             torch.empty(hq.shape[:-1], dtype=torch.float32).pin_memory()) for hq, _, _ in host]
 
     per_group = int(os.environ["PSA_E2E_GROUP"]) if os.environ.get("PSA_E2E_GROUP") else None
 
     def one():
-        if not has_work:
-            return None
-        return psa.psa_attention(hq, hk, hv, rc, device=device, out=out_h, lse=lse_h,
-                                 kv_heads_per_group=per_group)
+        for (hq, hk, hv), (out_h, lse_h) in zip(host, outs):
+            psa.psa_attention(hq, hk, hv, rc, device=device, out=out_h, lse=lse_h,
+                              kv_heads_per_group=per_group)
 
     for _ in range(2):
         one()
@@ -602,10 +611,11 @@ def run_e2e(psa, rc, q, k, v, args, stream, flops_all, world, device, has_work=T
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t[0])
     # PCIe floor of the same step: the H2D of Q/K/V alone (pinned, one stream)
-    dq = [torch.empty_like(x, device=device) for x in (hq, hk, hv)]
+    srcs = [x for sg in host for x in sg]
+    dq = [torch.empty_like(x, device=device) for x in srcs]
     a.record(stream)
     for _ in range(steps):
-        for dst, src in zip(dq, (hq, hk, hv)):
+        for dst, src in zip(dq, srcs):
             dst.copy_(src, non_blocking=True)
     b.record(stream)
     torch.cuda.synchronize()
@@ -615,9 +625,9 @@ def run_e2e(psa, rc, q, k, v, args, stream, flops_all, world, device, has_work=T
             "h2d_only_ms": round(h2d_ms, 3),
             "ms_per_step": round(ms, 3), "host_wall_ms_per_step": round(wall, 3), "steps": steps,
             "api": "psa_attention(pinned host q, k, v) -> host out, lse (staged H2D/compute/D2H)",
-            "h2d_bytes_per_step": int(sum(x.numel() * x.element_size() for x in (hq, hk, hv))),
-            "d2h_bytes_per_step": int(out_h.numel() * out_h.element_size()
-                                      + lse_h.numel() * lse_h.element_size())}
+            "h2d_bytes_per_step": int(sum(x.numel() * x.element_size() for x in srcs)),
+            "d2h_bytes_per_step": int(sum(o.numel() * o.element_size() + l_.numel() * l_.element_size()
+                                          for o, l_ in outs))}
 
 
 def main_reference(args, cfg, rank, world, device):

@@ -13,15 +13,28 @@ from paper_2512_04025_b200.parallel import gather_outputs, shard_heads
 
 
 @pytest.mark.parametrize("hq,hkv,world", [(40, 40, 8), (12, 12, 8), (28, 4, 8), (28, 4, 3),
-                                          (2, 2, 2), (40, 40, 1)])
+                                          (2, 2, 2), (40, 40, 1), (6, 3, 4), (28, 4, 5)])
 def test_shards_partition_heads(hq, hkv, world):
-    seen_q, seen_kv = [], []
+    """Every query head on exactly one rank, ranks balanced to within one head, each rank reads
+    the KV heads of its query heads, and its segments are uniform-GQA calls covering its range."""
+    from paper_2512_04025_b200.parallel import shard_segments
+    group = hq // hkv
+    seen_q, seen_kv, sizes = [], set(), []
     for r in range(world):
         q, kv = shard_heads(hq, hkv, world, r)
         seen_q += q
-        seen_kv += kv
-        assert all(h // (hq // hkv) in kv for h in q)
-    assert sorted(seen_q) == list(range(hq)) and sorted(seen_kv) == list(range(hkv))
+        seen_kv |= set(kv)
+        sizes.append(len(q))
+        assert all(h // group in kv for h in q)
+        covered = []
+        for q_lo, q_hi, kv_lo, kv_hi in shard_segments(hq, hkv, world, r):
+            g = (q_hi - q_lo) // (kv_hi - kv_lo)
+            assert g * (kv_hi - kv_lo) == q_hi - q_lo
+            assert all(h // group == kv_lo + (h - q_lo) // g for h in range(q_lo, q_hi))
+            covered += list(range(q_lo, q_hi))
+        assert covered == q
+    assert sorted(seen_q) == list(range(hq)) and seen_kv == set(range(hkv))
+    assert max(sizes) - min(sizes) <= 1
 
 
 def _free_port():
