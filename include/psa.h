@@ -173,6 +173,20 @@ int psa_attn_fwd_scatter(const void* q, const void* k, const void* v, const void
                          int32_t* skipped_rows, const int64_t* out_rows, void* stream);
 
 /*
+ * Backward of psa_attn_fwd for a fixed mask (the reference has none).
+ * Inputs: the forward's Q, K, V, pyramid, O (out), lse and plan, the level map (int8
+ * [batch, hq, n_q, n_k]) and dO (dout, bf16 like O).  Outputs dq [batch, hq, n, d] and dk, dv
+ * [batch, hkv, n, d] (bf16, gradients w.r.t. the RAW K/V: pooled levels are differentiated
+ * through their means).  workspace: psa_attn_bwd_workspace_bytes(batch, hq, n) bytes.
+ */
+size_t psa_attn_bwd_workspace_bytes(int64_t batch, int hq, int64_t n);
+int psa_attn_bwd(const void* q, const void* k, const void* v, const void* k_pyr,
+                 const void* v_pyr, const void* out, const void* dout, const float* lse,
+                 int64_t batch, int hq, int hkv, int64_t n, int d, int b_q, int b_k, int levels,
+                 const uint16_t* plan_csr, const int32_t* plan_info, const int8_t* level_map,
+                 int causal, void* dq, void* dk, void* dv, void* workspace, void* stream);
+
+/*
  * Token permutation.  Replaces apply_permutation (pkg/src/pyrattn/permute.py:131-137) for the
  * space-filling-curve reorder of pipeline._run_head (pipeline.py:257-263, unpermute :312-313):
  * dst[b][i] = src[b][index[i]] for b < bh, i < n; rows of row_bytes bytes (multiple of 4).

@@ -19,6 +19,7 @@ from .permute import Permutation, apply_permutation, hilbert_order, invert_permu
 from .pipeline import (PipelineResult, PSAResult, RunConfig, psa_attention, psa_forward_4d,
                        relative_error, report_to_json, run_pipeline)
 from .pyramid import PyramidKV, build_pyramid, build_pyramid_gather, level_cap_from_similarity
+from .autograd import psa_attention_differentiable
 from .tensorfile import read_tensor, write_tensor
 from .schedule import (ExecutionTile, Segment, TileSchedule, UtilizationStats, build_schedule,
                        execute_schedule, plan_utilization, utilization)
@@ -38,5 +39,5 @@ __all__ = [
     "antidiagonal_selection", "importance_antidiagonal", "importance_sampled", "level_bias",
     "level_cap_from_similarity", "make_layout",
     "psa_attention", "psa_forward_4d", "psa_streaming", "report_from_counts", "sample_tables",
-    "sparsity_report", "read_tensor", "write_tensor",
+    "sparsity_report", "read_tensor", "write_tensor", "psa_attention_differentiable",
 ]

@@ -17,7 +17,7 @@ CSRC = PKG / "csrc"
 BUILD = PKG / "build"
 LIB = PKG / "libpsa.so"
 SOURCES = ["psa_abi.cu", "psa_pyramid.cu", "psa_importance.cu", "psa_assign.cu",
-           "psa_attention.cu", "psa_xlogits.cu", "psa_permute.cu"]
+           "psa_attention.cu", "psa_xlogits.cu", "psa_permute.cu", "psa_backward.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",

@@ -70,6 +70,32 @@ def attention_forward(q4: torch.Tensor, pyr: PyramidKV, plan: MaskPlan, causal: 
     return out, lse, skipped
 
 
+def attention_backward(q4: torch.Tensor, pyr: PyramidKV, plan: MaskPlan, causal: bool,
+                       out: torch.Tensor, lse: torch.Tensor, dout: torch.Tensor):
+    """Gradients (dq, dk, dv) of attention_forward for the fixed mask ``plan`` (psa_attn_bwd):
+    dk/dv are w.r.t. the raw K/V of ``pyr`` (pooled levels differentiated through their means)."""
+    lay = pyr.layout
+    B, Hq, n, d = q4.shape
+    Hkv = pyr.k_raw.shape[1]
+    dev = q4.device
+    dout = dout.to(torch.bfloat16).contiguous()
+    if dout.shape != q4.shape or out.shape != q4.shape or lse.shape != q4.shape[:-1]:
+        raise ValidationError("out / lse / dout shapes do not match q")
+    dq = torch.empty_like(q4)
+    dk = torch.empty_like(pyr.k_raw)
+    dv = torch.empty_like(pyr.v_raw)
+    lib = _lib.load()
+    ws = torch.empty(lib.psa_attn_bwd_workspace_bytes(B, Hq, n), dtype=torch.uint8, device=dev)
+    rc = lib.psa_attn_bwd(
+        q4.data_ptr(), pyr.k_raw.data_ptr(), pyr.v_raw.data_ptr(), _lib.ptr(pyr.k_pyr),
+        _lib.ptr(pyr.v_pyr), out.data_ptr(), dout.data_ptr(), lse.data_ptr(), B, Hq, Hkv, n, d,
+        lay.q_block, lay.k_block, lay.levels, plan.csr.data_ptr(), plan.info.data_ptr(),
+        plan.level_map.data_ptr(), int(causal), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
+        ws.data_ptr(), stream_handle(dev))
+    _lib.check(rc, "psa_attn_bwd")
+    return dq, dk, dv
+
+
 def psa_streaming(q, pyramid: PyramidKV, mask, causal: bool = False) -> AttentionOutput:
     """Multi-level attention over the mask-selected (block, level) pairs (attention.py:171-218).
 
