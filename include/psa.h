@@ -177,9 +177,9 @@ int psa_attn_fwd_scatter(const void* q, const void* k, const void* v, const void
  * Inputs: the forward's Q, K, V, pyramid, O (out), lse and plan, the level map (int8
  * [batch, hq, n_q, n_k]) and dO (dout, bf16 like O).  Outputs dq [batch, hq, n, d] and dk, dv
  * [batch, hkv, n, d] (bf16, gradients w.r.t. the RAW K/V: pooled levels are differentiated
- * through their means).  workspace: psa_attn_bwd_workspace_bytes(batch, hq, n) bytes.
+ * through their means).  workspace: psa_attn_bwd_workspace_bytes(batch, hq, hkv, n, d) bytes.
  */
-size_t psa_attn_bwd_workspace_bytes(int64_t batch, int hq, int64_t n);
+size_t psa_attn_bwd_workspace_bytes(int64_t batch, int hq, int hkv, int64_t n, int d);
 int psa_attn_bwd(const void* q, const void* k, const void* v, const void* k_pyr,
                  const void* v_pyr, const void* out, const void* dout, const float* lse,
                  int64_t batch, int hq, int hkv, int64_t n, int d, int b_q, int b_k, int levels,

@@ -47,7 +47,7 @@ _SIGNATURES = {
                                      c_int, c_int, c_int64, c_int, c_int, c_int, c_int, c_void_p,
                                      c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
                                      c_void_p]),
-    "psa_attn_bwd_workspace_bytes": (c_size_t, [c_int64, c_int, c_int64]),
+    "psa_attn_bwd_workspace_bytes": (c_size_t, [c_int64, c_int, c_int, c_int64, c_int]),
     "psa_attn_bwd": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                              c_void_p, c_int64, c_int, c_int, c_int64, c_int, c_int, c_int, c_int,
                              c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p,

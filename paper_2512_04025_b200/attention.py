@@ -85,7 +85,7 @@ def attention_backward(q4: torch.Tensor, pyr: PyramidKV, plan: MaskPlan, causal:
     dk = torch.empty_like(pyr.k_raw)
     dv = torch.empty_like(pyr.v_raw)
     lib = _lib.load()
-    ws = torch.empty(lib.psa_attn_bwd_workspace_bytes(B, Hq, n), dtype=torch.uint8, device=dev)
+    ws = torch.empty(lib.psa_attn_bwd_workspace_bytes(B, Hq, Hkv, n, d), dtype=torch.uint8, device=dev)
     rc = lib.psa_attn_bwd(
         q4.data_ptr(), pyr.k_raw.data_ptr(), pyr.v_raw.data_ptr(), _lib.ptr(pyr.k_pyr),
         _lib.ptr(pyr.v_pyr), out.data_ptr(), dout.data_ptr(), lse.data_ptr(), B, Hq, Hkv, n, d,

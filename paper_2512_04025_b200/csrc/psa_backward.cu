@@ -12,9 +12,15 @@
 // over (query block, expanded KV block) pairs, and dK/dV land directly on raw rows; the pyramid
 // needs no transpose. With the mask fixed, importance and level assignment carry no gradient.
 //
+// The identity is applied at pooled granularity: the kernels compute with the L_h = b_k >> (h-1)
+// pooled rows (unbiased weights p' = p / 2^(h-1) for dK/dV, biased p for dQ) and only the final
+// add spreads a pooled row's gradient over its 2^(h-1) raw rows, so the work per selected block
+// scales with its pooled length like the forward's.
+//
 // First version: warp-level mma.sync (m16n8k16 bf16, fp32 accumulate) with ldmatrix fragments,
-// one CTA per (head, query block) for dQ and one per (KV head, KV block) for dK/dV; FLOPs per
-// selected block are those of a level-1 block (the expansion is not exploited).
+// one CTA per (head, query block) for dQ and one per (KV head, KV block) for dK/dV (8 warps,
+// 1 CTA per SM at ~230-255 registers); cfg3 backward 916 ms (dQ 361 ms, dK/dV 555 ms) against a
+// 36 ms forward. The tcgen05 / TMEM version is the next step.
 #include "common.cuh"
 #include "psa_internal.h"
 
@@ -113,17 +119,24 @@ __global__ void __launch_bounds__(256) bwd_drow_kernel(const uint16_t* __restric
 }
 
 // ---------------------------------------------------------------------------------------- dQ
-// One CTA per (head, query block). Warp w owns query rows 16w..16w+15; per selected block the
-// expanded K/V tile is staged in shared memory and walked in 64-key chunks:
-//   S = Q K^T, P = exp2(S c - lse2), dP = dO V^T, dS = P (dP - D), dQ += dS K.
+// One CTA per (head, query block); warp w owns query rows 16w..16w+15. The unit's selected
+// pooled blocks (level-major plan order) are packed back to back into 64-key chunks staged in
+// shared memory (a level-4 block is 15 rows, so several blocks share a chunk):
+//   S = Q K^T, P = exp2(S c + (h-1) - lse2), dP = dO V^T, dS = P (dP - D), dQ += dS K.
+// P carries the level bias here: dq = scale * sum_j ds_j k_j over POOLED keys.
+constexpr int kChunkKeys = 64;
+
 template <int D>
 __global__ void __launch_bounds__(kBwdThreads, 1) bwd_dq_kernel(const BwdParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   using T = BwdTile<D>;
   uint16_t* qs = reinterpret_cast<uint16_t*>(smem_raw);
   uint16_t* ds = qs + kBwdRows * T::kStride;
-  uint16_t* ks = ds + kBwdRows * T::kStride;
-  uint16_t* vs = ks + kBwdRows * T::kStride;
+  uint16_t* ks = ds + kBwdRows * T::kStride;  // kChunkKeys rows used
+  uint16_t* vs = ks + kChunkKeys * T::kStride;
+  int* ent_off = reinterpret_cast<int*>(vs + kChunkKeys * T::kStride);  // [n_k + 1] pooled-row prefix
+  float* cbias = reinterpret_cast<float*>(ent_off + p.n_k + 1);         // [kChunkKeys]
+  int* ckpos = reinterpret_cast<int*>(cbias + kChunkKeys);              // [kChunkKeys]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t unit = blockIdx.x;
   const int bhq = static_cast<int>(unit / p.n_q), i = static_cast<int>(unit % p.n_q);
@@ -131,10 +144,18 @@ __global__ void __launch_bounds__(kBwdThreads, 1) bwd_dq_kernel(const BwdParams 
   const int64_t bkv = static_cast<int64_t>(b) * p.hkv + hh / (p.hq / p.hkv);
   const int64_t row0 = static_cast<int64_t>(bhq) * p.n + static_cast<int64_t>(i) * p.b_q;
   const int n_ent = p.info[unit * 2];
+  const uint16_t* csr = p.csr + unit * p.n_k;
 
   load_tile<D>(qs, p.q + row0 * D, p.b_q, 0);
   load_tile<D>(ds, p.dout + row0 * D, p.b_q, 0);
-  // this thread's two rows (accumulator layout) and their softmax statistics
+  if (threadIdx.x == 0) {  // prefix of pooled rows over the unit's entries
+    int acc = 0;
+    for (int e = 0; e < n_ent; ++e) {
+      ent_off[e] = acc;
+      acc += p.b_k >> ((csr[e] >> 12) - 1);
+    }
+    ent_off[n_ent] = acc;
+  }
   const int ra = warp * 16 + (lane >> 2), rb = ra + 8;
   const float kLog2e = 1.4426950408889634f;
   float lse2[2], dd[2];
@@ -151,35 +172,62 @@ __global__ void __launch_bounds__(kBwdThreads, 1) bwd_dq_kernel(const BwdParams 
 #pragma unroll
   for (int t = 0; t < D / 8; ++t) dqa[t][0] = dqa[t][1] = dqa[t][2] = dqa[t][3] = 0.f;
   const uint32_t qs_a = smem_u32(qs), ds_a = smem_u32(ds), ks_a = smem_u32(ks), vs_a = smem_u32(vs);
-  // A-fragment addresses (rows of this warp) and B-fragment lane offsets
   const uint32_t a_off = ((warp * 16 + (lane & 15)) * T::kStride + (lane >> 4) * 8) * 2;
   const int bn = (lane & 7) + ((lane >> 4) << 3), bk = ((lane >> 3) & 1) * 8;   // [n][k] memory
   const int tk = (lane & 7) + (((lane >> 3) & 1) << 3), tn = (lane >> 4) << 3;  // [k][n] memory
   const int64_t qpos0 = static_cast<int64_t>(i) * p.b_q;
+  __syncthreads();
+  const int total = ent_off[n_ent];
 
-  for (int e = 0; e < n_ent; ++e) {
-    const uint32_t ent = p.csr[unit * p.n_k + e];
-    const int j = static_cast<int>(ent & 0xFFFu), h = static_cast<int>(ent >> 12);
+  for (int base = 0; base < total; base += kChunkKeys) {
+    const int nk = min(kChunkKeys, total - base);
+    __syncthreads();  // previous chunk fully consumed
+    // stage the chunk: key row c <- pooled row (e, t) with base + c = ent_off[e] + t
+    constexpr int kVec = D / 8;
+    for (int x = threadIdx.x; x < kChunkKeys * kVec; x += kBwdThreads) {
+      const int c = x / kVec, col = (x % kVec) * 8;
+      uint4 kv4 = make_uint4(0u, 0u, 0u, 0u), vv4 = kv4;
+      if (c < nk) {
+        const int g = base + c;
+        int lo = 0, hi = n_ent - 1;  // last entry with ent_off[e] <= g
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (ent_off[mid] <= g) lo = mid; else hi = mid - 1;
+        }
+        const uint32_t ent = csr[lo];
+        const int j = static_cast<int>(ent & 0xFFFu), h = static_cast<int>(ent >> 12);
+        const int t = g - ent_off[lo];
+        const int64_t src = static_cast<int64_t>(t) * D + col;
+        kv4 = *reinterpret_cast<const uint4*>(level_block(p.k, p.k_pyr, p.bkv_total, bkv, p.n, D, p.b_k, h, j) + src);
+        vv4 = *reinterpret_cast<const uint4*>(level_block(p.v, p.v_pyr, p.bkv_total, bkv, p.n, D, p.b_k, h, j) + src);
+        if (col == 0) {
+          cbias[c] = static_cast<float>(h - 1);
+          ckpos[c] = h == 1 ? j * p.b_k + t : -1;  // pooled levels never straddle (causal premask)
+        }
+      } else if (col == 0) {
+        cbias[c] = -INFINITY;
+        ckpos[c] = -1;
+      }
+      *reinterpret_cast<uint4*>(ks + c * T::kStride + col) = kv4;
+      *reinterpret_cast<uint4*>(vs + c * T::kStride + col) = vv4;
+    }
     __syncthreads();
-    load_tile<D>(ks, level_block(p.k, p.k_pyr, p.bkv_total, bkv, p.n, D, p.b_k, h, j), p.b_k, h - 1);
-    load_tile<D>(vs, level_block(p.v, p.v_pyr, p.bkv_total, bkv, p.n, D, p.b_k, h, j), p.b_k, h - 1);
-    __syncthreads();
-    const bool straddle = p.causal && (static_cast<int64_t>(j + 1) * p.b_k - 1 > qpos0);
-    for (int kc = 0; kc < p.b_k; kc += 64) {
-      float s[8][4], dp[8][4];
+    const int nt16 = (nk + 15) >> 4;  // 16-key tiles holding keys
+    float s[8][4], dp[8][4];
 #pragma unroll
-      for (int t = 0; t < 8; ++t)
+    for (int t = 0; t < 8; ++t)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) s[t][c] = dp[t][c] = 0.f;
+      for (int c = 0; c < 4; ++c) s[t][c] = dp[t][c] = 0.f;
 #pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk) {
-        uint32_t qa[4], da[4];
-        ldsm4(qa, qs_a + a_off + kk * 32);
-        ldsm4(da, ds_a + a_off + kk * 32);
+    for (int kk = 0; kk < D / 16; ++kk) {
+      uint32_t qa[4], da[4];
+      ldsm4(qa, qs_a + a_off + kk * 32);
+      ldsm4(da, ds_a + a_off + kk * 32);
 #pragma unroll
-        for (int t2 = 0; t2 < 4; ++t2) {  // two 8-key n-tiles per ldmatrix.x4
+      for (int t2 = 0; t2 < 4; ++t2) {
+        if (t2 < nt16) {
           uint32_t kb[4], vb[4];
-          const uint32_t off = ((kc + t2 * 16 + bn) * T::kStride + kk * 16 + bk) * 2;
+          const uint32_t off = ((t2 * 16 + bn) * T::kStride + kk * 16 + bk) * 2;
           ldsm4(kb, ks_a + off);
           ldsm4(vb, vs_a + off);
           mma16816(s[2 * t2], qa, kb[0], kb[1]);
@@ -188,39 +236,39 @@ __global__ void __launch_bounds__(kBwdThreads, 1) bwd_dq_kernel(const BwdParams 
           mma16816(dp[2 * t2 + 1], da, vb[2], vb[3]);
         }
       }
-      // P and dS (fp32), then dS as bf16 A fragments (16 rows x 64 keys)
-      uint32_t dsa[4][4];
+    }
+    uint32_t dsa[4][4];
 #pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        float v4[4];
+    for (int t = 0; t < 8; ++t) {
+      float v4[4];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int u = c >> 1;
-          const int key = kc + t * 8 + 2 * (lane & 3) + (c & 1);
-          const int64_t kpos = static_cast<int64_t>(j) * p.b_k + key;
-          const int64_t qpos = qpos0 + (u ? rb : ra);
-          const bool ok = live[u] && key < p.b_k && !(straddle && kpos > qpos);
-          const float pr = ok ? exp2f(fmaf(s[t][c], p.scale_log2, -lse2[u])) : 0.f;
-          v4[c] = pr * (dp[t][c] - dd[u]);
-        }
-        dsa[t >> 1][(t & 1) * 2 + 0] = pack_bf16x2(v4[0], v4[1]);
-        dsa[t >> 1][(t & 1) * 2 + 1] = pack_bf16x2(v4[2], v4[3]);
+      for (int c = 0; c < 4; ++c) {
+        const int u = c >> 1;
+        const int key = t * 8 + 2 * (lane & 3) + (c & 1);
+        const float bias = cbias[key];
+        const int kp = ckpos[key];
+        const int64_t qpos = qpos0 + (u ? rb : ra);
+        const bool ok = live[u] && bias != -INFINITY && !(p.causal && kp >= 0 && kp > qpos);
+        const float pr = ok ? exp2f(fmaf(s[t][c], p.scale_log2, bias - lse2[u])) : 0.f;
+        v4[c] = pr * (dp[t][c] - dd[u]);
       }
-      // dQ += dS (16 x 64) K (64 x D): K rows are the k dimension -> transposed ldmatrix
+      dsa[t >> 1][(t & 1) * 2 + 0] = pack_bf16x2(v4[0], v4[1]);
+      dsa[t >> 1][(t & 1) * 2 + 1] = pack_bf16x2(v4[2], v4[3]);
+    }
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
+    for (int kk = 0; kk < 4; ++kk) {
+      if (kk < nt16) {
         const uint32_t a[4] = {dsa[kk][0], dsa[kk][1], dsa[kk][2], dsa[kk][3]};
 #pragma unroll
         for (int t2 = 0; t2 < D / 16; ++t2) {
           uint32_t kb[4];
-          ldsm4t(kb, ks_a + ((kc + kk * 16 + tk) * T::kStride + t2 * 16 + tn) * 2);
+          ldsm4t(kb, ks_a + ((kk * 16 + tk) * T::kStride + t2 * 16 + tn) * 2);
           mma16816(dqa[2 * t2], a, kb[0], kb[1]);
           mma16816(dqa[2 * t2 + 1], a, kb[2], kb[3]);
         }
       }
     }
   }
-  // dQ = scale * acc -> bf16
 #pragma unroll
   for (int t = 0; t < D / 8; ++t) {
     const int c = t * 8 + 2 * (lane & 3);
@@ -234,33 +282,43 @@ __global__ void __launch_bounds__(kBwdThreads, 1) bwd_dq_kernel(const BwdParams 
 }
 
 // ------------------------------------------------------------------------------------ dK, dV
-// One CTA per (KV head, KV block j). The CTA first lists, level-major and in (query head,
-// query block) order, every (q head of the GQA group, query block) that selected block j, then
-// per level stages the expanded K/V tile and per listed query block recomputes the transposed
-// scores: S^T = K Q^T, P^T, dP^T = V dO^T, dS^T = P^T (dP^T - D); dV += P^T dO, dK += dS^T Q.
-// Warp w owns raw key rows 16w..16w+15; dK/dV accumulate in registers across all entries.
+// One CTA per (KV head, KV block j). The CTA lists, level-major and in (query head, query
+// block) order, every (q head of the GQA group, query block) that selected block j. Per level h
+// the POOLED block (L_h = b_k >> (h-1) rows, R = pow2(ceil(L_h / 16)) row tiles) is staged once;
+// warp w takes row tile w % R and the query slice (w / R) of every listed query block, so all 8
+// warps work at every level. Per listed query block (pooled, unbiased weights p' = p / 2^(h-1)):
+//   S^T = K Q^T, P'^T = exp2(S^T c - lse2), dP^T = V dO^T, dS^T = P'^T (dP^T - D),
+//   dV_h += P'^T dO, dK_h += dS^T Q.
+// A raw row r of block j receives the pooled gradients of row r >> (h-1) of every level, i.e.
+// the duplicate's gradient (file header). At the end of a level the warps' partials are summed
+// in shared memory and added to the CTA's raw rows in an fp32 scratch (exclusive to this CTA);
+// the last step writes bf16 dK (x scale) and dV.
 template <int D>
-__global__ void __launch_bounds__(kBwdThreads, 1) bwd_dkv_kernel(const BwdParams p, int cap) {
+__global__ void __launch_bounds__(kBwdThreads, 1) bwd_dkv_kernel(const BwdParams p, int cap,
+                                                                float* __restrict__ scratch) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   using T = BwdTile<D>;
   uint16_t* qs = reinterpret_cast<uint16_t*>(smem_raw);
   uint16_t* ds = qs + kBwdRows * T::kStride;
   uint16_t* ks = ds + kBwdRows * T::kStride;
   uint16_t* vs = ks + kBwdRows * T::kStride;
+  float* part = reinterpret_cast<float*>(smem_raw);  // level-end reduction (aliases the tiles)
   float* lse_s = reinterpret_cast<float*>(vs + kBwdRows * T::kStride);
   float* d_s = lse_s + kBwdRows;
   uint32_t* ents = reinterpret_cast<uint32_t*>(d_s + kBwdRows);
   __shared__ int warp_cnt[kBwdThreads / 32];
+  static_assert(2 * 8 * 16 * D * 4 <= 4 * BwdTile<D>::kBytes, "partials must fit in the tiles");
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int j = blockIdx.x;
   const int64_t bkv = blockIdx.y;
   const int b = static_cast<int>(bkv / p.hkv), hk = static_cast<int>(bkv % p.hkv);
   const int group = p.hq / p.hkv;
-  const int span = group * p.n_q;  // (q head of the group, query block) index space
+  const int span = group * p.n_q;
 
   // ---- deterministic level-major compaction of the entries selecting block j
   int total = 0;
+  int lvl_end[9];
   for (int h = 1; h <= p.levels; ++h) {
     for (int base = 0; base < span; base += kBwdThreads) {
       const int x = base + threadIdx.x;
@@ -280,128 +338,170 @@ __global__ void __launch_bounds__(kBwdThreads, 1) bwd_dkv_kernel(const BwdParams
       }
       if (hit) {
         const int slot = total + before + __popc(m & ((1u << lane) - 1u));
-        if (slot < cap) ents[slot] = (static_cast<uint32_t>(x) << 4) | static_cast<uint32_t>(h);
+        if (slot < cap) ents[slot] = static_cast<uint32_t>(x);
       }
       total += all;
       __syncthreads();
     }
+    lvl_end[h] = min(total, cap);
   }
-  const int n_ent = min(total, cap);  // each (q head, query block) holds one level: total <= cap
 
-  const int ra = warp * 16 + (lane >> 2);  // this thread's accumulator rows ra, ra + 8 (keys)
-  float dka[D / 8][4], dva[D / 8][4];
-#pragma unroll
-  for (int t = 0; t < D / 8; ++t)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) dka[t][c] = dva[t][c] = 0.f;
+  const int64_t krow0 = bkv * p.n + static_cast<int64_t>(j) * p.b_k;
+  float* sk = scratch + krow0 * D;                        // dK rows of block j (fp32)
+  float* sv = scratch + (p.bkv_total * p.n + krow0) * D;  // dV rows
   const uint32_t qs_a = smem_u32(qs), ds_a = smem_u32(ds), ks_a = smem_u32(ks), vs_a = smem_u32(vs);
-  const uint32_t a_off = ((warp * 16 + (lane & 15)) * T::kStride + (lane >> 4) * 8) * 2;
   const int bn = (lane & 7) + ((lane >> 4) << 3), bk = ((lane >> 3) & 1) * 8;
   const int tk = (lane & 7) + (((lane >> 3) & 1) << 3), tn = (lane >> 4) << 3;
   const float kLog2e = 1.4426950408889634f;
+  bool first = true;
 
-  int cur_h = 0;
-  for (int e = 0; e < n_ent; ++e) {
-    const uint32_t ent = ents[e];
-    const int h = static_cast<int>(ent & 15u);
-    const int x = static_cast<int>(ent >> 4);
-    const int g = x / p.n_q, iq = x % p.n_q;
-    const int64_t bhq = static_cast<int64_t>(b) * p.hq + hk * group + g;
-    const int64_t row0 = bhq * p.n + static_cast<int64_t>(iq) * p.b_q;
+  int e0 = 0;
+  for (int h = 1; h <= p.levels; ++h) {
+    const int e1 = lvl_end[h];
+    if (e1 == e0) continue;
+    const int L = p.b_k >> (h - 1);
+    int R = 1;
+    while (R * 16 < L) R <<= 1;  // row tiles (power of two, divides 8)
+    const int qsplit = 8 / R, qw = kBwdRows / qsplit;  // query columns per warp
+    const int rt = warp % R, qsl = warp / R;
+    const uint32_t a_off = ((rt * 16 + (lane & 15)) * T::kStride + (lane >> 4) * 8) * 2;
+    float dka[D / 8][4], dva[D / 8][4];
+#pragma unroll
+    for (int t = 0; t < D / 8; ++t)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) dka[t][c] = dva[t][c] = 0.f;
+    __syncthreads();  // partial buffers (aliasing the tiles) consumed
+    load_tile<D>(ks, level_block(p.k, p.k_pyr, p.bkv_total, bkv, p.n, D, p.b_k, h, j), L, 0);
+    load_tile<D>(vs, level_block(p.v, p.v_pyr, p.bkv_total, bkv, p.n, D, p.b_k, h, j), L, 0);
+    const int key_a = rt * 16 + (lane >> 2);  // this thread's pooled rows key_a, key_a + 8
+    for (int e = e0; e < e1; ++e) {
+      const int x = static_cast<int>(ents[e]);
+      const int g = x / p.n_q, iq = x % p.n_q;
+      const int64_t bhq = static_cast<int64_t>(b) * p.hq + hk * group + g;
+      const int64_t row0 = bhq * p.n + static_cast<int64_t>(iq) * p.b_q;
+      __syncthreads();
+      load_tile<D>(qs, p.q + row0 * D, p.b_q, 0);
+      load_tile<D>(ds, p.dout + row0 * D, p.b_q, 0);
+      if (threadIdx.x < kBwdRows) {
+        const int r = threadIdx.x;
+        lse_s[r] = r < p.b_q ? p.lse[row0 + r] : -INFINITY;
+        d_s[r] = r < p.b_q ? p.drow[row0 + r] : 0.f;
+      }
+      __syncthreads();
+      const int64_t qpos0 = static_cast<int64_t>(iq) * p.b_q;
+      const bool straddle = p.causal && (static_cast<int64_t>(j + 1) * p.b_k - 1 > qpos0);
+      for (int qc = qsl * qw; qc < (qsl + 1) * qw && qc < p.b_q; qc += 64) {
+        const int nq16 = min(4, (min((qsl + 1) * qw, qc + 64) - qc) >> 4);  // 16-query tiles
+        float st[8][4], dpt[8][4];
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) st[t][c] = dpt[t][c] = 0.f;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          uint32_t ka[4], va[4];
+          ldsm4(ka, ks_a + a_off + kk * 32);
+          ldsm4(va, vs_a + a_off + kk * 32);
+#pragma unroll
+          for (int t2 = 0; t2 < 4; ++t2) {
+            if (t2 < nq16) {
+              uint32_t qb[4], db[4];
+              const uint32_t off = ((qc + t2 * 16 + bn) * T::kStride + kk * 16 + bk) * 2;
+              ldsm4(qb, qs_a + off);
+              ldsm4(db, ds_a + off);
+              mma16816(st[2 * t2], ka, qb[0], qb[1]);
+              mma16816(st[2 * t2 + 1], ka, qb[2], qb[3]);
+              mma16816(dpt[2 * t2], va, db[0], db[1]);
+              mma16816(dpt[2 * t2 + 1], va, db[2], db[3]);
+            }
+          }
+        }
+        uint32_t pa[4][4], dsa[4][4];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          float pv[4], sv4[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int key = key_a + ((c >> 1) << 3);
+            const int qr = qc + t * 8 + 2 * (lane & 3) + (c & 1);  // may pass 127 (masked)
+            const int qi = min(qr, kBwdRows - 1);
+            const float l = lse_s[qi];
+            const int64_t kpos = static_cast<int64_t>(j) * p.b_k + key;  // level 1 only straddles
+            const bool ok = t < 2 * nq16 && key < L && qr < p.b_q && l != -INFINITY &&
+                            !(straddle && kpos > qpos0 + qr);
+            const float pr = ok ? exp2f(fmaf(st[t][c], p.scale_log2, -l * kLog2e)) : 0.f;
+            pv[c] = pr;
+            sv4[c] = pr * (dpt[t][c] - d_s[qi]);
+          }
+          pa[t >> 1][(t & 1) * 2 + 0] = pack_bf16x2(pv[0], pv[1]);
+          pa[t >> 1][(t & 1) * 2 + 1] = pack_bf16x2(pv[2], pv[3]);
+          dsa[t >> 1][(t & 1) * 2 + 0] = pack_bf16x2(sv4[0], sv4[1]);
+          dsa[t >> 1][(t & 1) * 2 + 1] = pack_bf16x2(sv4[2], sv4[3]);
+        }
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          if (kk < nq16) {
+            const uint32_t ap[4] = {pa[kk][0], pa[kk][1], pa[kk][2], pa[kk][3]};
+            const uint32_t as[4] = {dsa[kk][0], dsa[kk][1], dsa[kk][2], dsa[kk][3]};
+#pragma unroll
+            for (int t2 = 0; t2 < D / 16; ++t2) {
+              uint32_t db[4], qb[4];
+              const uint32_t off = ((qc + kk * 16 + tk) * T::kStride + t2 * 16 + tn) * 2;
+              ldsm4t(db, ds_a + off);
+              ldsm4t(qb, qs_a + off);
+              mma16816(dva[2 * t2], ap, db[0], db[1]);
+              mma16816(dva[2 * t2 + 1], ap, db[2], db[3]);
+              mma16816(dka[2 * t2], as, qb[0], qb[1]);
+              mma16816(dka[2 * t2 + 1], as, qb[2], qb[3]);
+            }
+          }
+        }
+      }
+    }
+    // ---- level end: partials -> shared memory [warp][16][D] (dK then dV), sum over the query
+    // slices, add row r >> (h-1) to every raw row r of the block
     __syncthreads();
-    if (h != cur_h) {
-      load_tile<D>(ks, level_block(p.k, p.k_pyr, p.bkv_total, bkv, p.n, D, p.b_k, h, j), p.b_k, h - 1);
-      load_tile<D>(vs, level_block(p.v, p.v_pyr, p.bkv_total, bkv, p.n, D, p.b_k, h, j), p.b_k, h - 1);
-      cur_h = h;
-    }
-    load_tile<D>(qs, p.q + row0 * D, p.b_q, 0);
-    load_tile<D>(ds, p.dout + row0 * D, p.b_q, 0);
-    if (threadIdx.x < kBwdRows) {
-      const int r = threadIdx.x;
-      const float l = r < p.b_q ? p.lse[row0 + r] : -INFINITY;
-      lse_s[r] = l;
-      d_s[r] = r < p.b_q ? p.drow[row0 + r] : 0.f;
+    float* pk = part;
+    float* pvv = part + 8 * 16 * D;
+#pragma unroll
+    for (int t = 0; t < D / 8; ++t) {
+      const int c = t * 8 + 2 * (lane & 3);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int r16 = (lane >> 2) + 8 * u;
+        pk[(warp * 16 + r16) * D + c] = dka[t][2 * u];
+        pk[(warp * 16 + r16) * D + c + 1] = dka[t][2 * u + 1];
+        pvv[(warp * 16 + r16) * D + c] = dva[t][2 * u];
+        pvv[(warp * 16 + r16) * D + c + 1] = dva[t][2 * u + 1];
+      }
     }
     __syncthreads();
-    const int64_t qpos0 = static_cast<int64_t>(iq) * p.b_q;
-    const bool straddle = p.causal && (static_cast<int64_t>(j + 1) * p.b_k - 1 > qpos0);
-    for (int qc = 0; qc < p.b_q; qc += 64) {
-      float st[8][4], dpt[8][4];
-#pragma unroll
-      for (int t = 0; t < 8; ++t)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) st[t][c] = dpt[t][c] = 0.f;
-#pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk) {
-        uint32_t ka[4], va[4];
-        ldsm4(ka, ks_a + a_off + kk * 32);
-        ldsm4(va, vs_a + a_off + kk * 32);
-#pragma unroll
-        for (int t2 = 0; t2 < 4; ++t2) {  // query n-tiles: Q / dO rows are [n][k] in memory
-          uint32_t qb[4], db[4];
-          const uint32_t off = ((qc + t2 * 16 + bn) * T::kStride + kk * 16 + bk) * 2;
-          ldsm4(qb, qs_a + off);
-          ldsm4(db, ds_a + off);
-          mma16816(st[2 * t2], ka, qb[0], qb[1]);
-          mma16816(st[2 * t2 + 1], ka, qb[2], qb[3]);
-          mma16816(dpt[2 * t2], va, db[0], db[1]);
-          mma16816(dpt[2 * t2 + 1], va, db[2], db[3]);
-        }
+    for (int x = threadIdx.x; x < p.b_k * D; x += kBwdThreads) {
+      const int r = x / D, c = x % D;
+      const int tp = r >> (h - 1);
+      const int w0 = tp >> 4, r16 = tp & 15;
+      float gk = 0.f, gv = 0.f;
+      for (int q2 = 0; q2 < qsplit; ++q2) {
+        const int w = w0 + q2 * R;
+        gk += pk[(w * 16 + r16) * D + c];
+        gv += pvv[(w * 16 + r16) * D + c];
       }
-      uint32_t pa[4][4], dsa[4][4];
-#pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        float pv[4], sv[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int key = ra + ((c >> 1) << 3);
-          const int qr = qc + t * 8 + 2 * (lane & 3) + (c & 1);
-          const float l = lse_s[qr];
-          const int64_t kpos = static_cast<int64_t>(j) * p.b_k + key;
-          const bool ok = qr < p.b_q && l != -INFINITY && !(straddle && kpos > qpos0 + qr);
-          const float pr = ok ? exp2f(fmaf(st[t][c], p.scale_log2, -l * kLog2e)) : 0.f;
-          pv[c] = pr;
-          sv[c] = pr * (dpt[t][c] - d_s[qr]);
-        }
-        pa[t >> 1][(t & 1) * 2 + 0] = pack_bf16x2(pv[0], pv[1]);
-        pa[t >> 1][(t & 1) * 2 + 1] = pack_bf16x2(pv[2], pv[3]);
-        dsa[t >> 1][(t & 1) * 2 + 0] = pack_bf16x2(sv[0], sv[1]);
-        dsa[t >> 1][(t & 1) * 2 + 1] = pack_bf16x2(sv[2], sv[3]);
-      }
-      // dV += P^T (16 keys x 64 queries) dO (64 x D); dK += dS^T Q: query rows are the k dim
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        const uint32_t ap[4] = {pa[kk][0], pa[kk][1], pa[kk][2], pa[kk][3]};
-        const uint32_t as[4] = {dsa[kk][0], dsa[kk][1], dsa[kk][2], dsa[kk][3]};
-#pragma unroll
-        for (int t2 = 0; t2 < D / 16; ++t2) {
-          uint32_t db[4], qb[4];
-          const uint32_t off = ((qc + kk * 16 + tk) * T::kStride + t2 * 16 + tn) * 2;
-          ldsm4t(db, ds_a + off);
-          ldsm4t(qb, qs_a + off);
-          mma16816(dva[2 * t2], ap, db[0], db[1]);
-          mma16816(dva[2 * t2 + 1], ap, db[2], db[3]);
-          mma16816(dka[2 * t2], as, qb[0], qb[1]);
-          mma16816(dka[2 * t2 + 1], as, qb[2], qb[3]);
-        }
-      }
+      sk[x] = first ? gk : sk[x] + gk;
+      sv[x] = first ? gv : sv[x] + gv;
     }
+    first = false;
+    e0 = e1;
   }
-  // raw rows of block j (keys beyond b_k are padding)
-  const int64_t krow0 = bkv * p.n + static_cast<int64_t>(j) * p.b_k;
-#pragma unroll
-  for (int t = 0; t < D / 8; ++t) {
-    const int c = t * 8 + 2 * (lane & 3);
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int r = ra + u * 8;
-      if (r < p.b_k) {
-        *reinterpret_cast<uint32_t*>(p.dk + (krow0 + r) * D + c) =
-            pack_bf16x2(dka[t][2 * u] * p.scale, dka[t][2 * u + 1] * p.scale);
-        *reinterpret_cast<uint32_t*>(p.dv + (krow0 + r) * D + c) =
-            pack_bf16x2(dva[t][2 * u], dva[t][2 * u + 1]);
-      }
+  __syncthreads();
+  for (int x = threadIdx.x; x < p.b_k * D / 2; x += kBwdThreads) {
+    const int r = (2 * x) / D, c = (2 * x) % D;
+    uint32_t okv = 0u, ovv = 0u;
+    if (!first) {
+      okv = pack_bf16x2(sk[r * D + c] * p.scale, sk[r * D + c + 1] * p.scale);
+      ovv = pack_bf16x2(sv[r * D + c], sv[r * D + c + 1]);
     }
+    *reinterpret_cast<uint32_t*>(p.dk + (krow0 + r) * D + c) = okv;
+    *reinterpret_cast<uint32_t*>(p.dv + (krow0 + r) * D + c) = ovv;
   }
 }
 
@@ -409,24 +509,27 @@ template <int D>
 static int launch_bwd(BwdParams p, int64_t batch, const uint16_t* out, void* ws, cudaStream_t s) {
   const int64_t rows = batch * p.hq * p.n;
   float* drow = static_cast<float*>(ws);
+  float* scratch = drow + ((rows + 63) / 64) * 64;
   p.drow = drow;
   bwd_drow_kernel<D><<<static_cast<unsigned>((rows + 7) / 8), 256, 0, s>>>(out, p.dout, rows, drow);
   int rc = psa_check_launch("bwd_drow_kernel");
   if (rc) return rc;
-  const size_t tiles = 4 * static_cast<size_t>(BwdTile<D>::kBytes);
+  const size_t smem_q = 2 * static_cast<size_t>(BwdTile<D>::kBytes) +
+                        2 * static_cast<size_t>(kChunkKeys) * BwdTile<D>::kStride * 2 +
+                        static_cast<size_t>(p.n_k + 1) * 4 + kChunkKeys * 8;
   cudaFuncSetAttribute(bwd_dq_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       static_cast<int>(tiles));
-  bwd_dq_kernel<D><<<static_cast<unsigned>(batch * p.hq * p.n_q), kBwdThreads, tiles, s>>>(p);
+                       static_cast<int>(smem_q));
+  bwd_dq_kernel<D><<<static_cast<unsigned>(batch * p.hq * p.n_q), kBwdThreads, smem_q, s>>>(p);
   rc = psa_check_launch("bwd_dq_kernel");
   if (rc) return rc;
-  const int group = p.hq / p.hkv;
-  const int cap = group * p.n_q;
-  const size_t smem = tiles + 2 * kBwdRows * sizeof(float) + static_cast<size_t>(cap) * 4;
+  const int cap = (p.hq / p.hkv) * p.n_q;
+  const size_t smem = 4 * static_cast<size_t>(BwdTile<D>::kBytes) + 2 * kBwdRows * sizeof(float) +
+                      static_cast<size_t>(cap) * 4;
   if (smem > 227 * 1024) return psa_fail(PSA_EINVAL, "too many query blocks per KV head for the backward kernel");
   cudaFuncSetAttribute(bwd_dkv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(smem));
   bwd_dkv_kernel<D><<<dim3(static_cast<unsigned>(p.n_k), static_cast<unsigned>(batch * p.hkv)),
-                      kBwdThreads, smem, s>>>(p, cap);
+                      kBwdThreads, smem, s>>>(p, cap, scratch);
   return psa_check_launch("bwd_dkv_kernel");
 }
 
@@ -434,8 +537,10 @@ static int launch_bwd(BwdParams p, int64_t batch, const uint16_t* out, void* ws,
 
 using namespace psa;
 
-extern "C" size_t psa_attn_bwd_workspace_bytes(int64_t batch, int hq, int64_t n) {
-  return static_cast<size_t>(batch * hq * n) * sizeof(float);
+extern "C" size_t psa_attn_bwd_workspace_bytes(int64_t batch, int hq, int hkv, int64_t n, int d) {
+  // D = rowsum(dO * O) per query row, then fp32 dK / dV accumulators of the raw rows
+  const int64_t rows = batch * hq * n;
+  return static_cast<size_t>((rows + 63) / 64 * 64 + 2 * batch * hkv * n * d) * sizeof(float);
 }
 
 extern "C" int psa_attn_bwd(const void* q, const void* k, const void* v, const void* k_pyr,
