@@ -19,8 +19,8 @@
 //
 // First version: warp-level mma.sync (m16n8k16 bf16, fp32 accumulate) with ldmatrix fragments,
 // one CTA per (head, query block) for dQ and one per (KV head, KV block) for dK/dV (8 warps,
-// 1 CTA per SM at ~230-255 registers); cfg3 backward 916 ms (dQ 361 ms, dK/dV 555 ms) against a
-// 36 ms forward. The tcgen05 / TMEM version is the next step.
+// 1 CTA per SM at ~230-255 registers, cp.async double-buffered K/V chunks and Q/dO tiles); cfg3
+// backward 839 ms against a 36 ms forward. The tcgen05 / TMEM version is the next step.
 #include "common.cuh"
 #include "psa_internal.h"
 
@@ -68,6 +68,13 @@ PSA_DEV void ldsm4t(uint32_t (&r)[4], uint32_t addr) {
                : "r"(addr));
 }
 PSA_DEV float bf2f(uint16_t x) { return __uint_as_float(static_cast<uint32_t>(x) << 16); }
+PSA_DEV void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem)
+               : "memory");
+}
+PSA_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+PSA_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // Tiles in shared memory: [128 rows][D + 8] bf16 (the 16-byte pad makes ldmatrix conflict-free).
 template <int D>
@@ -86,6 +93,18 @@ __device__ void load_tile(uint16_t* tile, const uint16_t* src, int rows, int exp
     uint4 val = make_uint4(0u, 0u, 0u, 0u);
     if (r < rows) val = *reinterpret_cast<const uint4*>(src + static_cast<int64_t>(r >> expand_shift) * D + c);
     *reinterpret_cast<uint4*>(tile + r * BwdTile<D>::kStride + c) = val;
+  }
+}
+
+// load_tile with cp.async (completion via cp_async_commit / cp_async_wait; zero rows stored)
+template <int D>
+__device__ void load_tile_async(uint16_t* tile, const uint16_t* src, int rows) {
+  constexpr int kVec = D / 8;
+  for (int e = threadIdx.x; e < kBwdRows * kVec; e += kBwdThreads) {
+    const int r = e / kVec, c = (e % kVec) * 8;
+    uint16_t* dst = tile + r * BwdTile<D>::kStride + c;
+    if (r < rows) cp_async16(dst, src + static_cast<int64_t>(r) * D + c);
+    else *reinterpret_cast<uint4*>(dst) = make_uint4(0u, 0u, 0u, 0u);
   }
 }
 
@@ -132,11 +151,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1) bwd_dq_kernel(const BwdParams 
   using T = BwdTile<D>;
   uint16_t* qs = reinterpret_cast<uint16_t*>(smem_raw);
   uint16_t* ds = qs + kBwdRows * T::kStride;
-  uint16_t* ks = ds + kBwdRows * T::kStride;  // kChunkKeys rows used
-  uint16_t* vs = ks + kChunkKeys * T::kStride;
-  int* ent_off = reinterpret_cast<int*>(vs + kChunkKeys * T::kStride);  // [n_k + 1] pooled-row prefix
-  float* cbias = reinterpret_cast<float*>(ent_off + p.n_k + 1);         // [kChunkKeys]
-  int* ckpos = reinterpret_cast<int*>(cbias + kChunkKeys);              // [kChunkKeys]
+  uint16_t* kbuf = ds + kBwdRows * T::kStride;  // 2 stages x kChunkKeys rows (K), then V
+  uint16_t* vbuf = kbuf + 2 * kChunkKeys * T::kStride;
+  int* ent_off = reinterpret_cast<int*>(vbuf + 2 * kChunkKeys * T::kStride);  // [n_k + 1]
+  float* cbias_b = reinterpret_cast<float*>(ent_off + p.n_k + 1);  // [2][kChunkKeys]
+  int* ckpos_b = reinterpret_cast<int*>(cbias_b + 2 * kChunkKeys);  // [2][kChunkKeys]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t unit = blockIdx.x;
   const int bhq = static_cast<int>(unit / p.n_q), i = static_cast<int>(unit % p.n_q);
@@ -171,7 +190,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) bwd_dq_kernel(const BwdParams 
   float dqa[D / 8][4];
 #pragma unroll
   for (int t = 0; t < D / 8; ++t) dqa[t][0] = dqa[t][1] = dqa[t][2] = dqa[t][3] = 0.f;
-  const uint32_t qs_a = smem_u32(qs), ds_a = smem_u32(ds), ks_a = smem_u32(ks), vs_a = smem_u32(vs);
+  const uint32_t qs_a = smem_u32(qs), ds_a = smem_u32(ds);
   const uint32_t a_off = ((warp * 16 + (lane & 15)) * T::kStride + (lane >> 4) * 8) * 2;
   const int bn = (lane & 7) + ((lane >> 4) << 3), bk = ((lane >> 3) & 1) * 8;   // [n][k] memory
   const int tk = (lane & 7) + (((lane >> 3) & 1) << 3), tn = (lane >> 4) << 3;  // [k][n] memory
@@ -179,14 +198,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1) bwd_dq_kernel(const BwdParams 
   __syncthreads();
   const int total = ent_off[n_ent];
 
-  for (int base = 0; base < total; base += kChunkKeys) {
-    const int nk = min(kChunkKeys, total - base);
-    __syncthreads();  // previous chunk fully consumed
-    // stage the chunk: key row c <- pooled row (e, t) with base + c = ent_off[e] + t
+  // stage chunk `base` into buffer st: key row c <- pooled row (e, t), base + c = ent_off[e] + t
+  auto stage = [&](int base, int st) {
     constexpr int kVec = D / 8;
+    const int nk = min(kChunkKeys, total - base);
+    uint16_t* kd = kbuf + st * kChunkKeys * T::kStride;
+    uint16_t* vd = vbuf + st * kChunkKeys * T::kStride;
     for (int x = threadIdx.x; x < kChunkKeys * kVec; x += kBwdThreads) {
       const int c = x / kVec, col = (x % kVec) * 8;
-      uint4 kv4 = make_uint4(0u, 0u, 0u, 0u), vv4 = kv4;
       if (c < nk) {
         const int g = base + c;
         int lo = 0, hi = n_ent - 1;  // last entry with ent_off[e] <= g
@@ -198,20 +217,37 @@ __global__ void __launch_bounds__(kBwdThreads, 1) bwd_dq_kernel(const BwdParams 
         const int j = static_cast<int>(ent & 0xFFFu), h = static_cast<int>(ent >> 12);
         const int t = g - ent_off[lo];
         const int64_t src = static_cast<int64_t>(t) * D + col;
-        kv4 = *reinterpret_cast<const uint4*>(level_block(p.k, p.k_pyr, p.bkv_total, bkv, p.n, D, p.b_k, h, j) + src);
-        vv4 = *reinterpret_cast<const uint4*>(level_block(p.v, p.v_pyr, p.bkv_total, bkv, p.n, D, p.b_k, h, j) + src);
+        cp_async16(kd + c * T::kStride + col, level_block(p.k, p.k_pyr, p.bkv_total, bkv, p.n, D, p.b_k, h, j) + src);
+        cp_async16(vd + c * T::kStride + col, level_block(p.v, p.v_pyr, p.bkv_total, bkv, p.n, D, p.b_k, h, j) + src);
         if (col == 0) {
-          cbias[c] = static_cast<float>(h - 1);
-          ckpos[c] = h == 1 ? j * p.b_k + t : -1;  // pooled levels never straddle (causal premask)
+          cbias_b[st * kChunkKeys + c] = static_cast<float>(h - 1);
+          ckpos_b[st * kChunkKeys + c] = h == 1 ? j * p.b_k + t : -1;  // pooled levels never straddle
         }
-      } else if (col == 0) {
-        cbias[c] = -INFINITY;
-        ckpos[c] = -1;
+      } else {
+        *reinterpret_cast<uint4*>(kd + c * T::kStride + col) = make_uint4(0u, 0u, 0u, 0u);
+        *reinterpret_cast<uint4*>(vd + c * T::kStride + col) = make_uint4(0u, 0u, 0u, 0u);
+        if (col == 0) {
+          cbias_b[st * kChunkKeys + c] = -INFINITY;
+          ckpos_b[st * kChunkKeys + c] = -1;
+        }
       }
-      *reinterpret_cast<uint4*>(ks + c * T::kStride + col) = kv4;
-      *reinterpret_cast<uint4*>(vs + c * T::kStride + col) = vv4;
+    }
+    cp_async_commit();
+  };
+  if (total > 0) stage(0, 0);
+  for (int base = 0, st = 0; base < total; base += kChunkKeys, st ^= 1) {
+    const int nk = min(kChunkKeys, total - base);
+    if (base + kChunkKeys < total) {
+      stage(base + kChunkKeys, st ^ 1);  // buffer st^1 was released by the sync ending chunk-1
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
+    const uint32_t ks_a = smem_u32(kbuf + st * kChunkKeys * T::kStride);
+    const uint32_t vs_a = smem_u32(vbuf + st * kChunkKeys * T::kStride);
+    const float* cbias = cbias_b + st * kChunkKeys;
+    const int* ckpos = ckpos_b + st * kChunkKeys;
     const int nt16 = (nk + 15) >> 4;  // 16-key tiles holding keys
     float s[8][4], dp[8][4];
 #pragma unroll
@@ -268,6 +304,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) bwd_dq_kernel(const BwdParams 
         }
       }
     }
+    __syncthreads();  // buffer st free for the chunk after next
   }
 #pragma unroll
   for (int t = 0; t < D / 8; ++t) {
@@ -298,16 +335,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1) bwd_dkv_kernel(const BwdParams
                                                                 float* __restrict__ scratch) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   using T = BwdTile<D>;
-  uint16_t* qs = reinterpret_cast<uint16_t*>(smem_raw);
-  uint16_t* ds = qs + kBwdRows * T::kStride;
-  uint16_t* ks = ds + kBwdRows * T::kStride;
+  // Q / dO double-buffered (stage st at qbuf + st * 2 tiles), then the pooled K and V tiles
+  uint16_t* qbuf = reinterpret_cast<uint16_t*>(smem_raw);
+  uint16_t* ks = qbuf + 4 * kBwdRows * T::kStride;
   uint16_t* vs = ks + kBwdRows * T::kStride;
-  float* part = reinterpret_cast<float*>(smem_raw);  // level-end reduction (aliases the tiles)
-  float* lse_s = reinterpret_cast<float*>(vs + kBwdRows * T::kStride);
-  float* d_s = lse_s + kBwdRows;
-  uint32_t* ents = reinterpret_cast<uint32_t*>(d_s + kBwdRows);
+  float* part = reinterpret_cast<float*>(smem_raw);  // level-end reduction (aliases Q / dO)
+  float* lse_b = reinterpret_cast<float*>(vs + kBwdRows * T::kStride);  // [2][128]
+  float* d_b = lse_b + 2 * kBwdRows;                                     // [2][128]
+  uint32_t* ents = reinterpret_cast<uint32_t*>(d_b + 2 * kBwdRows);
   __shared__ int warp_cnt[kBwdThreads / 32];
-  static_assert(2 * 8 * 16 * D * 4 <= 4 * BwdTile<D>::kBytes, "partials must fit in the tiles");
+  static_assert(2 * 8 * 16 * D * 4 <= 4 * BwdTile<D>::kBytes, "partials must fit in Q / dO");
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int j = blockIdx.x;
@@ -349,11 +386,27 @@ __global__ void __launch_bounds__(kBwdThreads, 1) bwd_dkv_kernel(const BwdParams
   const int64_t krow0 = bkv * p.n + static_cast<int64_t>(j) * p.b_k;
   float* sk = scratch + krow0 * D;                        // dK rows of block j (fp32)
   float* sv = scratch + (p.bkv_total * p.n + krow0) * D;  // dV rows
-  const uint32_t qs_a = smem_u32(qs), ds_a = smem_u32(ds), ks_a = smem_u32(ks), vs_a = smem_u32(vs);
+  const uint32_t ks_a = smem_u32(ks), vs_a = smem_u32(vs);
   const int bn = (lane & 7) + ((lane >> 4) << 3), bk = ((lane >> 3) & 1) * 8;
   const int tk = (lane & 7) + (((lane >> 3) & 1) << 3), tn = (lane >> 4) << 3;
   const float kLog2e = 1.4426950408889634f;
   bool first = true;
+  // stage entry e (its query block's Q, dO, lse, D) into buffer st with cp.async
+  auto stage = [&](int e, int st) {
+    const int x = static_cast<int>(ents[e]);
+    const int g = x / p.n_q, iq = x % p.n_q;
+    const int64_t bhq = static_cast<int64_t>(b) * p.hq + hk * group + g;
+    const int64_t row0 = bhq * p.n + static_cast<int64_t>(iq) * p.b_q;
+    uint16_t* q_t = qbuf + (2 * st) * kBwdRows * T::kStride;
+    load_tile_async<D>(q_t, p.q + row0 * D, p.b_q);
+    load_tile_async<D>(q_t + kBwdRows * T::kStride, p.dout + row0 * D, p.b_q);
+    if (threadIdx.x < kBwdRows) {
+      const int r = threadIdx.x;
+      lse_b[st * kBwdRows + r] = r < p.b_q ? p.lse[row0 + r] : -INFINITY;
+      d_b[st * kBwdRows + r] = r < p.b_q ? p.drow[row0 + r] : 0.f;
+    }
+    cp_async_commit();
+  };
 
   int e0 = 0;
   for (int h = 1; h <= p.levels; ++h) {
@@ -374,20 +427,20 @@ __global__ void __launch_bounds__(kBwdThreads, 1) bwd_dkv_kernel(const BwdParams
     load_tile<D>(ks, level_block(p.k, p.k_pyr, p.bkv_total, bkv, p.n, D, p.b_k, h, j), L, 0);
     load_tile<D>(vs, level_block(p.v, p.v_pyr, p.bkv_total, bkv, p.n, D, p.b_k, h, j), L, 0);
     const int key_a = rt * 16 + (lane >> 2);  // this thread's pooled rows key_a, key_a + 8
-    for (int e = e0; e < e1; ++e) {
-      const int x = static_cast<int>(ents[e]);
-      const int g = x / p.n_q, iq = x % p.n_q;
-      const int64_t bhq = static_cast<int64_t>(b) * p.hq + hk * group + g;
-      const int64_t row0 = bhq * p.n + static_cast<int64_t>(iq) * p.b_q;
-      __syncthreads();
-      load_tile<D>(qs, p.q + row0 * D, p.b_q, 0);
-      load_tile<D>(ds, p.dout + row0 * D, p.b_q, 0);
-      if (threadIdx.x < kBwdRows) {
-        const int r = threadIdx.x;
-        lse_s[r] = r < p.b_q ? p.lse[row0 + r] : -INFINITY;
-        d_s[r] = r < p.b_q ? p.drow[row0 + r] : 0.f;
+    stage(e0, 0);
+    for (int e = e0, st = 0; e < e1; ++e, st ^= 1) {
+      if (e + 1 < e1) {
+        stage(e + 1, st ^ 1);  // buffer st^1 was released by the sync ending entry e-1
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
       }
       __syncthreads();
+      const int iq = static_cast<int>(ents[e]) % p.n_q;
+      const uint32_t qs_a = smem_u32(qbuf + (2 * st) * kBwdRows * T::kStride);
+      const uint32_t ds_a = qs_a + kBwdRows * T::kStride * 2;
+      const float* lse_s = lse_b + st * kBwdRows;
+      const float* d_s = d_b + st * kBwdRows;
       const int64_t qpos0 = static_cast<int64_t>(iq) * p.b_q;
       const bool straddle = p.causal && (static_cast<int64_t>(j + 1) * p.b_k - 1 > qpos0);
       for (int qc = qsl * qw; qc < (qsl + 1) * qw && qc < p.b_q; qc += 64) {
@@ -457,6 +510,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) bwd_dkv_kernel(const BwdParams
           }
         }
       }
+      __syncthreads();  // buffer st free for the entry after next
     }
     // ---- level end: partials -> shared memory [warp][16][D] (dK then dV), sum over the query
     // slices, add row r >> (h-1) to every raw row r of the block
@@ -515,15 +569,15 @@ static int launch_bwd(BwdParams p, int64_t batch, const uint16_t* out, void* ws,
   int rc = psa_check_launch("bwd_drow_kernel");
   if (rc) return rc;
   const size_t smem_q = 2 * static_cast<size_t>(BwdTile<D>::kBytes) +
-                        2 * static_cast<size_t>(kChunkKeys) * BwdTile<D>::kStride * 2 +
-                        static_cast<size_t>(p.n_k + 1) * 4 + kChunkKeys * 8;
+                        4 * static_cast<size_t>(kChunkKeys) * BwdTile<D>::kStride * 2 +
+                        static_cast<size_t>(p.n_k + 1) * 4 + 2 * kChunkKeys * 8;
   cudaFuncSetAttribute(bwd_dq_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(smem_q));
   bwd_dq_kernel<D><<<static_cast<unsigned>(batch * p.hq * p.n_q), kBwdThreads, smem_q, s>>>(p);
   rc = psa_check_launch("bwd_dq_kernel");
   if (rc) return rc;
   const int cap = (p.hq / p.hkv) * p.n_q;
-  const size_t smem = 4 * static_cast<size_t>(BwdTile<D>::kBytes) + 2 * kBwdRows * sizeof(float) +
+  const size_t smem = 6 * static_cast<size_t>(BwdTile<D>::kBytes) + 4 * kBwdRows * sizeof(float) +
                       static_cast<size_t>(cap) * 4;
   if (smem > 227 * 1024) return psa_fail(PSA_EINVAL, "too many query blocks per KV head for the backward kernel");
   cudaFuncSetAttribute(bwd_dkv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
