@@ -561,7 +561,7 @@ EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
-
+// 2D bf16 [rows, cols] row-major, box = [box_rows, 64 cols], 128-byte swizzle.
 static int encode_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols,
                      uint32_t box_rows) {
   EncodeTiledFn fn = get_encode_fn();
