@@ -111,7 +111,10 @@ struct PlanCursor {
 // Register split via setmaxnreg within the CTA pool of 384 x 168: producer/MMA warpgroup 64,
 // softmax warpgroups 216 (128*64 + 256*216 <= 384*168, else the increase never completes).
 constexpr int kPPThreads = 384;
-constexpr int kPPPolyFrom = 96;  // columns [96, 128) of a row use the FMA-pipe exp2
+// Softmax columns >= kPPPolyFrom would use the FMA-pipe exp2 polynomial instead of MUFU.EX2.
+// Measured at cfg3: 128 (all MUFU) 25.9 ms, 112: 26.7, 96: 26.5, 80: 27.6, 64: 28.2 -- the lanes
+// are issue/latency-bound, not MUFU-bound, so the 6-instruction polynomial does not pay.
+constexpr int kPPPolyFrom = 128;
 
 template <uint32_t N>
 PSA_DEV void regs_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N)); }
