@@ -111,10 +111,6 @@ struct PlanCursor {
 // Register split via setmaxnreg within the CTA pool of 384 x 168: producer/MMA warpgroup 64,
 // softmax warpgroups 216 (128*64 + 256*216 <= 384*168, else the increase never completes).
 constexpr int kPPThreads = 384;
-// Softmax columns >= kPPPolyFrom would use the FMA-pipe exp2 polynomial instead of MUFU.EX2.
-// Measured at cfg3: 128 (all MUFU) 25.9 ms, 112: 26.7, 96: 26.5, 80: 27.6, 64: 28.2 -- the lanes
-// are issue/latency-bound, not MUFU-bound, so the 6-instruction polynomial does not pay.
-constexpr int kPPPolyFrom = 128;
 
 template <uint32_t N>
 PSA_DEV void regs_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N)); }
@@ -145,7 +141,7 @@ struct PP2Smem {
   uint32_t tmem_base;
 };
 
-template <int D, int POLY_FROM = kPPPolyFrom>
+template <int D>
 __global__ void __launch_bounds__(kPPThreads, 1)
     psa_attn_pp2_kernel(const __grid_constant__ AttnMaps maps, const AttnParams p,
                        const uint16_t* __restrict__ csr, const int32_t* __restrict__ info,
@@ -424,15 +420,12 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       for (int e = 0; e < 128; e += 4) {
         float2 a = fadd2(make_float2(y[e], y[e + 1]), negm);
         float2 c = fadd2(make_float2(y[e + 2], y[e + 3]), negm);
-        if (e >= POLY_FROM) {
-          a = ex2_poly2(a);
-          c = ex2_poly2(c);
-        } else {
-          a.x = ex2_approx(a.x);
-          a.y = ex2_approx(a.y);
-          c.x = ex2_approx(c.x);
-          c.y = ex2_approx(c.y);
-        }
+        // every exp on MUFU: an FMA-pipe polynomial for the last 16/32/48/64 columns measured
+        // 26.7/26.5/27.6/28.2 ms against 25.9 ms at cfg3 (the lanes are issue-bound, not MUFU-bound)
+        a.x = ex2_approx(a.x);
+        a.y = ex2_approx(a.y);
+        c.x = ex2_approx(c.x);
+        c.y = ex2_approx(c.y);
         ls0 = fadd2(ls0, a);
         ls1 = fadd2(ls1, c);
         pk[e / 2] = pack_bf16x2(a.x, a.y);
