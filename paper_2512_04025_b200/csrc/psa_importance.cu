@@ -386,7 +386,7 @@ static AdGeom ad_geometry(int64_t bhq, int64_t bkv, int64_t n, int b_q, int b_k,
   a.per = b_k / stride;
   a.c_max = (b_q + stride - 1) / stride;
   const int n_q = static_cast<int>(n / b_q), n_k = static_cast<int>(n / b_k);
-  a.xl = xl_geometry(bhq, bkv, n_q, n_k, stride, n_q * a.c_max, a.per);
+  a.xl = xl_geometry(bhq, bkv, n_q, n_k, stride, n_q * a.c_max, a.per, bhq * n);
   a.xl.ok = a.xl.ok && allow_xl;
   a.bpc = a.xl.ok ? a.xl.bpt : kImpCols / a.per;
   a.n_chunks = (n_k + a.bpc - 1) / a.bpc;
@@ -469,7 +469,8 @@ extern "C" int psa_importance_antidiagonal(const void* q, const void* k, int64_t
 
 static XlGeometry sampled_xl_geometry(int64_t bhq, int64_t bkv, int n_q, int s_q, int n_k,
                                       int s_k, bool allow) {
-  XlGeometry g = xl_geometry(bhq, bkv, n_q, n_k, 1, n_q * s_q, s_k);
+  XlGeometry g = xl_geometry(bhq, bkv, n_q, n_k, 1, n_q * s_q, s_k,
+                             bhq * static_cast<int64_t>(n_q) * s_q);
   g.ok = g.ok && allow;
   return g;
 }

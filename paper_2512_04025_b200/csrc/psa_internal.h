@@ -30,10 +30,12 @@ struct LevelRule {  // thresholds (mode 0) or quantile rank counts (mode 1)
 struct XlGeometry {
   bool ok;
   int per, bpt, n_halves, n_tiles, kp, rq_pad, classes;  // bpt: KV blocks per 16-key half
-  size_t off_ks, off_qm, off_km, off_flags, bytes;
+  int ksplit, tps;   // key tiles split over ksplit CTAs of tps tiles (merged by xl_merge_kernel)
+  int64_t out_rows;  // rows of the (m, l) statistics
+  size_t off_ks, off_qm, off_km, off_flags, off_part, bytes;
 };
 XlGeometry xl_geometry(int64_t bhq, int64_t bkv, int n_q, int n_k, int classes, int rows_per_class,
-                       int per);
+                       int per, int64_t out_rows);
 int xl_sampled_max(const void* q, const void* k, int64_t batch, int hq, int hkv, int64_t n, int d,
                    int b_q, int b_k, const int32_t* q_rows, const int32_t* k_rows, int s_q,
                    int s_k, const XlGeometry& g, void* ws, double* M, double* mstat,

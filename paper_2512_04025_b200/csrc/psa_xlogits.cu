@@ -31,6 +31,8 @@
 //           buffer g; their running (m, l) merge at the end). The epilogue is FP64-pipe bound
 //           (one fp64 exp per logit), so it keeps the tile's 32 logits in registers and
 //           evaluates them as independent chains.
+#include <algorithm>
+
 #include "common.cuh"
 #include "psa_internal.h"
 
@@ -189,6 +191,8 @@ struct XlParams {
   int64_t n;
   int hq, hkv, classes, stride, b_q, b_k, n_q, n_k;
   int r_total, rq_pad, kp, n_tiles, n_chunks, per, bpt;  // bpt: KV blocks per 16-key half
+  int ksplit, tps;  // key tiles split over ksplit CTAs of tps tiles each (partial row stats)
+  int64_t out_rows;  // rows of mstat / lstat
   double sqrt_d, inv_sqrt_d, scale;
   const uint16_t* q;
   const uint16_t* k;
@@ -202,6 +206,8 @@ struct XlParams {
   double* Mc;     // ANTIDIAG: chunk maxima [bhq][n][n_tiles]
   double* mstat;  // [bhq][R or n]
   double* lstat;
+  double* pm;     // ksplit > 1: per-split (m, l) [ksplit][out_rows], merged by xl_merge_kernel
+  double* pl;
 };
 
 struct XlMaps {
@@ -360,7 +366,7 @@ __global__ void __launch_bounds__(kXlThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qt = blockIdx.x;
   const int bhq = blockIdx.y;
-  const int cls = blockIdx.z;
+  const int cls = blockIdx.z / p.ksplit, split = blockIdx.z % p.ksplit;
   const int b = bhq / p.hq, h = bhq % p.hq;
   const int bkv = b * p.hkv + h / (p.hq / p.hkv);
   if (p.qflag[bhq] | p.kflag[bkv]) return;  // head handled by the fp64 DMMA kernel
@@ -371,7 +377,8 @@ __global__ void __launch_bounds__(kXlThreads, 1)
   KRows krows = krows0;
   krows.set_class(kcls, p.stride, p.b_k);
   if (qt * kXlQRows >= rows_valid) return;
-  const int T = p.n_tiles;
+  const int t0 = split * p.tps;                   // this CTA's key tiles [t0, t0 + T)
+  const int T = min(p.n_tiles, t0 + p.tps) - t0;  // >= 1 (ksplit <= n_tiles)
 
   if (threadIdx.x == 0) {
     if (smem_u32(smem_raw) & 1023u) __trap();
@@ -423,7 +430,8 @@ __global__ void __launch_bounds__(kXlThreads, 1)
         if (t >= kXlStages) mbar_wait_backoff(&sm.k_empty[s], ((t / kXlStages) - 1) & 1);
         mbar_arrive_expect_tx(&sm.k_full[s], kXlSlices * kXlKeys * kXlRowBytes);
         for (int bb = 0; bb < kXlSlices; ++bb)
-          tma_load_2d(&maps.ks, &sm.k_full[s], sm.k[s][bb], 0, (kset + bb) * p.kp + t * kXlKeys);
+          tma_load_2d(&maps.ks, &sm.k_full[s], sm.k[s][bb], 0,
+                      (kset + bb) * p.kp + (t0 + t) * kXlKeys);
       }
     }
   } else if (warp == 1) {
@@ -485,7 +493,8 @@ __global__ void __launch_bounds__(kXlThreads, 1)
     double rmax = -INFINITY;  // MAX mode: exact running max of the raw dot products
     double* xs = &sm.ex[0][e_tid];  // this thread's column: 16 values, stride kXlEpiThreads
 
-    for (int t = buf; t < T; t += 2) {
+    for (int tl = buf; tl < T; tl += 2) {
+      const int t = t0 + tl;  // global key tile
       const int hx = 2 * t + half;
       const int j0 = hx * p.bpt;  // first KV block of the half
       const int nb = max(0, min(p.bpt, p.n_k - j0));
@@ -493,7 +502,7 @@ __global__ void __launch_bounds__(kXlThreads, 1)
       const uint32_t valid_mask = (1u << nvalid) - 1u;
       const XlMeta kml = kmeta[t * kXlKeys + half * kXlHalf + (lane & (kXlHalf - 1))];
       const int kinfo = (kml.e << 1) | ((kml.tiny >> 28) != 0u ? 1 : 0);
-      mbar_wait(&sm.acc_full[buf], (t >> 1) & 1);
+      mbar_wait(&sm.acc_full[buf], (tl >> 1) & 1);
       tc_fence_after();
       double dv[kXlHalf];
 #pragma unroll
@@ -702,8 +711,13 @@ __global__ void __launch_bounds__(kXlThreads, 1)
         const double mg = sm.red_m[g][row];
         if (mg != -INFINITY) l = __dadd_rn(l, __dmul_rn(sm.red_l[g][row], exp(__dsub_rn(mg, m))));
       }
-      p.mstat[out_row] = m;
-      p.lstat[out_row] = l;
+      if (p.ksplit > 1) {
+        p.pm[split * p.out_rows + out_row] = m;
+        p.pl[split * p.out_rows + out_row] = l;
+      } else {
+        p.mstat[out_row] = m;
+        p.lstat[out_row] = l;
+      }
     }
   }
 
@@ -713,6 +727,32 @@ __global__ void __launch_bounds__(kXlThreads, 1)
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
+}
+
+// Key-split merge: m = max_s m_s, l = sum_s l_s exp(m_s - m) (the stats kernel's own group merge
+// across CTAs). Heads flagged for the fp64 kernel are left to it.
+__global__ void __launch_bounds__(256) xl_merge_kernel(const double* __restrict__ pm,
+                                                       const double* __restrict__ pl, int ksplit,
+                                                       int64_t out_rows, int64_t rows_per_head,
+                                                       int hq, int hkv,
+                                                       const int32_t* __restrict__ qflag,
+                                                       const int32_t* __restrict__ kflag,
+                                                       double* __restrict__ mstat,
+                                                       double* __restrict__ lstat) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= out_rows) return;
+  const int bhq = static_cast<int>(r / rows_per_head);
+  const int b = bhq / hq, h = bhq % hq;
+  if (qflag[bhq] | kflag[b * hkv + h / (hq / hkv)]) return;
+  double m = -INFINITY;
+  for (int s = 0; s < ksplit; ++s) m = fmax(m, pm[s * out_rows + r]);
+  double l = 0.0;
+  for (int s = 0; s < ksplit; ++s) {
+    const double ms = pm[s * out_rows + r];
+    if (ms != -INFINITY) l = __dadd_rn(l, __dmul_rn(pl[s * out_rows + r], exp(__dsub_rn(ms, m))));
+  }
+  mstat[r] = m;
+  lstat[r] = l;
 }
 
 // ------------------------------------------------------------------ host side
@@ -731,7 +771,7 @@ static int xl_encode(CUtensorMap* m, const void* base, uint64_t rows, uint32_t b
 }
 
 XlGeometry xl_geometry(int64_t bhq, int64_t bkv, int n_q, int n_k, int classes, int rows_per_class,
-                       int per) {
+                       int per, int64_t out_rows) {
   XlGeometry g{};
   g.ok = per >= 1 && per <= kXlHalf;
   if (!g.ok) return g;
@@ -740,6 +780,12 @@ XlGeometry xl_geometry(int64_t bhq, int64_t bkv, int n_q, int n_k, int classes, 
   g.n_halves = (n_k + g.bpt - 1) / g.bpt;
   g.n_tiles = (g.n_halves + 1) / 2;
   g.kp = g.n_tiles * kXlKeys;
+  // Key tiles per CTA ~48: a fixed property of the layout (not of the head count), so the grid
+  // stays full when few heads run per GPU and every configuration merges the same way.
+  g.ksplit = std::max(1, std::min(8, (g.n_tiles + 24) / 48));
+  g.tps = (g.n_tiles + g.ksplit - 1) / g.ksplit;
+  g.ksplit = (g.n_tiles + g.tps - 1) / g.tps;
+  g.out_rows = out_rows;
   g.rq_pad = (rows_per_class + kXlQRows - 1) / kXlQRows * kXlQRows;
   g.classes = classes;
   const size_t qs = static_cast<size_t>(bhq) * classes * kXlSlices * g.rq_pad * kXlRowBytes;
@@ -750,7 +796,8 @@ XlGeometry xl_geometry(int64_t bhq, int64_t bkv, int n_q, int n_k, int classes, 
   g.off_qm = g.off_ks + ks;
   g.off_km = g.off_qm + qm;
   g.off_flags = g.off_km + km;
-  g.bytes = g.off_flags + static_cast<size_t>(bhq + bkv) * sizeof(int32_t);
+  g.off_part = (g.off_flags + static_cast<size_t>(bhq + bkv) * sizeof(int32_t) + 255) / 256 * 256;
+  g.bytes = g.off_part + (g.ksplit > 1 ? 2 * static_cast<size_t>(g.ksplit) * out_rows * sizeof(double) : 0);
   g.bytes = (g.bytes + 255) / 256 * 256;
   return g;
 }
@@ -803,6 +850,11 @@ static int xl_launch(const void* q, const void* k, int64_t batch, int hq, int hk
   p.rq_pad = g.rq_pad;
   p.kp = g.kp;
   p.n_tiles = g.n_tiles;
+  p.ksplit = g.ksplit;
+  p.tps = g.tps;
+  p.out_rows = g.out_rows;
+  p.pm = reinterpret_cast<double*>(base + g.off_part);
+  p.pl = p.pm + static_cast<int64_t>(g.ksplit) * g.out_rows;
   p.n_chunks = g.n_halves;
   p.per = g.per;
   p.bpt = g.bpt;
@@ -822,8 +874,12 @@ static int xl_launch(const void* q, const void* k, int64_t batch, int hq, int hk
   const size_t smem = sizeof(XlSmem<D>);
   auto kern = g.per == 8 ? xl_stats_kernel<D, QR, KR, MODE, 8> : xl_stats_kernel<D, QR, KR, MODE, 0>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  kern<<<dim3(g.rq_pad / kXlQRows, bhq, g.classes), kXlThreads, smem, s>>>(maps, p, qr, kr);
-  return psa_check_launch("xl_stats_kernel");
+  kern<<<dim3(g.rq_pad / kXlQRows, bhq, g.classes * g.ksplit), kXlThreads, smem, s>>>(maps, p, qr, kr);
+  rc = psa_check_launch("xl_stats_kernel");
+  if (rc || g.ksplit == 1) return rc;
+  xl_merge_kernel<<<static_cast<unsigned>((g.out_rows + 255) / 256), 256, 0, s>>>(
+      p.pm, p.pl, g.ksplit, g.out_rows, g.out_rows / bhq, hq, hkv, qflag, kflag, mstat, lstat);
+  return psa_check_launch("xl_merge_kernel");
 }
 
 int xl_sampled_max(const void* q, const void* k, int64_t batch, int hq, int hkv, int64_t n, int d,
