@@ -780,9 +780,9 @@ XlGeometry xl_geometry(int64_t bhq, int64_t bkv, int n_q, int n_k, int classes, 
   g.n_halves = (n_k + g.bpt - 1) / g.bpt;
   g.n_tiles = (g.n_halves + 1) / 2;
   g.kp = g.n_tiles * kXlKeys;
-  // Key tiles per CTA ~48: a fixed property of the layout (not of the head count), so the grid
+  // Key tiles per CTA ~32: a fixed property of the layout (not of the head count), so the grid
   // stays full when few heads run per GPU and every configuration merges the same way.
-  g.ksplit = std::max(1, std::min(8, (g.n_tiles + 24) / 48));
+  g.ksplit = std::max(1, std::min(8, (g.n_tiles + 16) / 32));
   g.tps = (g.n_tiles + g.ksplit - 1) / g.ksplit;
   g.ksplit = (g.n_tiles + g.tps - 1) / g.tps;
   g.out_rows = out_rows;
