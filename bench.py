@@ -342,7 +342,10 @@ def main():
     stream = torch.cuda.current_stream(device)
 
     stage_names = ("pyramid", "importance", "assign", "attention")
-    launches_per_step = (1 + 2 + 1 + 1 + (1 if cfg["sim"] else 0)) * max(1, len(segs))
+    # pyramid 1; importance 6 (2 int8 slicers, xl_stats, xl_merge, the fp64 fallback kernel that
+    # exits for unflagged heads, finalize); similarity caps 1 if on; assign 1; attention 1 -- per
+    # uniform-GQA segment
+    launches_per_step = (1 + 6 + (1 if cfg["sim"] else 0) + 1 + 1) * max(1, len(segs))
     sim = SimThresholds(cfg["sim"]) if cfg["sim"] else None
 
     def step(events=None):
