@@ -334,6 +334,19 @@ def _with_tiny(x, rng, rows, per_row):
     ("antidiag", 4096, 128, 64, 8), ("antidiag", 3840, 128, 120, 4), ("antidiag", 1920, 64, 120, 8)])
 @pytest.mark.parametrize("tiny", [0, 2, 6, -1])
 def test_int8_exact_logits_match_fp64_path(kind, n, d, b, sk_or_stride, tiny):
+    _int8_vs_fp64(kind, n, d, b, sk_or_stride, tiny)
+
+
+@pytest.mark.parametrize("kind,n,d,b,sk_or_stride", [
+    ("sampled", 12288, 64, 64, 8), ("antidiag", 12288, 64, 64, 8)])
+@pytest.mark.parametrize("tiny", [0, 6])
+def test_int8_key_split_merge(kind, n, d, b, sk_or_stride, tiny):
+    """Sizes whose key tiles are split over several CTAs (xl_merge_kernel combines the per-split
+    (m, l)); with tiny=6 one head is flagged and left to the fp64 kernel by the merge."""
+    _int8_vs_fp64(kind, n, d, b, sk_or_stride, tiny)
+
+
+def _int8_vs_fp64(kind, n, d, b, sk_or_stride, tiny):
     """The int8 tensor-core logits (psa_xlogits.cu) reproduce the fp64 DMMA path: scores agree to
     a few ulps (only the softmax-denominator summation order differs), level maps exactly, and
     both match the oracle at 1e-12. tiny=2: exact corrections; tiny=6: fp64 fallback heads;
