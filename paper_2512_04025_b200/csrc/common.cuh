@@ -266,18 +266,12 @@ PSA_DEV float ex2_approx(float x) {
   return y;
 }
 
-// Exact round-to-nearest-even of a double to bf16 (no double rounding through fp32):
-// truncate to fp32 (RZ), remember whether anything was dropped, then round the fp32
-// bit pattern at bf16 precision with that sticky bit.
+// Exact round-to-nearest-even of a double to bf16 with ONE rounding (no double rounding through
+// fp32): cvt.rn.bf16.f64, a single F2F.BF16.F64 on sm_100a.
 PSA_DEV uint16_t dbl_to_bf16_bits(double x) {
-  float f = __double2float_rz(x);
-  bool sticky = static_cast<double>(f) != x;
-  uint32_t b = __float_as_uint(f);
-  uint32_t lsb = (b >> 16) & 1u;
-  uint32_t rb = b & 0xFFFFu;
-  uint32_t hi = b >> 16;
-  if (rb > 0x8000u || (rb == 0x8000u && (sticky || lsb))) hi += 1u;
-  return static_cast<uint16_t>(hi);
+  uint16_t r;
+  asm("cvt.rn.bf16.f64 %0, %1;" : "=h"(r) : "d"(x));
+  return r;
 }
 
 PSA_DEV double bf16_bits_to_dbl(uint16_t h) {
