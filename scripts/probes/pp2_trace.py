@@ -1,4 +1,5 @@
-"""Per-tile event trace of psa_attn_pp2_kernel. Apply scripts/probes/pp2_trace.patch first (adds
+"""Per-tile event trace of psa_attn_pp2_kernel. Apply scripts/probes/pp2_trace.patch to
+psa_attention.cu as of commit 4e7e050 (`git checkout 4e7e050 -- paper_2512_04025_b200/csrc`) first (adds
 the PSA_PP2_VAR=4|5 builds that record clock64 stamps for 8 CTAs mid-grid): MMA S/PV issue, lane
 S-ready / wait-start / P-done, K TMA issue, K/V ready at the MMA warp. cfg3 shapes."""
 import ctypes
