@@ -294,15 +294,16 @@ def test_pipeline_level_map_and_output(case):
 
 
 # ------------------------------------------------------------------ host staging (e2e API)
-@pytest.mark.parametrize("hq,hkv,causal,per_group", [(6, 6, False, 2), (8, 2, True, 1),
-                                                      (3, 3, False, None)])
-def test_staged_host_path_bit_identical(hq, hkv, causal, per_group):
+@pytest.mark.parametrize("hq,hkv,causal,per_group,batch", [
+    (6, 6, False, 2, 1), (8, 2, True, 1, 1), (3, 3, False, None, 1), (4, 2, False, None, 2)])
+def test_staged_host_path_bit_identical(hq, hkv, causal, per_group, batch):
     """psa_attention on host tensors (pipelined H2D/compute/D2H over head groups) returns exactly
     the device path's O, lse, level map and counts."""
     psa = _psa()
     n, d, b = 2048, 128, 64
-    q, k, v = gaussian_qkv(11, hq, n, d, kv_heads=hkv)
-    qh, kh, vh = (torch.from_numpy(x).to(torch.bfloat16).unsqueeze(0) for x in (q, k, v))
+    q, k, v = gaussian_qkv(11, hq * batch, n, d, kv_heads=hkv * batch)
+    qh, kh, vh = (torch.from_numpy(x).to(torch.bfloat16).reshape(batch, -1, n, d)
+                  for x in (q, k, v))
     kw = dict(b_q=b, b_k=b, levels=4, estimator="sampled-max", s_q=8, s_k=8, seed=0,
               mask="threshold", thresholds=TAUS_CFG1, causal=causal)
     dev = psa.psa_attention(qh.cuda(), kh.cuda(), vh.cuda(), **kw)
