@@ -150,23 +150,28 @@ PSA_DEV void emit_plan_row(const int8_t* lvl, int n_k, int levels, int b_k, int6
 }
 
 // Descending stable order of a row of n_k <= 128*IPT non-negative scores (numpy's stable argsort
-// of -s, mask.py:107-109): a CUB block radix sort of the fp64 bit patterns (monotone for
-// non-negative values; -0.0 is folded into +0.0 first, as the comparison-based sort treats
-// them as equal) with the column index as payload. Radix sort is stable, so equal scores keep
-// ascending column order; padding keys (0) follow every real score, zeros included.
-template <int IPT, int RB = 5>  // 5-bit digits: 1.62 ms vs 1.70 (6) and 2.53 (7) at cfg3
+// of -s, mask.py:107-109). The fp64 bit patterns are monotone for non-negative values (-0.0 is
+// folded into +0.0 first, as the comparison-based sort treats them as equal). A CUB block radix
+// sort orders the rows by the top 32 of the 63 value bits with the column index as payload
+// (7 passes instead of 13); radix sort is stable, so equal keys keep ascending column order.
+// Entries whose top 32 bits tie but whose low bits differ (rare) are then put in full order by
+// an insertion pass with the same (value desc, column asc) comparator. Padding keys (0) follow
+// every real score, zeros included.
+template <int IPT, int RB = 5>  // 5-bit digits
 __global__ void __launch_bounds__(128) assign_levels_kernel(
     const double* __restrict__ S, const int8_t* __restrict__ caps, AssignParams p,
     int8_t* __restrict__ level_map, uint16_t* __restrict__ csr, int32_t* __restrict__ info,
     unsigned long long* __restrict__ level_counts) {
-  using Sort = cub::BlockRadixSort<unsigned long long, 128, IPT, int, RB>;
+  using Sort = cub::BlockRadixSort<unsigned int, 128, IPT, int, RB>;
   __shared__ typename Sort::TempStorage sort_tmp;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* keys = reinterpret_cast<double*>(smem_raw);
   int* idx = reinterpret_cast<int*>(keys + p.n_pad);
   int8_t* lsorted = reinterpret_cast<int8_t*>(idx + p.n_pad);
   int8_t* lvl = lsorted + p.n_pad;
+  double* row_s = reinterpret_cast<double*>(smem_raw + static_cast<size_t>(p.n_pad) * 14 + 16);
   __shared__ double total_s;
+  __shared__ int unsorted_s;
   __shared__ int warp_tot[4];
 
   const int i = blockIdx.x;
@@ -174,21 +179,43 @@ __global__ void __launch_bounds__(128) assign_levels_kernel(
   const int64_t unit = bhq * p.n_q + i;
   const double* row = S + unit * p.n_k;
   {
-    unsigned long long kb[IPT];
+    unsigned int kb[IPT];
     int vb[IPT];
+    if (threadIdx.x == 0) unsorted_s = 0;
 #pragma unroll
     for (int e = 0; e < IPT; ++e) {  // blocked arrangement: thread t holds [t*IPT, t*IPT+IPT)
       const int t = threadIdx.x * IPT + e;
-      const double x = t < p.n_k ? row[t] : 0.0;
-      kb[e] = static_cast<unsigned long long>(__double_as_longlong(x == 0.0 ? 0.0 : x));
+      double x = t < p.n_k ? row[t] : 0.0;
+      x = x == 0.0 ? 0.0 : x;
+      row_s[t] = x;
+      kb[e] = static_cast<unsigned int>(static_cast<unsigned long long>(__double_as_longlong(x)) >> 31);
       vb[e] = t;
     }
-    Sort(sort_tmp).SortDescending(kb, vb, 0, 63);  // sign bit is 0: 63 key bits
+    Sort(sort_tmp).SortDescending(kb, vb, 0, 32);  // value bits 62..31
+    __syncthreads();  // row_s complete
 #pragma unroll
     for (int e = 0; e < IPT; ++e) {
       const int t = threadIdx.x * IPT + e;
-      keys[t] = __longlong_as_double(static_cast<long long>(kb[e]));
+      keys[t] = row_s[vb[e]];
       idx[t] = vb[e];
+    }
+  }
+  __syncthreads();
+  for (int t = 1 + threadIdx.x; t < p.n_pad; t += blockDim.x)  // low-bit ties out of order?
+    if (__double_as_longlong(keys[t]) > __double_as_longlong(keys[t - 1])) unsorted_s = 1;
+  __syncthreads();
+  if (unsorted_s && threadIdx.x == 0) {  // rare: insertion pass, (value desc, column asc)
+    for (int t = 1; t < p.n_pad; ++t) {
+      const double kv = keys[t];
+      const int iv = idx[t];
+      int u = t;
+      while (u > 0 && (keys[u - 1] < kv || (keys[u - 1] == kv && idx[u - 1] > iv))) {
+        keys[u] = keys[u - 1];
+        idx[u] = idx[u - 1];
+        --u;
+      }
+      keys[u] = kv;
+      idx[u] = iv;
     }
   }
   __syncthreads();
@@ -333,7 +360,7 @@ extern "C" int psa_assign_levels(const double* scores, int64_t batch, int hq, in
     }
   const int n_pad = 128 * ipt;
   p.n_pad = n_pad;
-  const size_t smem = static_cast<size_t>(n_pad) * (8 + 4 + 1) + n_k + 16;
+  const size_t smem = static_cast<size_t>(n_pad) * 14 + 16 + static_cast<size_t>(n_pad) * 8;
   dim3 grid(n_q, static_cast<unsigned>(batch * hq));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   auto launch = [&](auto kern) {

@@ -134,6 +134,22 @@ def test_assign_random_rows_match_oracle(rng):
         assert np.array_equal(g, orc.assign_quantile(s, pts)), name
 
 
+def test_assign_low_bit_ties_match_oracle(rng):
+    """Scores equal in their top 32 value bits and different below (the radix sort keys on the
+    top 32 bits; the insertion pass orders these): same levels as numpy's stable argsort, also
+    with exact duplicates mixed in."""
+    psa = _psa()
+    taus = (0.2, 0.45, 0.7, 0.9)
+    base = rng.random((64, 1)) * 0.01 + 0.001
+    s = base * (1.0 + rng.integers(0, 1 << 12, size=(64, 300)) * 2.0 ** -45)
+    s[:, ::5] = s[:, 1::5]  # exact duplicates
+    s = s[:, :300]
+    rows = [s, np.concatenate([s[:, :150], rng.random((64, 150))], axis=1)]
+    for x in rows:
+        got = psa.assign_threshold(torch.from_numpy(x).cuda(), psa.LevelThresholds(taus))
+        assert np.array_equal(got.cpu().numpy(), orc.assign_threshold(x, taus))
+
+
 # ------------------------------------------------------------------ attention kernel
 def _attention_case(q, k, v, mask, lay_args, causal=False, check_e2e=True):
     psa = _psa()
