@@ -27,28 +27,43 @@ struct AssignParams {
   int n_q, n_k, hq, hkv, b_q, b_k, levels, causal, n_pad;
 };
 
-// Extract `cnt` (<= 53) bits starting at bit `lo` of a 256-bit little-endian limb array.
+// Bits [lo, lo + cnt) (cnt <= 53) of a 256-bit little-endian limb array; bits below 0 read 0.
 PSA_DEV uint64_t bits256(const uint32_t (&w)[8], int lo, int cnt) {
-  uint64_t r = 0;
-  for (int b = 0; b < cnt; ++b) {
-    const int pos = lo + b;
-    if (pos >= 0 && pos < 256) r |= static_cast<uint64_t>((w[pos >> 5] >> (pos & 31)) & 1u) << b;
+  auto word = [&](int i) -> uint64_t { return (i >= 0 && i < 8) ? w[i] : 0u; };
+  uint64_t v;
+  if (lo >= 0) {
+    const int i = lo >> 5, sh = lo & 31;
+    v = (word(i) | (word(i + 1) << 32)) >> sh;
+    if (sh) v |= word(i + 2) << (64 - sh);
+  } else {
+    v = (lo > -64) ? (word(0) | (word(1) << 32)) << (-lo) : 0u;
   }
-  return r;
+  return cnt >= 64 ? v : (v & ((1ull << cnt) - 1ull));
+}
+// Any bit set below bit `lo` (lo may be <= 0 or >= 256).
+PSA_DEV bool any_below(const uint32_t (&w)[8], int lo) {
+  if (lo <= 0) return false;
+  const int full = min(lo >> 5, 8);
+  bool any = false;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) any = any || (i < full && w[i] != 0u);
+  if (full < 8 && (lo & 31)) any = any || (w[full] & ((1u << (lo & 31)) - 1u)) != 0u;
+  return any;
 }
 
 // Correctly rounded (half-to-even) sum of n non-negative finite doubles, sorted descending
-// (v[0] is the maximum). Executed by one full warp; the result is returned on every lane.
-// Equivalent to CPython math.fsum for this input class.
-PSA_DEV double exact_sum_sorted_nonneg(const double* v, int n) {
-  const int lane = threadIdx.x & 31;
+// (v[0] is the maximum). Called by the whole 128-thread block (red: 4 x 8 shared limbs); every
+// thread gets the result. Equivalent to CPython math.fsum for this input class.
+PSA_DEV double exact_sum_sorted_nonneg(const double* v, int n, unsigned long long* red,
+                                       int* sticky_s) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double vmax = v[0];
   if (!(vmax > 0.0)) return 0.0;
   const int emax = ilogb(vmax);
   const int lsb = emax - 243;  // window bit 0 weight 2^lsb; sum < 2^(emax+13) <= 2^(lsb+256)
   uint64_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   bool sticky = false;
-  for (int i = lane; i < n; i += 32) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const uint64_t bits = __double_as_longlong(v[i]);
     const int e = static_cast<int>((bits >> 52) & 0x7FF);
     uint64_t m = bits & 0xFFFFFFFFFFFFFull;
@@ -80,6 +95,21 @@ PSA_DEV double exact_sum_sorted_nonneg(const double* v, int n) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc[L] += __shfl_xor_sync(0xffffffffu, acc[L], o);
   sticky = __any_sync(0xffffffffu, sticky);
+  if (threadIdx.x == 0) *sticky_s = 0;
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int L = 0; L < 8; ++L) red[warp * 8 + L] = acc[L];
+    if (sticky) atomicOr(sticky_s, 1);
+  }
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+#pragma unroll
+  for (int L = 0; L < 8; ++L) {
+    acc[L] = 0;
+    for (int w2 = 0; w2 < nw; ++w2) acc[L] += red[w2 * 8 + L];  // < 2^41 per limb: no overflow
+  }
+  sticky = *sticky_s != 0;
   uint32_t w[8];
   uint64_t carry = 0;
 #pragma unroll
@@ -95,8 +125,7 @@ PSA_DEV double exact_sum_sorted_nonneg(const double* v, int n) {
   if (lsb + p < -1022) r = max(r, -1074 - lsb);  // subnormal result
   uint64_t mant = bits256(w, r, p - r + 1);
   const bool rbit = bits256(w, r - 1, 1) != 0;
-  bool st = sticky;
-  for (int b = 0; b < r - 1 && !st; ++b) st = ((w[b >> 5] >> (b & 31)) & 1u) != 0;
+  const bool st = sticky || any_below(w, r - 1);
   if (rbit && (st || (mant & 1ull))) mant += 1;
   return ldexp(static_cast<double>(mant), lsb + r);
 }
@@ -172,6 +201,8 @@ __global__ void __launch_bounds__(128) assign_levels_kernel(
   double* row_s = reinterpret_cast<double*>(smem_raw + static_cast<size_t>(p.n_pad) * 14 + 16);
   __shared__ double total_s;
   __shared__ int unsorted_s;
+  __shared__ unsigned long long red_s[4 * 8];
+  __shared__ int sticky_s;
   __shared__ int warp_tot[4];
 
   const int i = blockIdx.x;
@@ -221,8 +252,8 @@ __global__ void __launch_bounds__(128) assign_levels_kernel(
   __syncthreads();
 
   if (p.rule.mode == 0) {
-    if (threadIdx.x < 32) {
-      const double tot = exact_sum_sorted_nonneg(keys, p.n_k);  // math.fsum(row)
+    {
+      const double tot = exact_sum_sorted_nonneg(keys, p.n_k, red_s, &sticky_s);  // math.fsum(row)
       if (threadIdx.x == 0) total_s = tot;
     }
     __syncthreads();
