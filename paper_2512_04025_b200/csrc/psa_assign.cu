@@ -265,14 +265,16 @@ __global__ void __launch_bounds__(128) assign_levels_kernel(
     if (threadIdx.x == 0) {
       // The recurrence is inherently sequential; keep only it on one thread and store
       // cum_t in place of e_t (read just before it is overwritten).
-      double total = 0.0, comp = 0.0;
-#pragma unroll 4
-      for (int t = 0; t < p.n_k; ++t) {
+      // t = 0: total = 0 < x (the else branch of Neumaier's |total| >= |x| test); for t >= 1 the
+      // test always holds since the values are sorted descending and non-negative (total >=
+      // x_{t-1} >= x_t), so the loop carries no compare or select.
+      double total = keys[0], comp = 0.0;  // fl(0 + x0) = x0, d = (x0 - x0) + 0 = 0
+      keys[0] = fmin(total, 1.0);
+#pragma unroll 8
+      for (int t = 1; t < p.n_k; ++t) {
         const double x = keys[t];
         const double tt = __dadd_rn(total, x);
-        const double d = fabs(total) >= fabs(x) ? __dadd_rn(__dsub_rn(total, tt), x)
-                                                : __dadd_rn(__dsub_rn(x, tt), total);
-        comp = __dadd_rn(comp, d);
+        comp = __dadd_rn(comp, __dadd_rn(__dsub_rn(total, tt), x));
         total = tt;
         keys[t] = fmin(__dadd_rn(total, comp), 1.0);
       }
