@@ -356,21 +356,35 @@ __global__ void __launch_bounds__(kImpThreads, 2)
   }
 }
 
-// S_ij = (sum_{p < b_q} E[p, j] * exp(m_c(p, j) - m_p) / l_p) / b_q, p ascending
+// S_ij = (sum_{p < b_q} E[p, j] * w(p, c) ) / b_q, p ascending, with one weight
+// w = exp(m_c - m_p) / l_p per (row, chunk) shared by the chunk's bpc blocks (one thread per
+// chunk): an exp and a division per (row, chunk) instead of per (row, block).
 __global__ void __launch_bounds__(128) antidiag_finalize_kernel(
     const double* __restrict__ E, const double* __restrict__ Mc, const double* __restrict__ mstat,
     const double* __restrict__ lstat, int64_t n, int b_q, int n_q, int n_k, int bpc, int n_chunks,
     double* __restrict__ S) {
   const int i = blockIdx.x;
   const int64_t bhq = blockIdx.y;
-  for (int j = threadIdx.x; j < n_k; j += blockDim.x) {
-    double acc = 0.0;
+  constexpr int kMaxBpc = 8;  // blocks per work item (a chunk of bpc > 8 blocks spans several)
+  const int subs = (bpc + kMaxBpc - 1) / kMaxBpc;
+  for (int it = threadIdx.x; it < n_chunks * subs; it += blockDim.x) {
+    const int c = it / subs, sub = it % subs;
+    const int j0 = c * bpc + sub * kMaxBpc;
+    const int nb = min(min(kMaxBpc, bpc - sub * kMaxBpc), n_k - j0);
+    double acc[kMaxBpc];
+#pragma unroll
+    for (int u = 0; u < kMaxBpc; ++u) acc[u] = 0.0;
+#pragma unroll 4
     for (int p = 0; p < b_q; ++p) {
       const int64_t a = bhq * n + static_cast<int64_t>(i) * b_q + p;
-      const double w = exp(__dsub_rn(Mc[a * n_chunks + j / bpc], mstat[a]));
-      acc = __dadd_rn(acc, __ddiv_rn(__dmul_rn(E[a * n_k + j], w), lstat[a]));
+      const double w = __ddiv_rn(exp(__dsub_rn(Mc[a * n_chunks + c], mstat[a])), lstat[a]);
+#pragma unroll
+      for (int u = 0; u < kMaxBpc; ++u)
+        if (u < nb) acc[u] = __dadd_rn(acc[u], __dmul_rn(E[a * n_k + j0 + u], w));
     }
-    S[(bhq * n_q + i) * n_k + j] = __ddiv_rn(acc, static_cast<double>(b_q));
+#pragma unroll
+    for (int u = 0; u < kMaxBpc; ++u)
+      if (u < nb) S[(bhq * n_q + i) * n_k + j0 + u] = __ddiv_rn(acc[u], static_cast<double>(b_q));
   }
 }
 
