@@ -255,7 +255,8 @@ def test_mask_validation():
 
 # ------------------------------------------------------------------ fused pipeline
 @pytest.mark.parametrize("case", ["cfg1", "wan_small", "quantile", "binary", "simcap", "causal_gqa",
-                                  "mean", "antidiag_gqa_causal", "antidiag_wan"])
+                                  "mean", "antidiag_gqa_causal", "antidiag_wan",
+                                  "grid_causal_gqa"])
 def test_pipeline_level_map_and_output(case):
     psa = _psa()
     kw = dict(estimator="sampled-max", s_q=8, s_k=8, seed=0, mask="threshold",
@@ -286,6 +287,10 @@ def test_pipeline_level_map_and_output(case):
     elif case == "antidiag_wan":
         n, d, b, H = 3840, 128, 120, 4
         kw.update(estimator="antidiagonal", stride=8, thresholds=(0.1634, 0.2803, 0.3738, 0.95))
+    elif case == "grid_causal_gqa":  # curve permutation (fused gathers / scatter) + causal + GQA
+        n, d, b, H = 2048, 128, 64, 4
+        kw.update(causal=True, grid=(8, 16, 16), unpermute=True)
+        hq, hkv = 4, 2
     else:
         n, d, b, H = 4096, 64, 64, 4
         kw["estimator"] = "sampled-mean"
@@ -298,7 +303,9 @@ def test_pipeline_level_map_and_output(case):
     lm = res.level_map.cpu().numpy()[0]
     lay = orc.Layout(n, d, b, b, H)
     okw = {x: kw.get(x) for x in ("estimator", "s_q", "s_k", "seed", "mask", "thresholds",
-                                  "cutpoints", "tau", "sim_thresholds", "causal", "stride")}
+                                  "cutpoints", "tau", "sim_thresholds", "causal", "stride",
+                                  "grid")}
+    okw["unpermute"] = bool(kw.get("unpermute", False))
     out = res.out.float().cpu().numpy()
     mism = 0
     for h in range(hq):
