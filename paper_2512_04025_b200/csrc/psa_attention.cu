@@ -619,6 +619,378 @@ static int launch_attn(const void* q, const void* k, const void* v, const void* 
   return psa_check_launch("psa_attn_pp2_kernel");
 }
 
+
+// ====================================================================== backward dQ (tcgen05)
+// dQ of the multi-level attention for a fixed mask (psa_backward.cu has the derivation): the
+// same work unit, plan walk and K/V producers as the forward, with
+//   S = Q K^T and dP = dO V^T (SS MMAs into TMEM), P = exp2(S c + (h-1) - lse2) (lse known: no
+//   running max), dS = P (dP - D) -> shared memory (128B-swizzled like P), dQ += dS K (K read
+//   MN-major like V in the forward's PV).
+// Two softmax warpgroups split the 128 key columns of a tile (no cross-warp exchange is needed
+// since the row statistics are final). TMEM: S0 | S1 | dP | dQ (512 columns at D = 128).
+struct BwdQSmem {
+  uint8_t q[kTileRows * 128 * 2];
+  uint8_t dout[kTileRows * 128 * 2];
+  uint8_t k[2][kTileRows * 128 * 2];
+  uint8_t v[2][kTileRows * 128 * 2];
+  uint8_t ds[kTileRows * kTileRows * 2];
+  float bias[kMetaRing][kTileRows];
+  uint32_t meta[kMetaRing][kChunks];
+  uint64_t q_full;
+  uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
+  uint64_t meta_full[kMetaRing], meta_empty[kMetaRing];
+  uint64_t s_full[2], sp_read, ds_full, ds_free, dq_done;
+  uint32_t tmem_base;
+};
+
+struct BwdQMaps {
+  AttnMaps a;  // q, k[], v[]
+  CUtensorMap dout;
+};
+
+__global__ void __launch_bounds__(kPPThreads, 1)
+    psa_bwd_dq_tc_kernel(const __grid_constant__ BwdQMaps maps, const AttnParams p,
+                         const uint16_t* __restrict__ csr, const int32_t* __restrict__ info,
+                         const float* __restrict__ lse, const float* __restrict__ drow,
+                         float scale, uint16_t* __restrict__ dq) {
+  constexpr int D = 128;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  auto& sm = *reinterpret_cast<BwdQSmem*>(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t unit = blockIdx.x;
+  const int bhq = static_cast<int>(unit / p.n_q);
+  const int i = static_cast<int>(unit % p.n_q);
+  const int b = bhq / p.hq, hh = bhq % p.hq;
+  const int64_t bhkv = static_cast<int64_t>(b) * p.hkv + hh / (p.hq / p.hkv);
+  const int n_ent = info[unit * 2 + 0];
+  const int T = (info[unit * 2 + 1] + kTileRows - 1) / kTileRows;
+  const int64_t q_row0 = static_cast<int64_t>(bhq) * p.n + static_cast<int64_t>(i) * p.b_q;
+  constexpr uint32_t kDP = 256, kDQ = 384;
+
+  if (threadIdx.x == 0) {
+    if (smem_u32(smem_raw) & 1023u) __trap();
+    mbar_init(&sm.q_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&sm.k_full[s], 1);
+      mbar_init(&sm.k_empty[s], 1);
+      mbar_init(&sm.v_full[s], 1);
+      mbar_init(&sm.v_empty[s], 1);
+      mbar_init(&sm.s_full[s], 1);
+    }
+    for (int s = 0; s < kMetaRing; ++s) {
+      mbar_init(&sm.meta_full[s], 1);
+      mbar_init(&sm.meta_empty[s], 8);  // one arrive per softmax warp
+    }
+    mbar_init(&sm.sp_read, 8);
+    mbar_init(&sm.ds_full, 8);
+    mbar_init(&sm.ds_free, 1);
+    mbar_init(&sm.dq_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    tmem_alloc(&sm.tmem_base, 512);
+    tmem_relinquish();
+  }
+  {  // K/V rows past the last filled slot of a tile are read by the MMAs: keep them finite
+    uint4* z = reinterpret_cast<uint4*>(&sm.k[0][0]);
+    const int nvec = 4 * kTileRows * 128 * 2 / 16;
+    for (int t = threadIdx.x; t < nvec; t += kPPThreads) z[t] = make_uint4(0, 0, 0, 0);
+    fence_proxy_async_smem();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp < 4) {
+    regs_dec<64>();
+    if (warp == 0) {  // K producer (+ Q, dO)
+      if (T > 0) {
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&sm.q_full, 2 * kTileRows * D * 2);
+          for (int c = 0; c < D / 64; ++c) {
+            tma_load_2d(&maps.a.q, &sm.q_full, sm.q + c * kTileRows * 128, c * 64,
+                        static_cast<int>(q_row0));
+            tma_load_2d(&maps.dout, &sm.q_full, sm.dout + c * kTileRows * 128, c * 64,
+                        static_cast<int>(q_row0));
+          }
+        }
+        PlanCursor pc;
+        pc.init(csr + unit * p.n_k, n_ent, lane);
+        for (int t = 0; t < T; ++t) {
+          const int ks = t & 1;
+          const TileSeg sg = pc.next(p, bhkv, lane);
+          if (t >= 2) mbar_wait(&sm.k_empty[ks], ((t >> 1) - 1) & 1);
+          if (lane == 0) mbar_arrive_expect_tx(&sm.k_full[ks], static_cast<uint32_t>(sg.total) * D * 2);
+          __syncwarp();
+          if (sg.fits)
+            for (int c = 0; c < D / 64; ++c)
+              tma_load_2d(&maps.a.k[sg.h - 1], &sm.k_full[ks],
+                          sm.k[ks] + c * kTileRows * 128 + sg.off * 128, c * 64, sg.row);
+        }
+      }
+    } else if (warp == 3) {  // V producer
+      if (T > 0) {
+        PlanCursor pc;
+        pc.init(csr + unit * p.n_k, n_ent, lane);
+        for (int t = 0; t < T; ++t) {
+          const int vs = t & 1;
+          const TileSeg sg = pc.next(p, bhkv, lane);
+          if (t >= 2) mbar_wait(&sm.v_empty[vs], ((t >> 1) - 1) & 1);
+          if (lane == 0) mbar_arrive_expect_tx(&sm.v_full[vs], static_cast<uint32_t>(sg.total) * D * 2);
+          __syncwarp();
+          if (sg.fits)
+            for (int c = 0; c < D / 64; ++c)
+              tma_load_2d(&maps.a.v[sg.h - 1], &sm.v_full[vs],
+                          sm.v[vs] + c * kTileRows * 128 + sg.off * 128, c * 64, sg.row);
+        }
+      }
+    } else if (warp == 2) {  // bias / causal metadata (as in the forward)
+      if (T > 0) {
+        const int64_t q_lo = static_cast<int64_t>(i) * p.b_q;
+        PlanCursor pc;
+        pc.init(csr + unit * p.n_k, n_ent, lane);
+        for (int t = 0; t < T; ++t) {
+          const int ms = t % kMetaRing;
+          const TileSeg sg = pc.next(p, bhkv, lane);
+          if (t >= kMetaRing) mbar_wait(&sm.meta_empty[ms], ((t / kMetaRing) - 1) & 1);
+          {
+            int g = 0;
+            for (int q = 1; q < sg.nseg; ++q)
+              if (__shfl_sync(0xffffffffu, sg.off, q) <= 4 * lane) g = q;
+            const int goff = __shfl_sync(0xffffffffu, sg.off, g);
+            const int gL = __shfl_sync(0xffffffffu, sg.L, g);
+            const int gh = __shfl_sync(0xffffffffu, sg.h, g);
+            const int r0 = 4 * lane - goff;
+            const float bv = static_cast<float>(gh - 1);
+            float4 w = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+            if (4 * lane < sg.total) {
+              w.x = r0 + 0 < gL ? bv : -INFINITY;
+              w.y = r0 + 1 < gL ? bv : -INFINITY;
+              w.z = r0 + 2 < gL ? bv : -INFINITY;
+              w.w = r0 + 3 < gL ? bv : -INFINITY;
+            }
+            *reinterpret_cast<float4*>(&sm.bias[ms][4 * lane]) = w;
+          }
+          if (p.causal && sg.fits) {
+            const bool straddle = static_cast<int64_t>(sg.j + 1) * p.b_k - 1 > q_lo;
+            for (int c = 0; c < sg.sz / 8; ++c)
+              sm.meta[ms][sg.off / 8 + c] =
+                  (straddle ? 1u : 0u) | (static_cast<uint32_t>(sg.j * p.b_k + c * 8) << 1);
+          }
+          if (p.causal && lane < kChunks && 8 * lane >= sg.total) sm.meta[ms][lane] = 0u;
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.meta_full[ms]);
+        }
+      }
+    } else {  // MMA issuer (warp 1)
+      if (T > 0) {
+        constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128, false, false);
+        constexpr uint32_t idesc_q = umma_idesc_bf16(128, D, false, true);
+        const uint64_t q_desc0 = umma_desc_sw128(smem_u32(sm.q), 16, 1024);
+        const uint64_t do_desc0 = umma_desc_sw128(smem_u32(sm.dout), 16, 1024);
+        const uint64_t ds_desc0 = umma_desc_sw128(smem_u32(sm.ds), 16, 1024);
+        auto issue_sd = [&](int t) {  // S(t) = Q K^T into S[t & 1], dP(t) = dO V^T
+          const int st = t & 1;
+          mbar_wait(&sm.k_full[st], (t >> 1) & 1);
+          mbar_wait(&sm.v_full[st], (t >> 1) & 1);
+          tc_fence_after();
+          const uint64_t k_desc0 = umma_desc_sw128(smem_u32(sm.k[st]), 16, 1024);
+          const uint64_t v_desc0 = umma_desc_sw128(smem_u32(sm.v[st]), 16, 1024);
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk) {
+              const uint32_t koff = ((kk >> 2) * kTileRows * 128 + (kk & 3) * 32) >> 4;
+              mma_bf16_ss(tmem + st * 128, q_desc0 + koff, k_desc0 + koff, idesc_s,
+                          kk > 0 ? 1u : 0u);
+            }
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk) {
+              const uint32_t koff = ((kk >> 2) * kTileRows * 128 + (kk & 3) * 32) >> 4;
+              mma_bf16_ss(tmem + kDP, do_desc0 + koff, v_desc0 + koff, idesc_s,
+                          kk > 0 ? 1u : 0u);
+            }
+            mma_commit(&sm.v_empty[st]);
+            mma_commit(&sm.s_full[st]);
+          }
+          __syncwarp();
+        };
+        mbar_wait(&sm.q_full, 0);
+        tc_fence_after();
+        issue_sd(0);
+        for (int t = 0; t < T; ++t) {
+          const int st = t & 1;
+          if (t + 1 < T) {
+            mbar_wait(&sm.sp_read, t & 1);  // softmax read S(t) and dP(t)
+            issue_sd(t + 1);
+          }
+          mbar_wait(&sm.ds_full, t & 1);
+          tc_fence_after();
+          const uint64_t kmn_desc0 = umma_desc_sw128(smem_u32(sm.k[st]), kTileRows * 128, 1024);
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < kTileRows / 16; ++kk) {
+              const uint32_t poff = ((kk >> 2) * kTileRows * 128 + (kk & 3) * 32) >> 4;
+              mma_bf16_ss(tmem + kDQ, ds_desc0 + poff, kmn_desc0 + ((kk * 16 * 128) >> 4),
+                          idesc_q, (t > 0 || kk > 0) ? 1u : 0u);
+            }
+            mma_commit(&sm.k_empty[st]);
+            mma_commit(&sm.ds_free);
+            if (t + 1 == T) mma_commit(&sm.dq_done);
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else {
+    regs_inc<216>();
+    const int g = (warp - 4) >> 2;  // key columns [64 g, 64 g + 64)
+    const int wq = warp & 3;
+    const int row = wq * 32 + lane;
+    const uint32_t t_lane = tmem + (static_cast<uint32_t>(wq * 32) << 16);
+    const int qpos = i * p.b_q + row;
+    const bool valid = row < p.b_q;
+    const float l = valid ? lse[q_row0 + row] : -INFINITY;
+    const bool live = l != -INFINITY;
+    const float lse2 = live ? l * 1.4426950408889634f : 0.f;
+    const float dd = valid ? drow[q_row0 + row] : 0.f;
+    const float2 scale2 = make_float2(p.scale_log2, p.scale_log2);
+    for (int t = 0; t < T; ++t) {
+      const int st = t & 1, ms = t % kMetaRing;
+      mbar_wait(&sm.s_full[st], (t >> 1) & 1);
+      tc_fence_after();
+      uint32_t sv[2][32], pv[2][32];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) tmem_ld32(t_lane + st * 128 + 64 * g + c * 32, sv[c]);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) tmem_ld32(t_lane + kDP + 64 * g + c * 32, pv[c]);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        tmem_ld_wait(sv[c]);
+        tmem_ld_wait(pv[c]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.sp_read);
+      mbar_wait(&sm.meta_full[ms], (t / kMetaRing) & 1);
+      uint32_t pk[32];
+#pragma unroll
+      for (int e = 0; e < 64; e += 2) {
+        const int col = 64 * g + e;
+        const float* x = reinterpret_cast<const float*>(&sv[e >> 5][e & 31]);
+        const float* y = reinterpret_cast<const float*>(&pv[e >> 5][e & 31]);
+        const float2 bv = *reinterpret_cast<const float2*>(&sm.bias[ms][col]);
+        float2 a = ffma2(make_float2(x[0], x[1]), scale2, bv);
+        a = fadd2(a, make_float2(-lse2, -lse2));
+        float p0 = live ? ex2_approx(a.x) : 0.f, p1 = live ? ex2_approx(a.y) : 0.f;
+        if (p.causal) {
+          const uint32_t w = sm.meta[ms][col >> 3];
+          if (w & 1u) {
+            const int kp = static_cast<int>(w >> 1) + (col & 7);
+            if (kp > qpos) p0 = 0.f;
+            if (kp + 1 > qpos) p1 = 0.f;
+          }
+        }
+        pk[e >> 1] = pack_bf16x2(p0 * (y[0] - dd), p1 * (y[1] - dd));
+      }
+      if (lane == 0) mbar_arrive(&sm.meta_empty[ms]);
+      if (t >= 1) mbar_wait(&sm.ds_free, (t - 1) & 1);  // dQ(t-1) has read the previous dS
+      {  // dS (bf16) -> shared memory, K-major 128B-swizzled: [key half][row][128 B]
+        uint8_t* prow = sm.ds + g * kTileRows * 128 + row * 128;
+        const int sw = row & 7;
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch)
+          *reinterpret_cast<uint4*>(prow + ((ch ^ sw) << 4)) =
+              make_uint4(pk[ch * 4], pk[ch * 4 + 1], pk[ch * 4 + 2], pk[ch * 4 + 3]);
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.ds_full);
+    }
+    if (T > 0) {
+      mbar_wait(&sm.dq_done, 0);
+      tc_fence_after();
+    }
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      uint32_t o[32];
+      if (T > 0) {
+        tmem_ld32(t_lane + kDQ + 64 * g + c * 32, o);
+        tmem_ld_wait(o);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) o[e] = 0u;
+      }
+      if (valid) {
+        uint16_t* orow = dq + (q_row0 + row) * D + 64 * g + c * 32;
+#pragma unroll
+        for (int v4 = 0; v4 < 4; ++v4) {
+          uint32_t w[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            w[u] = pack_bf16x2(__uint_as_float(o[v4 * 8 + 2 * u]) * scale,
+                               __uint_as_float(o[v4 * 8 + 2 * u + 1]) * scale);
+          *reinterpret_cast<uint4*>(orow + v4 * 8) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+int attn_bwd_dq_tc(const void* q, const void* k, const void* v, const void* k_pyr,
+                   const void* v_pyr, const void* dout, const float* lse, const float* drow,
+                   int64_t batch, int hq, int hkv, int64_t n, int b_q, int b_k, int levels,
+                   const uint16_t* csr, const int32_t* info, int causal, void* dq,
+                   cudaStream_t s) {
+  constexpr int D = 128;
+  BwdQMaps maps;
+  memset(&maps, 0, sizeof(maps));
+  AttnParams p{};
+  p.n = n;
+  p.hq = hq;
+  p.hkv = hkv;
+  p.b_q = b_q;
+  p.b_k = b_k;
+  p.levels = levels;
+  p.n_q = static_cast<int>(n / b_q);
+  p.n_k = static_cast<int>(n / b_k);
+  p.causal = causal;
+  p.scale_log2 = static_cast<float>(1.4426950408889634 / sqrt(static_cast<double>(D)));
+  const int64_t bhkv = batch * hkv;
+  int rc = encode_2d(&maps.a.q, q, static_cast<uint64_t>(batch * hq * n), D, kTileRows);
+  if (rc) return rc;
+  rc = encode_2d(&maps.dout, dout, static_cast<uint64_t>(batch * hq * n), D, kTileRows);
+  if (rc) return rc;
+  int64_t off_elems = 0;
+  for (int h = 1; h <= levels; ++h) {
+    const int L = b_k >> (h - 1);
+    int sz = 8;
+    while (sz < L) sz <<= 1;
+    const uint64_t rows = static_cast<uint64_t>(bhkv * (n >> (h - 1)));
+    const void* kb = h == 1 ? k : static_cast<const void*>(static_cast<const uint16_t*>(k_pyr) + off_elems);
+    const void* vb = h == 1 ? v : static_cast<const void*>(static_cast<const uint16_t*>(v_pyr) + off_elems);
+    if (h > 1) off_elems += static_cast<int64_t>(rows) * D;
+    rc = encode_2d(&maps.a.k[h - 1], kb, rows, D, sz);
+    if (rc) return rc;
+    rc = encode_2d(&maps.a.v[h - 1], vb, rows, D, sz);
+    if (rc) return rc;
+  }
+  const size_t smem = sizeof(BwdQSmem);
+  cudaFuncSetAttribute(psa_bwd_dq_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(smem));
+  psa_bwd_dq_tc_kernel<<<static_cast<unsigned>(batch * hq * p.n_q), kPPThreads, smem, s>>>(
+      maps, p, csr, info, lse, drow, static_cast<float>(1.0 / sqrt(static_cast<double>(D))),
+      static_cast<uint16_t*>(dq));
+  return psa_check_launch("psa_bwd_dq_tc_kernel");
+}
+
 }  // namespace psa
 
 using namespace psa;

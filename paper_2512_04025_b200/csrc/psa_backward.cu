@@ -17,10 +17,11 @@
 // add spreads a pooled row's gradient over its 2^(h-1) raw rows, so the work per selected block
 // scales with its pooled length like the forward's.
 //
-// First version: warp-level mma.sync (m16n8k16 bf16, fp32 accumulate) with ldmatrix fragments,
-// one CTA per (head, query block) for dQ and one per (KV head, KV block) for dK/dV (8 warps,
-// 1 CTA per SM at ~230-255 registers, cp.async double-buffered K/V chunks and Q/dO tiles); cfg3
-// backward 839 ms against a 36 ms forward. The tcgen05 / TMEM version is the next step.
+// dQ at D = 128 runs on tcgen05 / TMEM (psa_bwd_dq_tc_kernel in psa_attention.cu: the forward's
+// producers and plan walk, S and dP in TMEM, dS through shared memory; 37 ms at cfg3). The dK/dV
+// pass and D = 64 dQ are warp-level mma.sync (m16n8k16 bf16, fp32 accumulate) with ldmatrix
+// fragments, one CTA per (KV head, KV block) for dK/dV (8 warps, cp.async double-buffered Q/dO
+// tiles): cfg3 backward 537 ms (dK/dV 500 ms) against a 34 ms forward.
 #include "common.cuh"
 #include "psa_internal.h"
 
@@ -571,10 +572,15 @@ static int launch_bwd(BwdParams p, int64_t batch, const uint16_t* out, void* ws,
   const size_t smem_q = 2 * static_cast<size_t>(BwdTile<D>::kBytes) +
                         4 * static_cast<size_t>(kChunkKeys) * BwdTile<D>::kStride * 2 +
                         static_cast<size_t>(p.n_k + 1) * 4 + 2 * kChunkKeys * 8;
-  cudaFuncSetAttribute(bwd_dq_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       static_cast<int>(smem_q));
-  bwd_dq_kernel<D><<<static_cast<unsigned>(batch * p.hq * p.n_q), kBwdThreads, smem_q, s>>>(p);
-  rc = psa_check_launch("bwd_dq_kernel");
+  if (D == 128) {  // tcgen05 / TMEM dQ pass (psa_attention.cu): 37 ms vs ~300 ms at cfg3
+    rc = attn_bwd_dq_tc(p.q, p.k, p.v, p.k_pyr, p.v_pyr, p.dout, p.lse, drow, batch, p.hq, p.hkv,
+                        p.n, p.b_q, p.b_k, p.levels, p.csr, p.info, p.causal, p.dq, s);
+  } else {
+    cudaFuncSetAttribute(bwd_dq_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem_q));
+    bwd_dq_kernel<D><<<static_cast<unsigned>(batch * p.hq * p.n_q), kBwdThreads, smem_q, s>>>(p);
+    rc = psa_check_launch("bwd_dq_kernel");
+  }
   if (rc) return rc;
   const int cap = (p.hq / p.hkv) * p.n_q;
   const size_t smem = 6 * static_cast<size_t>(BwdTile<D>::kBytes) + 4 * kBwdRows * sizeof(float) +

@@ -46,6 +46,13 @@ int xl_antidiag(const void* q, const void* k, int64_t batch, int hq, int hkv, in
 // device flags [bhq] then [bkv]: heads the int8 path could not represent exactly
 const int32_t* xl_qflags(const XlGeometry& g, const void* ws);
 
+// tcgen05 dQ pass of the backward (psa_attention.cu; D = 128)
+int attn_bwd_dq_tc(const void* q, const void* k, const void* v, const void* k_pyr,
+                   const void* v_pyr, const void* dout, const float* lse, const float* drow,
+                   int64_t batch, int hq, int hkv, int64_t n, int b_q, int b_k, int levels,
+                   const uint16_t* csr, const int32_t* info, int causal, void* dq,
+                   cudaStream_t s);
+
 // cuTensorMapEncodeTiled from the driver (psa_attention.cu)
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
