@@ -991,6 +991,399 @@ int attn_bwd_dq_tc(const void* q, const void* k, const void* v, const void* k_py
   return psa_check_launch("psa_bwd_dq_tc_kernel");
 }
 
+
+// ====================================================================== backward dK/dV (tcgen05)
+// One CTA per (KV head, KV block j), as the mma.sync version in psa_backward.cu: the CTA lists
+// (level-major) the (query head, query block) entries that selected block j; per level the
+// pooled block K_h / V_h is one TMA tile (box = slot rows), and per entry
+//   S^T = K_h Q^T and dP^T = V_h dO^T (SS MMAs, pooled keys as M = 128 TMEM lanes),
+//   P'^T = exp2(S^T c - lse2) (unbiased: the raw-row gradient is the duplicate's, see
+//   psa_backward.cu), dS^T = P'^T (dP^T - D) -> shared memory (128B-swizzled, queries as K),
+//   dV_h += P'^T dO and dK_h += dS^T Q (dO / Q read MN-major like V in the forward) in TMEM.
+// At the end of a level the pooled rows are spread over their 2^(h-1) raw rows into the CTA's
+// fp32 scratch rows; the last step writes bf16 dK (x scale) and dV. TMEM: S^T | dP^T | dV | dK.
+struct BwdKVSmem {
+  uint8_t kt[kTileRows * 128 * 2];
+  uint8_t vt[kTileRows * 128 * 2];
+  uint8_t q[2][kTileRows * 128 * 2];     // double-buffered per entry
+  uint8_t dout[2][kTileRows * 128 * 2];
+  float lse2[2][kTileRows];
+  float dd[2][kTileRows];
+  uint64_t kv_full, q_full[2], q_free[2], s_full[2], pds_full[2], acc_done, acc_free;
+  uint32_t tmem_base;
+  int lvl_end[kMaxLevels + 1];
+  int warp_cnt[kPPThreads / 32];
+};
+
+__global__ void __launch_bounds__(kPPThreads, 1)
+    psa_bwd_dkv_tc_kernel(const __grid_constant__ BwdQMaps maps, const AttnParams p,
+                          const int8_t* __restrict__ level_map, const float* __restrict__ lse,
+                          const float* __restrict__ drow, float scale, int cap,
+                          float* __restrict__ scratch, int64_t bkv_total,
+                          uint16_t* __restrict__ dk, uint16_t* __restrict__ dv) {
+  constexpr int D = 128;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  auto& sm = *reinterpret_cast<BwdKVSmem*>(smem_raw);
+  uint32_t* ents = reinterpret_cast<uint32_t*>(smem_raw + sizeof(BwdKVSmem));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j = blockIdx.x;
+  const int64_t bkv = blockIdx.y;
+  const int b = static_cast<int>(bkv / p.hkv), hk = static_cast<int>(bkv % p.hkv);
+  const int group = p.hq / p.hkv;
+  const int span = group * p.n_q;
+  constexpr uint32_t kST = 0, kDPT = 128, kDV = 256, kDK = 384;
+
+  if (threadIdx.x == 0) {
+    if (smem_u32(smem_raw) & 1023u) __trap();
+    mbar_init(&sm.kv_full, 1);
+    for (int u = 0; u < 2; ++u) {
+      mbar_init(&sm.q_full[u], 1);
+      mbar_init(&sm.q_free[u], 1);
+    }
+    for (int u = 0; u < 2; ++u) {  // query halves: one per softmax warpgroup
+      mbar_init(&sm.s_full[u], 1);
+      mbar_init(&sm.pds_full[u], 4);
+    }
+    mbar_init(&sm.acc_done, 1);
+    mbar_init(&sm.acc_free, 8);
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    tmem_alloc(&sm.tmem_base, 512);
+    tmem_relinquish();
+  }
+  {  // tile rows never written by a TMA box are read by the MMAs: keep them finite
+    uint4* z = reinterpret_cast<uint4*>(sm.kt);
+    const int nvec = 2 * kTileRows * 128 * 2 / 16;  // pooled K / V tiles
+    for (int t = threadIdx.x; t < nvec; t += kPPThreads) z[t] = make_uint4(0, 0, 0, 0);
+    fence_proxy_async_smem();
+  }
+  // ---- deterministic level-major list of the entries (query head of the group, query block)
+  int total = 0;
+  for (int h = 1; h <= p.levels; ++h) {
+    for (int base = 0; base < span; base += kPPThreads) {
+      const int x = base + threadIdx.x;
+      bool hit = false;
+      if (x < span) {
+        const int g = x / p.n_q, iq = x % p.n_q;
+        const int64_t bhq = static_cast<int64_t>(b) * p.hq + hk * group + g;
+        hit = level_map[(bhq * p.n_q + iq) * p.n_k + j] == h;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, hit);
+      if (lane == 0) sm.warp_cnt[warp] = __popc(m);
+      __syncthreads();
+      int before = 0, all = 0;
+      for (int w = 0; w < kPPThreads / 32; ++w) {
+        before += w < warp ? sm.warp_cnt[w] : 0;
+        all += sm.warp_cnt[w];
+      }
+      if (hit) {
+        const int slot = total + before + __popc(m & ((1u << lane) - 1u));
+        if (slot < cap) ents[slot] = static_cast<uint32_t>(x);
+      }
+      total += all;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) sm.lvl_end[h] = min(total, cap);
+  }
+  if (threadIdx.x == 0) sm.lvl_end[0] = 0;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+  const int64_t krow0 = bkv * p.n + static_cast<int64_t>(j) * p.b_k;
+  float* sk = scratch + krow0 * D;
+  float* sv = scratch + (bkv_total * p.n + krow0) * D;
+
+  if (warp < 4) {
+    regs_dec<72>();  // 128 x 72 + 256 x 216 = 384 x 168
+    if (warp == 0) {  // producer: pooled K/V per level, Q / dO / lse / D per entry
+      int e_prev = -1;
+      for (int h = 1; h <= p.levels; ++h) {
+        const int e0 = sm.lvl_end[h - 1], e1 = sm.lvl_end[h];
+        if (e0 == e1) continue;
+        if (e_prev >= 0) mbar_wait(&sm.q_free[e_prev & 1], (e_prev >> 1) & 1);  // its MMAs done
+        const int L = p.b_k >> (h - 1);
+        int sz = 8;
+        while (sz < L) sz <<= 1;
+        const int row = static_cast<int>(bkv * (p.n >> (h - 1)) + static_cast<int64_t>(j) * L);
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&sm.kv_full, 2u * sz * D * 2);
+          for (int c = 0; c < D / 64; ++c) {
+            tma_load_2d(&maps.a.k[h - 1], &sm.kv_full, sm.kt + c * kTileRows * 128, c * 64, row);
+            tma_load_2d(&maps.a.v[h - 1], &sm.kv_full, sm.vt + c * kTileRows * 128, c * 64, row);
+          }
+        }
+        for (int e = e0; e < e1; ++e) {
+          const int qb = e & 1;
+          if (e >= 2) mbar_wait(&sm.q_free[qb], ((e >> 1) - 1) & 1);  // entry e-2 done
+          const int x = static_cast<int>(ents[e]);
+          const int g = x / p.n_q, iq = x % p.n_q;
+          const int64_t bhq = static_cast<int64_t>(b) * p.hq + hk * group + g;
+          const int64_t q_row0 = bhq * p.n + static_cast<int64_t>(iq) * p.b_q;
+          for (int r = lane; r < kTileRows; r += 32) {
+            const float l = r < p.b_q ? lse[q_row0 + r] : -INFINITY;
+            sm.lse2[qb][r] = l == -INFINITY ? -INFINITY : l * 1.4426950408889634f;
+            sm.dd[qb][r] = r < p.b_q ? drow[q_row0 + r] : 0.f;
+          }
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive_expect_tx(&sm.q_full[qb], 2u * kTileRows * D * 2);
+            for (int c = 0; c < D / 64; ++c) {
+              tma_load_2d(&maps.a.q, &sm.q_full[qb], sm.q[qb] + c * kTileRows * 128, c * 64,
+                          static_cast<int>(q_row0));
+              tma_load_2d(&maps.dout, &sm.q_full[qb], sm.dout[qb] + c * kTileRows * 128, c * 64,
+                          static_cast<int>(q_row0));
+            }
+          }
+          e_prev = e;
+        }
+      }
+    } else if (warp == 1) {  // MMA issuer
+      // Two query halves ping-pong with the softmax warpgroups: while one half's P'^T / dS^T
+      // is being formed, the tensor core runs the other half's dV / dK and the next entry's S^T.
+      constexpr uint32_t idesc_s = umma_idesc_bf16(128, 64, false, false);
+      constexpr uint32_t idesc_o = umma_idesc_bf16(128, D, false, true);
+      const uint64_t kt_desc = umma_desc_sw128(smem_u32(sm.kt), 16, 1024);
+      const uint64_t vt_desc = umma_desc_sw128(smem_u32(sm.vt), 16, 1024);
+      auto issue_s = [&](int e, int half) {  // S^T / dP^T of queries [64 half, 64 half + 64)
+        const int qb = e & 1;
+        const uint64_t q_desc = umma_desc_sw128(smem_u32(sm.q[qb]), 16, 1024) + ((half * 64 * 128) >> 4);
+        const uint64_t do_desc =
+            umma_desc_sw128(smem_u32(sm.dout[qb]), 16, 1024) + ((half * 64 * 128) >> 4);
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t koff = ((kk >> 2) * kTileRows * 128 + (kk & 3) * 32) >> 4;
+            mma_bf16_ss(tmem + kST + 64 * half, kt_desc + koff, q_desc + koff, idesc_s, kk > 0 ? 1u : 0u);
+          }
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t koff = ((kk >> 2) * kTileRows * 128 + (kk & 3) * 32) >> 4;
+            mma_bf16_ss(tmem + kDPT + 64 * half, vt_desc + koff, do_desc + koff, idesc_s,
+                        kk > 0 ? 1u : 0u);
+          }
+          mma_commit(&sm.s_full[half]);
+        }
+        __syncwarp();
+      };
+      auto issue_acc = [&](int e, int half, bool zero) {  // dV += P'^T dO, dK += dS^T Q (half)
+        const int qb = e & 1;
+        const uint64_t q_mn = umma_desc_sw128(smem_u32(sm.q[qb]), kTileRows * 128, 1024);
+        const uint64_t do_mn = umma_desc_sw128(smem_u32(sm.dout[qb]), kTileRows * 128, 1024);
+        if (elect_one()) {
+          // P'^T / dS^T (bf16 pairs) sit in the first 32 S^T / dP^T columns of the half
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint32_t boff = ((half * 64 + kk * 16) * 128) >> 4;
+            const uint32_t acc = (zero && kk == 0) ? 0u : 1u;
+            mma_bf16_ts(tmem + kDV, tmem + kST + 64 * half + kk * 8, do_mn + boff, idesc_o, acc);
+            mma_bf16_ts(tmem + kDK, tmem + kDPT + 64 * half + kk * 8, q_mn + boff, idesc_o, acc);
+          }
+        }
+        __syncwarp();
+      };
+
+      int lvl = 0;
+      for (int h = 1; h <= p.levels; ++h) {
+        const int e0 = sm.lvl_end[h - 1], e1 = sm.lvl_end[h];
+        if (e0 == e1) continue;
+        mbar_wait(&sm.kv_full, lvl & 1);
+        if (lvl > 0) mbar_wait(&sm.acc_free, (lvl - 1) & 1);  // previous level's dV/dK read out
+        mbar_wait(&sm.q_full[e0 & 1], (e0 >> 1) & 1);
+        tc_fence_after();
+        issue_s(e0, 0);
+        issue_s(e0, 1);
+        for (int e = e0; e < e1; ++e) {
+          const bool more = e + 1 < e1;
+          mbar_wait(&sm.pds_full[0], e & 1);
+          tc_fence_after();
+          issue_acc(e, 0, e == e0);
+          if (more) {
+            mbar_wait(&sm.q_full[(e + 1) & 1], ((e + 1) >> 1) & 1);
+            tc_fence_after();
+            issue_s(e + 1, 0);
+          }
+          mbar_wait(&sm.pds_full[1], e & 1);
+          tc_fence_after();
+          issue_acc(e, 1, false);
+          if (elect_one()) {
+            mma_commit(&sm.q_free[e & 1]);
+            if (!more) mma_commit(&sm.acc_done);
+          }
+          __syncwarp();
+          if (more) issue_s(e + 1, 1);
+        }
+        ++lvl;
+      }
+    }
+  } else {
+    regs_inc<216>();
+    const int g = (warp - 4) >> 2;  // query columns [64 g, 64 g + 64); d columns at level end
+    const int wq = warp & 3;
+    const int row = wq * 32 + lane;  // pooled key row (TMEM lane)
+    const uint32_t t_lane = tmem + (static_cast<uint32_t>(wq * 32) << 16);
+    const float2 scale2 = make_float2(p.scale_log2, p.scale_log2);
+    bool first = true;
+    int lvl = 0;
+    for (int h = 1; h <= p.levels; ++h) {
+      const int e0 = sm.lvl_end[h - 1], e1 = sm.lvl_end[h];
+      if (e0 == e1) continue;
+      const int L = p.b_k >> (h - 1);
+      for (int e = e0; e < e1; ++e) {
+        mbar_wait(&sm.s_full[g], e & 1);
+        tc_fence_after();
+        const int iq = static_cast<int>(ents[e]) % p.n_q;
+        const int qb = e & 1;
+        const bool straddle =
+            p.causal && static_cast<int64_t>(j + 1) * p.b_k - 1 > static_cast<int64_t>(iq) * p.b_q;
+        const int kpos = j * p.b_k + row;  // level 1 only straddles
+        const int qpos0 = iq * p.b_q + 64 * g;
+        uint32_t pp[32], sp[32];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {  // 32 query columns at a time (register pressure)
+          uint32_t sv[32], dv2[32];
+          tmem_ld32(t_lane + kST + 64 * g + c * 32, sv);
+          tmem_ld32(t_lane + kDPT + 64 * g + c * 32, dv2);
+          tmem_ld_wait(sv);
+          tmem_ld_wait(dv2);
+#pragma unroll
+          for (int e2 = 0; e2 < 32; e2 += 2) {
+            const int cl = c * 32 + e2;  // column within this warpgroup's 64
+            const int col = 64 * g + cl;
+            const float2 l2 = *reinterpret_cast<const float2*>(&sm.lse2[qb][col]);
+            const float2 d2 = *reinterpret_cast<const float2*>(&sm.dd[qb][col]);
+            const float2 a = ffma2(make_float2(__uint_as_float(sv[e2]), __uint_as_float(sv[e2 + 1])),
+                                   scale2, make_float2(-l2.x, -l2.y));
+            float p0 = l2.x != -INFINITY ? ex2_approx(a.x) : 0.f;
+            float p1 = l2.y != -INFINITY ? ex2_approx(a.y) : 0.f;
+            if (straddle) {
+              if (kpos > qpos0 + cl) p0 = 0.f;
+              if (kpos > qpos0 + cl + 1) p1 = 0.f;
+            }
+            pp[cl >> 1] = pack_bf16x2(p0, p1);
+            sp[cl >> 1] = pack_bf16x2(p0 * (__uint_as_float(dv2[e2]) - d2.x),
+                                      p1 * (__uint_as_float(dv2[e2 + 1]) - d2.y));
+          }
+        }
+        // P'^T / dS^T as bf16 pairs over the first 32 of this half's (already read) columns
+        tmem_st32(t_lane + kST + 64 * g, pp);
+        tmem_st32(t_lane + kDPT + 64 * g, sp);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.pds_full[g]);
+      }
+      // ---- level end: pooled rows -> their 2^(h-1) raw rows (fp32 scratch of this block)
+      mbar_wait(&sm.acc_done, lvl & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t ok[32], ov[32];
+        tmem_ld32(t_lane + kDK + 64 * g + c * 32, ok);
+        tmem_ld32(t_lane + kDV + 64 * g + c * 32, ov);
+        tmem_ld_wait(ok);
+        tmem_ld_wait(ov);
+        if (row < L) {
+          const int f = 1 << (h - 1);
+          for (int u = 0; u < f; ++u) {
+            const int r = row * f + u;
+            float4* pk4 = reinterpret_cast<float4*>(sk + static_cast<int64_t>(r) * D + 64 * g + c * 32);
+            float4* pv4 = reinterpret_cast<float4*>(sv + static_cast<int64_t>(r) * D + 64 * g + c * 32);
+#pragma unroll
+            for (int q4 = 0; q4 < 8; ++q4) {
+              float4 a = make_float4(__uint_as_float(ok[4 * q4]), __uint_as_float(ok[4 * q4 + 1]),
+                                     __uint_as_float(ok[4 * q4 + 2]), __uint_as_float(ok[4 * q4 + 3]));
+              float4 w = make_float4(__uint_as_float(ov[4 * q4]), __uint_as_float(ov[4 * q4 + 1]),
+                                     __uint_as_float(ov[4 * q4 + 2]), __uint_as_float(ov[4 * q4 + 3]));
+              if (!first) {
+                const float4 a0 = pk4[q4], w0 = pv4[q4];
+                a = make_float4(a0.x + a.x, a0.y + a.y, a0.z + a.z, a0.w + a.w);
+                w = make_float4(w0.x + w.x, w0.y + w.y, w0.z + w.z, w0.w + w.w);
+              }
+              pk4[q4] = a;
+              pv4[q4] = w;
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.acc_free);
+      first = false;
+      ++lvl;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  // ---- bf16 outputs of the raw rows of block j (zeros when no query block selected it)
+  const bool any = sm.lvl_end[p.levels] > 0;
+  for (int x = threadIdx.x; x < p.b_k * D / 2; x += kPPThreads) {
+    const int r = (2 * x) / D, c = (2 * x) % D;
+    uint32_t okv = 0u, ovv = 0u;
+    if (any) {
+      okv = pack_bf16x2(sk[r * D + c] * scale, sk[r * D + c + 1] * scale);
+      ovv = pack_bf16x2(sv[r * D + c], sv[r * D + c + 1]);
+    }
+    *reinterpret_cast<uint32_t*>(dk + (krow0 + r) * D + c) = okv;
+    *reinterpret_cast<uint32_t*>(dv + (krow0 + r) * D + c) = ovv;
+  }
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+int attn_bwd_dkv_tc(const void* q, const void* k, const void* v, const void* k_pyr,
+                    const void* v_pyr, const void* dout, const float* lse, const float* drow,
+                    int64_t batch, int hq, int hkv, int64_t n, int b_q, int b_k, int levels,
+                    const int8_t* level_map, int causal, float* scratch, void* dk, void* dv,
+                    cudaStream_t s) {
+  constexpr int D = 128;
+  BwdQMaps maps;
+  memset(&maps, 0, sizeof(maps));
+  AttnParams p{};
+  p.n = n;
+  p.hq = hq;
+  p.hkv = hkv;
+  p.b_q = b_q;
+  p.b_k = b_k;
+  p.levels = levels;
+  p.n_q = static_cast<int>(n / b_q);
+  p.n_k = static_cast<int>(n / b_k);
+  p.causal = causal;
+  p.scale_log2 = static_cast<float>(1.4426950408889634 / sqrt(static_cast<double>(D)));
+  const int64_t bhkv = batch * hkv;
+  int rc = encode_2d(&maps.a.q, q, static_cast<uint64_t>(batch * hq * n), D, kTileRows);
+  if (rc) return rc;
+  rc = encode_2d(&maps.dout, dout, static_cast<uint64_t>(batch * hq * n), D, kTileRows);
+  if (rc) return rc;
+  int64_t off_elems = 0;
+  for (int h = 1; h <= levels; ++h) {
+    const int L = b_k >> (h - 1);
+    int sz = 8;
+    while (sz < L) sz <<= 1;
+    const uint64_t rows = static_cast<uint64_t>(bhkv * (n >> (h - 1)));
+    const void* kb = h == 1 ? k : static_cast<const void*>(static_cast<const uint16_t*>(k_pyr) + off_elems);
+    const void* vb = h == 1 ? v : static_cast<const void*>(static_cast<const uint16_t*>(v_pyr) + off_elems);
+    if (h > 1) off_elems += static_cast<int64_t>(rows) * D;
+    rc = encode_2d(&maps.a.k[h - 1], kb, rows, D, sz);
+    if (rc) return rc;
+    rc = encode_2d(&maps.a.v[h - 1], vb, rows, D, sz);
+    if (rc) return rc;
+  }
+  const int cap = (hq / hkv) * p.n_q;
+  const size_t smem = sizeof(BwdKVSmem) + static_cast<size_t>(cap) * 4;
+  if (smem > 227 * 1024) return psa_fail(PSA_EINVAL, "too many query blocks per KV head for the backward kernel");
+  cudaFuncSetAttribute(psa_bwd_dkv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(smem));
+  psa_bwd_dkv_tc_kernel<<<dim3(static_cast<unsigned>(p.n_k), static_cast<unsigned>(bhkv)),
+                          kPPThreads, smem, s>>>(
+      maps, p, level_map, lse, drow, static_cast<float>(1.0 / sqrt(static_cast<double>(D))), cap,
+      scratch, bhkv, static_cast<uint16_t*>(dk), static_cast<uint16_t*>(dv));
+  return psa_check_launch("psa_bwd_dkv_tc_kernel");
+}
+
 }  // namespace psa
 
 using namespace psa;

@@ -17,11 +17,14 @@
 // add spreads a pooled row's gradient over its 2^(h-1) raw rows, so the work per selected block
 // scales with its pooled length like the forward's.
 //
-// dQ at D = 128 runs on tcgen05 / TMEM (psa_bwd_dq_tc_kernel in psa_attention.cu: the forward's
-// producers and plan walk, S and dP in TMEM, dS through shared memory; 37 ms at cfg3). The dK/dV
-// pass and D = 64 dQ are warp-level mma.sync (m16n8k16 bf16, fp32 accumulate) with ldmatrix
-// fragments, one CTA per (KV head, KV block) for dK/dV (8 warps, cp.async double-buffered Q/dO
-// tiles): cfg3 backward 537 ms (dK/dV 500 ms) against a 34 ms forward.
+// At D = 128 both passes run on tcgen05 / TMEM (psa_attention.cu):
+//  - psa_bwd_dq_tc_kernel: the forward's producers and plan walk, S and dP in TMEM, dS through
+//    shared memory; 26 ms at cfg3;
+//  - psa_bwd_dkv_tc_kernel: one CTA per (KV head, KV block), level-major entry list, S^T / dP^T
+//    in TMEM, P'^T / dS^T written back over them as the TMEM A operand of dV / dK, double-buffered
+//    Q / dO; 180 ms at cfg3 (one pooled block per 128-row MMA: coarse levels fill few rows).
+// D = 64 uses warp-level mma.sync kernels (m16n8k16 bf16, fp32 accumulate, ldmatrix fragments,
+// cp.async double-buffered tiles). cfg3 backward ~300 ms against a 34 ms forward.
 #include "common.cuh"
 #include "psa_internal.h"
 
@@ -572,7 +575,7 @@ static int launch_bwd(BwdParams p, int64_t batch, const uint16_t* out, void* ws,
   const size_t smem_q = 2 * static_cast<size_t>(BwdTile<D>::kBytes) +
                         4 * static_cast<size_t>(kChunkKeys) * BwdTile<D>::kStride * 2 +
                         static_cast<size_t>(p.n_k + 1) * 4 + 2 * kChunkKeys * 8;
-  if (D == 128) {  // tcgen05 / TMEM dQ pass (psa_attention.cu): 37 ms vs ~300 ms at cfg3
+  if (D == 128) {  // tcgen05 / TMEM dQ pass (psa_attention.cu): 26 ms vs ~300 ms at cfg3
     rc = attn_bwd_dq_tc(p.q, p.k, p.v, p.k_pyr, p.v_pyr, p.dout, p.lse, drow, batch, p.hq, p.hkv,
                         p.n, p.b_q, p.b_k, p.levels, p.csr, p.info, p.causal, p.dq, s);
   } else {
@@ -582,6 +585,10 @@ static int launch_bwd(BwdParams p, int64_t batch, const uint16_t* out, void* ws,
     rc = psa_check_launch("bwd_dq_kernel");
   }
   if (rc) return rc;
+  if (D == 128)  // tcgen05 / TMEM dK/dV pass (psa_attention.cu)
+    return attn_bwd_dkv_tc(p.q, p.k, p.v, p.k_pyr, p.v_pyr, p.dout, p.lse, drow, batch, p.hq,
+                           p.hkv, p.n, p.b_q, p.b_k, p.levels, p.level_map, p.causal, scratch,
+                           p.dk, p.dv, s);
   const int cap = (p.hq / p.hkv) * p.n_q;
   const size_t smem = 6 * static_cast<size_t>(BwdTile<D>::kBytes) + 4 * kBwdRows * sizeof(float) +
                       static_cast<size_t>(cap) * 4;

@@ -22,3 +22,8 @@ for k in psa_attn_pp2 xl_stats assign_levels pyramid_kernel; do
      -o gpurun_out/${k}_full -f python bench.py --config cfg3 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_$k.log 2>&1
   echo "ncu $k rc=$?"
 done
+timeout 300 python scripts/probes/bwd_probe.py > gpurun_out/bwd_probe.log 2>&1
+echo "bwd probe rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:psa_bwd_dkv_tc -s 2 -c 1 \
+   -o gpurun_out/psa_bwd_dkv_tc_full -f python scripts/probes/bwd_probe.py > gpurun_out/ncu_bwd_dkv.log 2>&1
+echo "ncu bwd_dkv rc=$?"
