@@ -1009,43 +1009,59 @@ struct BwdKVSmem {
   uint8_t dout[2][kTileRows * 128 * 2];
   float lse2[2][kTileRows];
   float dd[2][kTileRows];
-  uint64_t kv_full, q_full[2], q_free[2], s_full[2], pds_full[2], acc_done, acc_free;
+  uint64_t kv_full, q_full[2], q_free[2], s_full[2], pds_full[2], acc_done;
   uint32_t tmem_base;
-  int lvl_end[kMaxLevels + 1];
+  int n_ent;
   int warp_cnt[kPPThreads / 32];
 };
 
+// One CTA per (KV head, level h, unit u). A unit is the f = 2^(h-1) neighbouring KV blocks
+// [u f, u f + f) whose level-h pooled rows (L = b_k >> (h-1) each) fill one tile of f L = b_k rows,
+// so every level keeps the M = 128 MMAs full. The entries are the (query head, query block) pairs
+// that selected at least one of the unit's blocks at level h, each with an f-bit row mask; rows of
+// blocks the entry did not select at h get P = dS = 0. The unit writes its pooled dK / dV rows
+// (fp32, unscaled) to the level-h slab of the scratch; bwd_unpool_kernel sums the levels per raw row.
 __global__ void __launch_bounds__(kPPThreads, 1)
     psa_bwd_dkv_tc_kernel(const __grid_constant__ BwdQMaps maps, const AttnParams p,
                           const int8_t* __restrict__ level_map, const float* __restrict__ lse,
-                          const float* __restrict__ drow, float scale, int cap,
-                          float* __restrict__ scratch, int64_t bkv_total,
-                          uint16_t* __restrict__ dk, uint16_t* __restrict__ dv) {
+                          const float* __restrict__ drow, int cap, float* __restrict__ scratch,
+                          int64_t bkv_total) {
   constexpr int D = 128;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   auto& sm = *reinterpret_cast<BwdKVSmem*>(smem_raw);
   uint32_t* ents = reinterpret_cast<uint32_t*>(smem_raw + sizeof(BwdKVSmem));
+  uint16_t* emask = reinterpret_cast<uint16_t*>(ents + cap);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int j = blockIdx.x;
   const int64_t bkv = blockIdx.y;
   const int b = static_cast<int>(bkv / p.hkv), hk = static_cast<int>(bkv % p.hkv);
   const int group = p.hq / p.hkv;
   const int span = group * p.n_q;
+  // blockIdx.x -> (level h, unit u): level h has ceil(n_k / 2^(h-1)) units
+  int h = 1, u = blockIdx.x;
+  int64_t slab = 0;  // pooled rows of the levels before h (scratch slab offset, per KV head)
+  while (u >= (p.n_k + (1 << (h - 1)) - 1) >> (h - 1)) {
+    u -= (p.n_k + (1 << (h - 1)) - 1) >> (h - 1);
+    slab += p.n >> (h - 1);
+    ++h;
+  }
+  const int f = 1 << (h - 1);
+  const int L = p.b_k >> (h - 1);
+  const int j0 = u * f;
+  const int nb = min(f, p.n_k - j0);  // blocks in this unit
+  const int64_t n_h = p.n >> (h - 1);
+  const int rows_u = nb * L;          // pooled rows owned by this unit
   constexpr uint32_t kST = 0, kDPT = 128, kDV = 256, kDK = 384;
 
   if (threadIdx.x == 0) {
     if (smem_u32(smem_raw) & 1023u) __trap();
     mbar_init(&sm.kv_full, 1);
-    for (int u = 0; u < 2; ++u) {
-      mbar_init(&sm.q_full[u], 1);
-      mbar_init(&sm.q_free[u], 1);
-    }
-    for (int u = 0; u < 2; ++u) {  // query halves: one per softmax warpgroup
-      mbar_init(&sm.s_full[u], 1);
-      mbar_init(&sm.pds_full[u], 4);
+    for (int w = 0; w < 2; ++w) {
+      mbar_init(&sm.q_full[w], 1);
+      mbar_init(&sm.q_free[w], 1);
+      mbar_init(&sm.s_full[w], 1);   // query halves: one per softmax warpgroup
+      mbar_init(&sm.pds_full[w], 4);
     }
     mbar_init(&sm.acc_done, 1);
-    mbar_init(&sm.acc_free, 8);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -1058,88 +1074,87 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     for (int t = threadIdx.x; t < nvec; t += kPPThreads) z[t] = make_uint4(0, 0, 0, 0);
     fence_proxy_async_smem();
   }
-  // ---- deterministic level-major list of the entries (query head of the group, query block)
+  // ---- deterministic list of the entries that selected any block of the unit at level h
   int total = 0;
-  for (int h = 1; h <= p.levels; ++h) {
-    for (int base = 0; base < span; base += kPPThreads) {
-      const int x = base + threadIdx.x;
-      bool hit = false;
-      if (x < span) {
-        const int g = x / p.n_q, iq = x % p.n_q;
-        const int64_t bhq = static_cast<int64_t>(b) * p.hq + hk * group + g;
-        hit = level_map[(bhq * p.n_q + iq) * p.n_k + j] == h;
-      }
-      const unsigned m = __ballot_sync(0xffffffffu, hit);
-      if (lane == 0) sm.warp_cnt[warp] = __popc(m);
-      __syncthreads();
-      int before = 0, all = 0;
-      for (int w = 0; w < kPPThreads / 32; ++w) {
-        before += w < warp ? sm.warp_cnt[w] : 0;
-        all += sm.warp_cnt[w];
-      }
-      if (hit) {
-        const int slot = total + before + __popc(m & ((1u << lane) - 1u));
-        if (slot < cap) ents[slot] = static_cast<uint32_t>(x);
-      }
-      total += all;
-      __syncthreads();
+  for (int base = 0; base < span; base += kPPThreads) {
+    const int x = base + threadIdx.x;
+    uint32_t m16 = 0;
+    if (x < span) {
+      const int g = x / p.n_q, iq = x % p.n_q;
+      const int64_t bhq = static_cast<int64_t>(b) * p.hq + hk * group + g;
+      const int8_t* lm = level_map + (bhq * p.n_q + iq) * p.n_k + j0;
+      for (int t = 0; t < nb; ++t) m16 |= (lm[t] == h ? 1u : 0u) << t;
     }
-    if (threadIdx.x == 0) sm.lvl_end[h] = min(total, cap);
+    const bool hit = m16 != 0;
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (lane == 0) sm.warp_cnt[warp] = __popc(m);
+    __syncthreads();
+    int before = 0, all = 0;
+    for (int w = 0; w < kPPThreads / 32; ++w) {
+      before += w < warp ? sm.warp_cnt[w] : 0;
+      all += sm.warp_cnt[w];
+    }
+    if (hit) {
+      const int slot = total + before + __popc(m & ((1u << lane) - 1u));
+      if (slot < cap) {
+        ents[slot] = static_cast<uint32_t>(x);
+        emask[slot] = static_cast<uint16_t>(m16);
+      }
+    }
+    total += all;
+    __syncthreads();
   }
-  if (threadIdx.x == 0) sm.lvl_end[0] = 0;
+  if (threadIdx.x == 0) sm.n_ent = min(total, cap);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
-  const int64_t krow0 = bkv * p.n + static_cast<int64_t>(j) * p.b_k;
-  float* sk = scratch + krow0 * D;
-  float* sv = scratch + (bkv_total * p.n + krow0) * D;
+  const int n_ent = sm.n_ent;
+  // level-h slab of this KV head: pooled rows [j0 L, j0 L + rows_u)
+  const int64_t prow0 = bkv * (2 * p.n) + slab + static_cast<int64_t>(j0) * L;
+  float* sk = scratch + prow0 * D;
+  float* sv = scratch + (bkv_total * 2 * p.n + prow0) * D;
 
   if (warp < 4) {
     regs_dec<72>();  // 128 x 72 + 256 x 216 = 384 x 168
-    if (warp == 0) {  // producer: pooled K/V per level, Q / dO / lse / D per entry
-      int e_prev = -1;
-      for (int h = 1; h <= p.levels; ++h) {
-        const int e0 = sm.lvl_end[h - 1], e1 = sm.lvl_end[h];
-        if (e0 == e1) continue;
-        if (e_prev >= 0) mbar_wait(&sm.q_free[e_prev & 1], (e_prev >> 1) & 1);  // its MMAs done
-        const int L = p.b_k >> (h - 1);
-        int sz = 8;
-        while (sz < L) sz <<= 1;
-        const int row = static_cast<int>(bkv * (p.n >> (h - 1)) + static_cast<int64_t>(j) * L);
-        if (lane == 0) {
-          mbar_arrive_expect_tx(&sm.kv_full, 2u * sz * D * 2);
+    if (warp == 0 && n_ent > 0) {  // producer: the unit's pooled K/V once, Q / dO / lse / D per entry
+      int sz = 8;
+      while (sz < L) sz <<= 1;
+      const int row = static_cast<int>(bkv * n_h + static_cast<int64_t>(j0) * L);
+      if (lane == 0) {
+        const int nbox = (rows_u + sz - 1) / sz;
+        mbar_arrive_expect_tx(&sm.kv_full, 2u * nbox * sz * D * 2);
+        for (int bx = 0; bx < nbox; ++bx)
           for (int c = 0; c < D / 64; ++c) {
-            tma_load_2d(&maps.a.k[h - 1], &sm.kv_full, sm.kt + c * kTileRows * 128, c * 64, row);
-            tma_load_2d(&maps.a.v[h - 1], &sm.kv_full, sm.vt + c * kTileRows * 128, c * 64, row);
+            const int off = c * kTileRows * 128 + bx * sz * 128;
+            tma_load_2d(&maps.a.k[h - 1], &sm.kv_full, sm.kt + off, c * 64, row + bx * sz);
+            tma_load_2d(&maps.a.v[h - 1], &sm.kv_full, sm.vt + off, c * 64, row + bx * sz);
           }
+      }
+      for (int e = 0; e < n_ent; ++e) {
+        const int qb = e & 1;
+        if (e >= 2) mbar_wait(&sm.q_free[qb], ((e >> 1) - 1) & 1);  // entry e-2 done
+        const int x = static_cast<int>(ents[e]);
+        const int g = x / p.n_q, iq = x % p.n_q;
+        const int64_t bhq = static_cast<int64_t>(b) * p.hq + hk * group + g;
+        const int64_t q_row0 = bhq * p.n + static_cast<int64_t>(iq) * p.b_q;
+        for (int r = lane; r < kTileRows; r += 32) {
+          const float l = r < p.b_q ? lse[q_row0 + r] : -INFINITY;
+          sm.lse2[qb][r] = l == -INFINITY ? -INFINITY : l * 1.4426950408889634f;
+          sm.dd[qb][r] = r < p.b_q ? drow[q_row0 + r] : 0.f;
         }
-        for (int e = e0; e < e1; ++e) {
-          const int qb = e & 1;
-          if (e >= 2) mbar_wait(&sm.q_free[qb], ((e >> 1) - 1) & 1);  // entry e-2 done
-          const int x = static_cast<int>(ents[e]);
-          const int g = x / p.n_q, iq = x % p.n_q;
-          const int64_t bhq = static_cast<int64_t>(b) * p.hq + hk * group + g;
-          const int64_t q_row0 = bhq * p.n + static_cast<int64_t>(iq) * p.b_q;
-          for (int r = lane; r < kTileRows; r += 32) {
-            const float l = r < p.b_q ? lse[q_row0 + r] : -INFINITY;
-            sm.lse2[qb][r] = l == -INFINITY ? -INFINITY : l * 1.4426950408889634f;
-            sm.dd[qb][r] = r < p.b_q ? drow[q_row0 + r] : 0.f;
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&sm.q_full[qb], 2u * kTileRows * D * 2);
+          for (int c = 0; c < D / 64; ++c) {
+            tma_load_2d(&maps.a.q, &sm.q_full[qb], sm.q[qb] + c * kTileRows * 128, c * 64,
+                        static_cast<int>(q_row0));
+            tma_load_2d(&maps.dout, &sm.q_full[qb], sm.dout[qb] + c * kTileRows * 128, c * 64,
+                        static_cast<int>(q_row0));
           }
-          __syncwarp();
-          if (lane == 0) {
-            mbar_arrive_expect_tx(&sm.q_full[qb], 2u * kTileRows * D * 2);
-            for (int c = 0; c < D / 64; ++c) {
-              tma_load_2d(&maps.a.q, &sm.q_full[qb], sm.q[qb] + c * kTileRows * 128, c * 64,
-                          static_cast<int>(q_row0));
-              tma_load_2d(&maps.dout, &sm.q_full[qb], sm.dout[qb] + c * kTileRows * 128, c * 64,
-                          static_cast<int>(q_row0));
-            }
-          }
-          e_prev = e;
         }
       }
-    } else if (warp == 1) {  // MMA issuer
+    } else if (warp == 1 && n_ent > 0) {  // MMA issuer
       // Two query halves ping-pong with the softmax warpgroups: while one half's P'^T / dS^T
       // is being formed, the tensor core runs the other half's dV / dK and the next entry's S^T.
       constexpr uint32_t idesc_s = umma_idesc_bf16(128, 64, false, false);
@@ -1183,155 +1198,154 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         }
         __syncwarp();
       };
-
-      int lvl = 0;
-      for (int h = 1; h <= p.levels; ++h) {
-        const int e0 = sm.lvl_end[h - 1], e1 = sm.lvl_end[h];
-        if (e0 == e1) continue;
-        mbar_wait(&sm.kv_full, lvl & 1);
-        if (lvl > 0) mbar_wait(&sm.acc_free, (lvl - 1) & 1);  // previous level's dV/dK read out
-        mbar_wait(&sm.q_full[e0 & 1], (e0 >> 1) & 1);
+      mbar_wait(&sm.kv_full, 0);
+      mbar_wait(&sm.q_full[0], 0);
+      tc_fence_after();
+      issue_s(0, 0);
+      issue_s(0, 1);
+      for (int e = 0; e < n_ent; ++e) {
+        const bool more = e + 1 < n_ent;
+        mbar_wait(&sm.pds_full[0], e & 1);
         tc_fence_after();
-        issue_s(e0, 0);
-        issue_s(e0, 1);
-        for (int e = e0; e < e1; ++e) {
-          const bool more = e + 1 < e1;
-          mbar_wait(&sm.pds_full[0], e & 1);
+        issue_acc(e, 0, e == 0);
+        if (more) {
+          mbar_wait(&sm.q_full[(e + 1) & 1], ((e + 1) >> 1) & 1);
           tc_fence_after();
-          issue_acc(e, 0, e == e0);
-          if (more) {
-            mbar_wait(&sm.q_full[(e + 1) & 1], ((e + 1) >> 1) & 1);
-            tc_fence_after();
-            issue_s(e + 1, 0);
-          }
-          mbar_wait(&sm.pds_full[1], e & 1);
-          tc_fence_after();
-          issue_acc(e, 1, false);
-          if (elect_one()) {
-            mma_commit(&sm.q_free[e & 1]);
-            if (!more) mma_commit(&sm.acc_done);
-          }
-          __syncwarp();
-          if (more) issue_s(e + 1, 1);
+          issue_s(e + 1, 0);
         }
-        ++lvl;
+        mbar_wait(&sm.pds_full[1], e & 1);
+        tc_fence_after();
+        issue_acc(e, 1, false);
+        if (elect_one()) {
+          mma_commit(&sm.q_free[e & 1]);
+          if (!more) mma_commit(&sm.acc_done);
+        }
+        __syncwarp();
+        if (more) issue_s(e + 1, 1);
       }
     }
   } else {
     regs_inc<216>();
-    const int g = (warp - 4) >> 2;  // query columns [64 g, 64 g + 64); d columns at level end
+    const int g = (warp - 4) >> 2;  // query columns [64 g, 64 g + 64); d columns at the end
     const int wq = warp & 3;
-    const int row = wq * 32 + lane;  // pooled key row (TMEM lane)
+    const int row = wq * 32 + lane;  // pooled key row of the unit (TMEM lane)
     const uint32_t t_lane = tmem + (static_cast<uint32_t>(wq * 32) << 16);
     const float2 scale2 = make_float2(p.scale_log2, p.scale_log2);
-    bool first = true;
-    int lvl = 0;
-    for (int h = 1; h <= p.levels; ++h) {
-      const int e0 = sm.lvl_end[h - 1], e1 = sm.lvl_end[h];
-      if (e0 == e1) continue;
-      const int L = p.b_k >> (h - 1);
-      for (int e = e0; e < e1; ++e) {
-        mbar_wait(&sm.s_full[g], e & 1);
-        tc_fence_after();
-        const int iq = static_cast<int>(ents[e]) % p.n_q;
-        const int qb = e & 1;
-        const bool straddle =
-            p.causal && static_cast<int64_t>(j + 1) * p.b_k - 1 > static_cast<int64_t>(iq) * p.b_q;
-        const int kpos = j * p.b_k + row;  // level 1 only straddles
-        const int qpos0 = iq * p.b_q + 64 * g;
-        uint32_t pp[32], sp[32];
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {  // 32 query columns at a time (register pressure)
-          uint32_t sv[32], dv2[32];
-          tmem_ld32(t_lane + kST + 64 * g + c * 32, sv);
-          tmem_ld32(t_lane + kDPT + 64 * g + c * 32, dv2);
-          tmem_ld_wait(sv);
-          tmem_ld_wait(dv2);
-#pragma unroll
-          for (int e2 = 0; e2 < 32; e2 += 2) {
-            const int cl = c * 32 + e2;  // column within this warpgroup's 64
-            const int col = 64 * g + cl;
-            const float2 l2 = *reinterpret_cast<const float2*>(&sm.lse2[qb][col]);
-            const float2 d2 = *reinterpret_cast<const float2*>(&sm.dd[qb][col]);
-            const float2 a = ffma2(make_float2(__uint_as_float(sv[e2]), __uint_as_float(sv[e2 + 1])),
-                                   scale2, make_float2(-l2.x, -l2.y));
-            float p0 = l2.x != -INFINITY ? ex2_approx(a.x) : 0.f;
-            float p1 = l2.y != -INFINITY ? ex2_approx(a.y) : 0.f;
-            if (straddle) {
-              if (kpos > qpos0 + cl) p0 = 0.f;
-              if (kpos > qpos0 + cl + 1) p1 = 0.f;
-            }
-            pp[cl >> 1] = pack_bf16x2(p0, p1);
-            sp[cl >> 1] = pack_bf16x2(p0 * (__uint_as_float(dv2[e2]) - d2.x),
-                                      p1 * (__uint_as_float(dv2[e2 + 1]) - d2.y));
-          }
-        }
-        // P'^T / dS^T as bf16 pairs over the first 32 of this half's (already read) columns
-        tmem_st32(t_lane + kST + 64 * g, pp);
-        tmem_st32(t_lane + kDPT + 64 * g, sp);
-        tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.pds_full[g]);
-      }
-      // ---- level end: pooled rows -> their 2^(h-1) raw rows (fp32 scratch of this block)
-      mbar_wait(&sm.acc_done, lvl & 1);
+    const int blk = row / L;  // block of the unit this row belongs to
+    for (int e = 0; e < n_ent; ++e) {
+      mbar_wait(&sm.s_full[g], e & 1);
       tc_fence_after();
+      const int iq = static_cast<int>(ents[e]) % p.n_q;
+      const bool live = blk < nb && ((emask[e] >> blk) & 1u);
+      const int qb = e & 1;
+      const bool straddle =  // causal diagonal blocks are always level 1 (f = 1)
+          p.causal && h == 1 && static_cast<int64_t>(j0 + 1) * p.b_k - 1 > static_cast<int64_t>(iq) * p.b_q;
+      const int kpos = j0 * p.b_k + row;
+      const int qpos0 = iq * p.b_q + 64 * g;
+      uint32_t pp[32], sp[32];
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint32_t ok[32], ov[32];
+      for (int c = 0; c < 2; ++c) {  // 32 query columns at a time (register pressure)
+        uint32_t sv2[32], dv2[32];
+        tmem_ld32(t_lane + kST + 64 * g + c * 32, sv2);
+        tmem_ld32(t_lane + kDPT + 64 * g + c * 32, dv2);
+        tmem_ld_wait(sv2);
+        tmem_ld_wait(dv2);
+#pragma unroll
+        for (int e2 = 0; e2 < 32; e2 += 2) {
+          const int cl = c * 32 + e2;  // column within this warpgroup's 64
+          const int col = 64 * g + cl;
+          const float2 l2 = *reinterpret_cast<const float2*>(&sm.lse2[qb][col]);
+          const float2 d2 = *reinterpret_cast<const float2*>(&sm.dd[qb][col]);
+          const float2 a = ffma2(make_float2(__uint_as_float(sv2[e2]), __uint_as_float(sv2[e2 + 1])),
+                                 scale2, make_float2(-l2.x, -l2.y));
+          float p0 = l2.x != -INFINITY ? ex2_approx(a.x) : 0.f;
+          float p1 = l2.y != -INFINITY ? ex2_approx(a.y) : 0.f;
+          if (!live) p0 = p1 = 0.f;
+          if (straddle) {
+            if (kpos > qpos0 + cl) p0 = 0.f;
+            if (kpos > qpos0 + cl + 1) p1 = 0.f;
+          }
+          pp[cl >> 1] = pack_bf16x2(p0, p1);
+          sp[cl >> 1] = pack_bf16x2(p0 * (__uint_as_float(dv2[e2]) - d2.x),
+                                    p1 * (__uint_as_float(dv2[e2 + 1]) - d2.y));
+        }
+      }
+      // P'^T / dS^T as bf16 pairs over the first 32 of this half's (already read) columns
+      tmem_st32(t_lane + kST + 64 * g, pp);
+      tmem_st32(t_lane + kDPT + 64 * g, sp);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.pds_full[g]);
+    }
+    // ---- the unit's pooled rows -> the level-h slab (zeros when no entry selected them)
+    if (n_ent > 0) {
+      mbar_wait(&sm.acc_done, 0);
+      tc_fence_after();
+    }
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      uint32_t ok[32], ov[32];
+      if (n_ent > 0) {
         tmem_ld32(t_lane + kDK + 64 * g + c * 32, ok);
         tmem_ld32(t_lane + kDV + 64 * g + c * 32, ov);
         tmem_ld_wait(ok);
         tmem_ld_wait(ov);
-        if (row < L) {
-          const int f = 1 << (h - 1);
-          for (int u = 0; u < f; ++u) {
-            const int r = row * f + u;
-            float4* pk4 = reinterpret_cast<float4*>(sk + static_cast<int64_t>(r) * D + 64 * g + c * 32);
-            float4* pv4 = reinterpret_cast<float4*>(sv + static_cast<int64_t>(r) * D + 64 * g + c * 32);
+      } else {
 #pragma unroll
-            for (int q4 = 0; q4 < 8; ++q4) {
-              float4 a = make_float4(__uint_as_float(ok[4 * q4]), __uint_as_float(ok[4 * q4 + 1]),
-                                     __uint_as_float(ok[4 * q4 + 2]), __uint_as_float(ok[4 * q4 + 3]));
-              float4 w = make_float4(__uint_as_float(ov[4 * q4]), __uint_as_float(ov[4 * q4 + 1]),
-                                     __uint_as_float(ov[4 * q4 + 2]), __uint_as_float(ov[4 * q4 + 3]));
-              if (!first) {
-                const float4 a0 = pk4[q4], w0 = pv4[q4];
-                a = make_float4(a0.x + a.x, a0.y + a.y, a0.z + a.z, a0.w + a.w);
-                w = make_float4(w0.x + w.x, w0.y + w.y, w0.z + w.z, w0.w + w.w);
-              }
-              pk4[q4] = a;
-              pv4[q4] = w;
-            }
-          }
+        for (int t = 0; t < 32; ++t) ok[t] = ov[t] = 0u;
+      }
+      if (row < rows_u) {
+        float4* pk4 = reinterpret_cast<float4*>(sk + static_cast<int64_t>(row) * D + 64 * g + c * 32);
+        float4* pv4 = reinterpret_cast<float4*>(sv + static_cast<int64_t>(row) * D + 64 * g + c * 32);
+#pragma unroll
+        for (int q4 = 0; q4 < 8; ++q4) {
+          pk4[q4] = make_float4(__uint_as_float(ok[4 * q4]), __uint_as_float(ok[4 * q4 + 1]),
+                                __uint_as_float(ok[4 * q4 + 2]), __uint_as_float(ok[4 * q4 + 3]));
+          pv4[q4] = make_float4(__uint_as_float(ov[4 * q4]), __uint_as_float(ov[4 * q4 + 1]),
+                                __uint_as_float(ov[4 * q4 + 2]), __uint_as_float(ov[4 * q4 + 3]));
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.acc_free);
-      first = false;
-      ++lvl;
     }
   }
   tc_fence_before();
   __syncthreads();
-  // ---- bf16 outputs of the raw rows of block j (zeros when no query block selected it)
-  const bool any = sm.lvl_end[p.levels] > 0;
-  for (int x = threadIdx.x; x < p.b_k * D / 2; x += kPPThreads) {
-    const int r = (2 * x) / D, c = (2 * x) % D;
-    uint32_t okv = 0u, ovv = 0u;
-    if (any) {
-      okv = pack_bf16x2(sk[r * D + c] * scale, sk[r * D + c + 1] * scale);
-      ovv = pack_bf16x2(sv[r * D + c], sv[r * D + c + 1]);
-    }
-    *reinterpret_cast<uint32_t*>(dk + (krow0 + r) * D + c) = okv;
-    *reinterpret_cast<uint32_t*>(dv + (krow0 + r) * D + c) = ovv;
-  }
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
+}
+
+// dK / dV of raw row r = sum over levels of the level's pooled gradient row r >> (h-1) (the
+// duplicate identity, psa_backward.cu header); dK takes the softmax scale. One thread per 4 columns.
+__global__ void bwd_unpool_kernel(const float* __restrict__ scratch, int64_t bkv_total, int64_t n,
+                                  int levels, float scale, uint16_t* __restrict__ dk,
+                                  uint16_t* __restrict__ dv) {
+  constexpr int D = 128;
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= bkv_total * n * (D / 4)) return;
+  const int c = static_cast<int>(t % (D / 4)) * 4;
+  const int64_t rr = t / (D / 4);
+  const int64_t bkv = rr / n, r = rr % n;
+  const float* sk = scratch + bkv * (2 * n) * D;
+  const float* sv = scratch + (bkv_total + bkv) * (2 * n) * D;
+  float4 a = make_float4(0.f, 0.f, 0.f, 0.f), w = a;
+  int64_t slab = 0;
+  for (int h = 1; h <= levels; ++h) {
+    const int64_t pr = (slab + (r >> (h - 1))) * D + c;
+    const float4 x = *reinterpret_cast<const float4*>(sk + pr);
+    const float4 y = *reinterpret_cast<const float4*>(sv + pr);
+    a = make_float4(a.x + x.x, a.y + x.y, a.z + x.z, a.w + x.w);
+    w = make_float4(w.x + y.x, w.y + y.y, w.z + y.z, w.w + y.w);
+    slab += n >> (h - 1);
+  }
+  uint2 ok, ov;
+  ok.x = pack_bf16x2(a.x * scale, a.y * scale);
+  ok.y = pack_bf16x2(a.z * scale, a.w * scale);
+  ov.x = pack_bf16x2(w.x, w.y);
+  ov.y = pack_bf16x2(w.z, w.w);
+  *reinterpret_cast<uint2*>(dk + rr * D + c) = ok;
+  *reinterpret_cast<uint2*>(dv + rr * D + c) = ov;
 }
 
 int attn_bwd_dkv_tc(const void* q, const void* k, const void* v, const void* k_pyr,
@@ -1359,6 +1373,7 @@ int attn_bwd_dkv_tc(const void* q, const void* k, const void* v, const void* k_p
   rc = encode_2d(&maps.dout, dout, static_cast<uint64_t>(batch * hq * n), D, kTileRows);
   if (rc) return rc;
   int64_t off_elems = 0;
+  int units = 0;
   for (int h = 1; h <= levels; ++h) {
     const int L = b_k >> (h - 1);
     int sz = 8;
@@ -1371,17 +1386,22 @@ int attn_bwd_dkv_tc(const void* q, const void* k, const void* v, const void* k_p
     if (rc) return rc;
     rc = encode_2d(&maps.a.v[h - 1], vb, rows, D, sz);
     if (rc) return rc;
+    units += (p.n_k + (1 << (h - 1)) - 1) >> (h - 1);
   }
   const int cap = (hq / hkv) * p.n_q;
-  const size_t smem = sizeof(BwdKVSmem) + static_cast<size_t>(cap) * 4;
+  const size_t smem = sizeof(BwdKVSmem) + static_cast<size_t>(cap) * 6;
   if (smem > 227 * 1024) return psa_fail(PSA_EINVAL, "too many query blocks per KV head for the backward kernel");
   cudaFuncSetAttribute(psa_bwd_dkv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(smem));
-  psa_bwd_dkv_tc_kernel<<<dim3(static_cast<unsigned>(p.n_k), static_cast<unsigned>(bhkv)),
-                          kPPThreads, smem, s>>>(
-      maps, p, level_map, lse, drow, static_cast<float>(1.0 / sqrt(static_cast<double>(D))), cap,
-      scratch, bhkv, static_cast<uint16_t*>(dk), static_cast<uint16_t*>(dv));
-  return psa_check_launch("psa_bwd_dkv_tc_kernel");
+  psa_bwd_dkv_tc_kernel<<<dim3(static_cast<unsigned>(units), static_cast<unsigned>(bhkv)),
+                          kPPThreads, smem, s>>>(maps, p, level_map, lse, drow, cap, scratch, bhkv);
+  rc = psa_check_launch("psa_bwd_dkv_tc_kernel");
+  if (rc) return rc;
+  const int64_t threads = bhkv * n * (D / 4);
+  bwd_unpool_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(
+      scratch, bhkv, n, levels, static_cast<float>(1.0 / sqrt(static_cast<double>(D))),
+      static_cast<uint16_t*>(dk), static_cast<uint16_t*>(dv));
+  return psa_check_launch("bwd_unpool_kernel");
 }
 
 }  // namespace psa

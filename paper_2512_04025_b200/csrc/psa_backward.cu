@@ -20,11 +20,12 @@
 // At D = 128 both passes run on tcgen05 / TMEM (psa_attention.cu):
 //  - psa_bwd_dq_tc_kernel: the forward's producers and plan walk, S and dP in TMEM, dS through
 //    shared memory; 26 ms at cfg3;
-//  - psa_bwd_dkv_tc_kernel: one CTA per (KV head, KV block), level-major entry list, S^T / dP^T
-//    in TMEM, P'^T / dS^T written back over them as the TMEM A operand of dV / dK, double-buffered
-//    Q / dO; 180 ms at cfg3 (one pooled block per 128-row MMA: coarse levels fill few rows).
+//  - psa_bwd_dkv_tc_kernel: one CTA per (KV head, level, unit of 2^(h-1) blocks packed into one
+//    tile), S^T / dP^T in TMEM, P'^T / dS^T written back over them as the TMEM A operand of
+//    dV / dK, double-buffered Q / dO, per-level pooled fp32 slabs summed by bwd_unpool_kernel;
+//    74 ms at cfg3.
 // D = 64 uses warp-level mma.sync kernels (m16n8k16 bf16, fp32 accumulate, ldmatrix fragments,
-// cp.async double-buffered tiles). cfg3 backward ~300 ms against a 34 ms forward.
+// cp.async double-buffered tiles). cfg3 backward ~144 ms against a 34 ms forward.
 #include "common.cuh"
 #include "psa_internal.h"
 
@@ -605,9 +606,10 @@ static int launch_bwd(BwdParams p, int64_t batch, const uint16_t* out, void* ws,
 using namespace psa;
 
 extern "C" size_t psa_attn_bwd_workspace_bytes(int64_t batch, int hq, int hkv, int64_t n, int d) {
-  // D = rowsum(dO * O) per query row, then fp32 dK / dV accumulators of the raw rows
+  // D = rowsum(dO * O) per query row, then fp32 dK / dV accumulators: the raw rows (D = 64), or
+  // the pooled rows of every level, < 2 n per KV head (D = 128 tcgen05 pass)
   const int64_t rows = batch * hq * n;
-  return static_cast<size_t>((rows + 63) / 64 * 64 + 2 * batch * hkv * n * d) * sizeof(float);
+  return static_cast<size_t>((rows + 63) / 64 * 64 + 4 * batch * hkv * n * d) * sizeof(float);
 }
 
 extern "C" int psa_attn_bwd(const void* q, const void* k, const void* v, const void* k_pyr,

@@ -1,7 +1,7 @@
 set -x
 timeout 600 python -m pytest tests/test_gpu_backward.py -x -q 2>&1 | tail -5
 timeout 300 python scripts/probes/bwd_probe.py 2>&1 | tail -4
-timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:bwd --csv --log-file gpurun_out/bwd_launch.csv python scripts/probes/bwd_probe.py > /dev/null 2>&1
+timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"bwd|unpool" --csv --log-file gpurun_out/bwd_launch.csv python scripts/probes/bwd_probe.py > /dev/null 2>&1
 python - <<'P'
 import csv,collections
 d=collections.defaultdict(list)
