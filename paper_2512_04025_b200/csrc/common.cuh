@@ -89,6 +89,13 @@ PSA_DEV void tma_load_2d(const void* map, uint64_t* bar, void* smem_dst, int c0,
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+// 1D bulk copy global -> shared (bytes % 16 == 0, both addresses 16-byte aligned)
+PSA_DEV void bulk_load_1d(void* smem_dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(smem_dst)), "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
 // make generic-proxy shared-memory writes visible to the async proxy (tcgen05.mma / TMA)
 PSA_DEV void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

@@ -1007,7 +1007,7 @@ struct BwdKVSmem {
   uint8_t vt[kTileRows * 128 * 2];
   uint8_t q[2][kTileRows * 128 * 2];     // double-buffered per entry
   uint8_t dout[2][kTileRows * 128 * 2];
-  float lse2[2][kTileRows];
+  float lse_q[2][kTileRows];  // raw lse / D of the entry's query rows (double-buffered)
   float dd[2][kTileRows];
   uint64_t kv_full, q_full[2], q_free[2], s_full[2], pds_full[2], acc_done;
   uint32_t tmem_base;
@@ -1072,6 +1072,10 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     uint4* z = reinterpret_cast<uint4*>(sm.kt);
     const int nvec = 2 * kTileRows * 128 * 2 / 16;  // pooled K / V tiles
     for (int t = threadIdx.x; t < nvec; t += kPPThreads) z[t] = make_uint4(0, 0, 0, 0);
+    for (int t = threadIdx.x; t < 2 * kTileRows; t += kPPThreads) {  // rows >= b_q stay finite
+      (&sm.lse_q[0][0])[t] = 0.f;
+      (&sm.dd[0][0])[t] = 0.f;
+    }
     fence_proxy_async_smem();
   }
   // ---- deterministic list of the entries that selected any block of the unit at level h
@@ -1118,6 +1122,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
   if (warp < 4) {
     regs_dec<72>();  // 128 x 72 + 256 x 216 = 384 x 168
     if (warp == 0 && n_ent > 0) {  // producer: the unit's pooled K/V once, Q / dO / lse / D per entry
+      const bool bulk_rows = p.b_q % 4 == 0 && p.n % 4 == 0;
       int sz = 8;
       while (sz < L) sz <<= 1;
       const int row = static_cast<int>(bkv * n_h + static_cast<int64_t>(j0) * L);
@@ -1138,14 +1143,18 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         const int g = x / p.n_q, iq = x % p.n_q;
         const int64_t bhq = static_cast<int64_t>(b) * p.hq + hk * group + g;
         const int64_t q_row0 = bhq * p.n + static_cast<int64_t>(iq) * p.b_q;
-        for (int r = lane; r < kTileRows; r += 32) {
-          const float l = r < p.b_q ? lse[q_row0 + r] : -INFINITY;
-          sm.lse2[qb][r] = l == -INFINITY ? -INFINITY : l * 1.4426950408889634f;
-          sm.dd[qb][r] = r < p.b_q ? drow[q_row0 + r] : 0.f;
-        }
+        if (!bulk_rows)
+          for (int r = lane; r < p.b_q; r += 32) {
+            sm.lse_q[qb][r] = lse[q_row0 + r];
+            sm.dd[qb][r] = drow[q_row0 + r];
+          }
         __syncwarp();
         if (lane == 0) {
-          mbar_arrive_expect_tx(&sm.q_full[qb], 2u * kTileRows * D * 2);
+          mbar_arrive_expect_tx(&sm.q_full[qb], 2u * kTileRows * D * 2 + (bulk_rows ? 8u * p.b_q : 0u));
+          if (bulk_rows) {  // lse / D rows ride the same transaction (no serial global loads)
+            bulk_load_1d(sm.lse_q[qb], lse + q_row0, 4u * p.b_q, &sm.q_full[qb]);
+            bulk_load_1d(sm.dd[qb], drow + q_row0, 4u * p.b_q, &sm.q_full[qb]);
+          }
           for (int c = 0; c < D / 64; ++c) {
             tma_load_2d(&maps.a.q, &sm.q_full[qb], sm.q[qb] + c * kTileRows * 128, c * 64,
                         static_cast<int>(q_row0));
@@ -1231,6 +1240,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     const int row = wq * 32 + lane;  // pooled key row of the unit (TMEM lane)
     const uint32_t t_lane = tmem + (static_cast<uint32_t>(wq * 32) << 16);
     const float2 scale2 = make_float2(p.scale_log2, p.scale_log2);
+    const float2 nlog2e2 = make_float2(-1.4426950408889634f, -1.4426950408889634f);
     const int blk = row / L;  // block of the unit this row belongs to
     for (int e = 0; e < n_ent; ++e) {
       mbar_wait(&sm.s_full[g], e & 1);
@@ -1254,13 +1264,15 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         for (int e2 = 0; e2 < 32; e2 += 2) {
           const int cl = c * 32 + e2;  // column within this warpgroup's 64
           const int col = 64 * g + cl;
-          const float2 l2 = *reinterpret_cast<const float2*>(&sm.lse2[qb][col]);
+          const float2 lr = *reinterpret_cast<const float2*>(&sm.lse_q[qb][col]);
           const float2 d2 = *reinterpret_cast<const float2*>(&sm.dd[qb][col]);
+          const float2 l2 = fmul2(lr, nlog2e2);
           const float2 a = ffma2(make_float2(__uint_as_float(sv2[e2]), __uint_as_float(sv2[e2 + 1])),
-                                 scale2, make_float2(-l2.x, -l2.y));
-          float p0 = l2.x != -INFINITY ? ex2_approx(a.x) : 0.f;
-          float p1 = l2.y != -INFINITY ? ex2_approx(a.y) : 0.f;
-          if (!live) p0 = p1 = 0.f;
+                                 scale2, l2);
+          float p0 = lr.x != -INFINITY ? ex2_approx(a.x) : 0.f;
+          float p1 = lr.y != -INFINITY ? ex2_approx(a.y) : 0.f;
+          if (!live || col >= p.b_q) p0 = 0.f;
+          if (!live || col + 1 >= p.b_q) p1 = 0.f;
           if (straddle) {
             if (kpos > qpos0 + cl) p0 = 0.f;
             if (kpos > qpos0 + cl + 1) p1 = 0.f;

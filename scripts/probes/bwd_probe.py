@@ -51,3 +51,14 @@ counts = res.plan.level_counts.cpu().tolist()
 sel_blocks = sum(counts[1:])
 flops = 2.5 * 4 * cfg["d"] * sel_blocks * cfg["b_q"] * cfg["b_k"]  # expanded blocks: S, dP, dV, dK, dQ
 print(f"cfg3 backward {ms:.2f} ms; selected blocks {sel_blocks}; {flops / ms / 1e9:.0f} TFLOP/s on expanded-block work")
+
+# per-kernel device times (CUPTI) of the same calls
+from torch.profiler import ProfilerActivity, profile  # noqa: E402
+
+with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    for _ in range(3):
+        attention_backward(q, res.pyramid, res.plan, False, res.out, res.lse, g)
+    torch.cuda.synchronize()
+for ev in prof.key_averages():
+    if ev.device_type.name == "CUDA" and ev.count:
+        print(f"  {ev.key[:60]:60s} x{ev.count:3d} {ev.device_time_total / ev.count / 1e3:9.3f} ms")
