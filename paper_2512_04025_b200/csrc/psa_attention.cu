@@ -1007,7 +1007,7 @@ struct BwdKVSmem {
   uint8_t vt[kTileRows * 128 * 2];
   uint8_t q[2][kTileRows * 128 * 2];     // double-buffered per entry
   uint8_t dout[2][kTileRows * 128 * 2];
-  float lse_q[2][kTileRows];  // raw lse / D of the entry's query rows (double-buffered)
+  float nl2[2][kTileRows];  // -lse log2(e) / D of the entry's query rows (double-buffered)
   float dd[2][kTileRows];
   uint64_t kv_full, q_full[2], q_free[2], s_full[2], pds_full[2], acc_done;
   uint32_t tmem_base;
@@ -1023,7 +1023,7 @@ struct BwdKVSmem {
 // (fp32, unscaled) to the level-h slab of the scratch; bwd_unpool_kernel sums the levels per raw row.
 __global__ void __launch_bounds__(kPPThreads, 1)
     psa_bwd_dkv_tc_kernel(const __grid_constant__ BwdQMaps maps, const AttnParams p,
-                          const int8_t* __restrict__ level_map, const float* __restrict__ lse,
+                          const int8_t* __restrict__ level_map, const float* __restrict__ nl2,
                           const float* __restrict__ drow, int cap, float* __restrict__ scratch,
                           int64_t bkv_total) {
   constexpr int D = 128;
@@ -1072,8 +1072,8 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     uint4* z = reinterpret_cast<uint4*>(sm.kt);
     const int nvec = 2 * kTileRows * 128 * 2 / 16;  // pooled K / V tiles
     for (int t = threadIdx.x; t < nvec; t += kPPThreads) z[t] = make_uint4(0, 0, 0, 0);
-    for (int t = threadIdx.x; t < 2 * kTileRows; t += kPPThreads) {  // rows >= b_q stay finite
-      (&sm.lse_q[0][0])[t] = 0.f;
+    for (int t = threadIdx.x; t < 2 * kTileRows; t += kPPThreads) {  // rows >= b_q: P = dS = 0
+      (&sm.nl2[0][0])[t] = -INFINITY;
       (&sm.dd[0][0])[t] = 0.f;
     }
     fence_proxy_async_smem();
@@ -1145,14 +1145,14 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         const int64_t q_row0 = bhq * p.n + static_cast<int64_t>(iq) * p.b_q;
         if (!bulk_rows)
           for (int r = lane; r < p.b_q; r += 32) {
-            sm.lse_q[qb][r] = lse[q_row0 + r];
+            sm.nl2[qb][r] = nl2[q_row0 + r];
             sm.dd[qb][r] = drow[q_row0 + r];
           }
         __syncwarp();
         if (lane == 0) {
           mbar_arrive_expect_tx(&sm.q_full[qb], 2u * kTileRows * D * 2 + (bulk_rows ? 8u * p.b_q : 0u));
           if (bulk_rows) {  // lse / D rows ride the same transaction (no serial global loads)
-            bulk_load_1d(sm.lse_q[qb], lse + q_row0, 4u * p.b_q, &sm.q_full[qb]);
+            bulk_load_1d(sm.nl2[qb], nl2 + q_row0, 4u * p.b_q, &sm.q_full[qb]);
             bulk_load_1d(sm.dd[qb], drow + q_row0, 4u * p.b_q, &sm.q_full[qb]);
           }
           for (int c = 0; c < D / 64; ++c) {
@@ -1240,7 +1240,6 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     const int row = wq * 32 + lane;  // pooled key row of the unit (TMEM lane)
     const uint32_t t_lane = tmem + (static_cast<uint32_t>(wq * 32) << 16);
     const float2 scale2 = make_float2(p.scale_log2, p.scale_log2);
-    const float2 nlog2e2 = make_float2(-1.4426950408889634f, -1.4426950408889634f);
     const int blk = row / L;  // block of the unit this row belongs to
     for (int e = 0; e < n_ent; ++e) {
       mbar_wait(&sm.s_full[g], e & 1);
@@ -1253,6 +1252,9 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       const int kpos = j0 * p.b_k + row;
       const int qpos0 = iq * p.b_q + 64 * g;
       uint32_t pp[32], sp[32];
+      // rows of blocks this entry did not select at h: exp2(-inf) = 0 through the additive term
+      const float kill = live ? 0.f : -INFINITY;
+      const float2 kill2 = make_float2(kill, kill);
 #pragma unroll
       for (int c = 0; c < 2; ++c) {  // 32 query columns at a time (register pressure)
         uint32_t sv2[32], dv2[32];
@@ -1264,16 +1266,12 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         for (int e2 = 0; e2 < 32; e2 += 2) {
           const int cl = c * 32 + e2;  // column within this warpgroup's 64
           const int col = 64 * g + cl;
-          const float2 lr = *reinterpret_cast<const float2*>(&sm.lse_q[qb][col]);
+          const float2 nl = *reinterpret_cast<const float2*>(&sm.nl2[qb][col]);
           const float2 d2 = *reinterpret_cast<const float2*>(&sm.dd[qb][col]);
-          const float2 l2 = fmul2(lr, nlog2e2);
           const float2 a = ffma2(make_float2(__uint_as_float(sv2[e2]), __uint_as_float(sv2[e2 + 1])),
-                                 scale2, l2);
-          float p0 = lr.x != -INFINITY ? ex2_approx(a.x) : 0.f;
-          float p1 = lr.y != -INFINITY ? ex2_approx(a.y) : 0.f;
-          if (!live || col >= p.b_q) p0 = 0.f;
-          if (!live || col + 1 >= p.b_q) p1 = 0.f;
-          if (straddle) {
+                                 scale2, fadd2(nl, kill2));
+          float p0 = ex2_approx(a.x), p1 = ex2_approx(a.y);
+          if (straddle) {  // causal diagonal block (warp-uniform, rare)
             if (kpos > qpos0 + cl) p0 = 0.f;
             if (kpos > qpos0 + cl + 1) p1 = 0.f;
           }
@@ -1363,8 +1361,8 @@ __global__ void bwd_unpool_kernel(const float* __restrict__ scratch, int64_t bkv
 int attn_bwd_dkv_tc(const void* q, const void* k, const void* v, const void* k_pyr,
                     const void* v_pyr, const void* dout, const float* lse, const float* drow,
                     int64_t batch, int hq, int hkv, int64_t n, int b_q, int b_k, int levels,
-                    const int8_t* level_map, int causal, float* scratch, void* dk, void* dv,
-                    cudaStream_t s) {
+                    const int8_t* level_map, int causal, const float* nl2, float* scratch,
+                    void* dk, void* dv, cudaStream_t s) {
   constexpr int D = 128;
   BwdQMaps maps;
   memset(&maps, 0, sizeof(maps));
@@ -1406,7 +1404,7 @@ int attn_bwd_dkv_tc(const void* q, const void* k, const void* v, const void* k_p
   cudaFuncSetAttribute(psa_bwd_dkv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(smem));
   psa_bwd_dkv_tc_kernel<<<dim3(static_cast<unsigned>(units), static_cast<unsigned>(bhkv)),
-                          kPPThreads, smem, s>>>(maps, p, level_map, lse, drow, cap, scratch, bhkv);
+                          kPPThreads, smem, s>>>(maps, p, level_map, nl2, drow, cap, scratch, bhkv);
   rc = psa_check_launch("psa_bwd_dkv_tc_kernel");
   if (rc) return rc;
   const int64_t threads = bhkv * n * (D / 4);

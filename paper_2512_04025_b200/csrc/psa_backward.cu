@@ -125,9 +125,13 @@ PSA_DEV const uint16_t* level_block(const uint16_t* raw, const uint16_t* pyr, in
 
 // D_r = rowsum(dO_r * O_r) (fp32), one warp per row
 template <int D>
+// Also nl2[r] = -lse[r] log2(e) (-inf for a fully masked row), the additive term of the dK/dV
+// pass's exp2 so that its softmax needs no per-column checks.
 __global__ void __launch_bounds__(256) bwd_drow_kernel(const uint16_t* __restrict__ out,
                                                        const uint16_t* __restrict__ dout,
-                                                       int64_t rows, float* __restrict__ drow) {
+                                                       const float* __restrict__ lse,
+                                                       int64_t rows, float* __restrict__ drow,
+                                                       float* __restrict__ nl2) {
   const int64_t r = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (r >= rows) return;
@@ -139,7 +143,11 @@ __global__ void __launch_bounds__(256) bwd_drow_kernel(const uint16_t* __restric
     acc = fmaf(bf2f(o >> 16), bf2f(g >> 16), acc);
   }
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) drow[r] = acc;
+  if (lane == 0) {
+    drow[r] = acc;
+    const float l = lse[r];
+    nl2[r] = l == -INFINITY ? -INFINITY : -l * 1.4426950408889634f;
+  }
 }
 
 // ---------------------------------------------------------------------------------------- dQ
@@ -568,9 +576,10 @@ template <int D>
 static int launch_bwd(BwdParams p, int64_t batch, const uint16_t* out, void* ws, cudaStream_t s) {
   const int64_t rows = batch * p.hq * p.n;
   float* drow = static_cast<float*>(ws);
-  float* scratch = drow + ((rows + 63) / 64) * 64;
+  float* nl2 = drow + ((rows + 63) / 64) * 64;
+  float* scratch = nl2 + ((rows + 63) / 64) * 64;
   p.drow = drow;
-  bwd_drow_kernel<D><<<static_cast<unsigned>((rows + 7) / 8), 256, 0, s>>>(out, p.dout, rows, drow);
+  bwd_drow_kernel<D><<<static_cast<unsigned>((rows + 7) / 8), 256, 0, s>>>(out, p.dout, p.lse, rows, drow, nl2);
   int rc = psa_check_launch("bwd_drow_kernel");
   if (rc) return rc;
   const size_t smem_q = 2 * static_cast<size_t>(BwdTile<D>::kBytes) +
@@ -588,7 +597,7 @@ static int launch_bwd(BwdParams p, int64_t batch, const uint16_t* out, void* ws,
   if (rc) return rc;
   if (D == 128)  // tcgen05 / TMEM dK/dV pass (psa_attention.cu)
     return attn_bwd_dkv_tc(p.q, p.k, p.v, p.k_pyr, p.v_pyr, p.dout, p.lse, drow, batch, p.hq,
-                           p.hkv, p.n, p.b_q, p.b_k, p.levels, p.level_map, p.causal, scratch,
+                           p.hkv, p.n, p.b_q, p.b_k, p.levels, p.level_map, p.causal, nl2, scratch,
                            p.dk, p.dv, s);
   const int cap = (p.hq / p.hkv) * p.n_q;
   const size_t smem = 6 * static_cast<size_t>(BwdTile<D>::kBytes) + 4 * kBwdRows * sizeof(float) +
@@ -609,7 +618,7 @@ extern "C" size_t psa_attn_bwd_workspace_bytes(int64_t batch, int hq, int hkv, i
   // D = rowsum(dO * O) per query row, then fp32 dK / dV accumulators: the raw rows (D = 64), or
   // the pooled rows of every level, < 2 n per KV head (D = 128 tcgen05 pass)
   const int64_t rows = batch * hq * n;
-  return static_cast<size_t>((rows + 63) / 64 * 64 + 4 * batch * hkv * n * d) * sizeof(float);
+  return static_cast<size_t>(2 * ((rows + 63) / 64 * 64) + 4 * batch * hkv * n * d) * sizeof(float);
 }
 
 extern "C" int psa_attn_bwd(const void* q, const void* k, const void* v, const void* k_pyr,

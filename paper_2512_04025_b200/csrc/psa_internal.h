@@ -57,8 +57,8 @@ int attn_bwd_dq_tc(const void* q, const void* k, const void* v, const void* k_py
 int attn_bwd_dkv_tc(const void* q, const void* k, const void* v, const void* k_pyr,
                     const void* v_pyr, const void* dout, const float* lse, const float* drow,
                     int64_t batch, int hq, int hkv, int64_t n, int b_q, int b_k, int levels,
-                    const int8_t* level_map, int causal, float* scratch, void* dk, void* dv,
-                    cudaStream_t s);
+                    const int8_t* level_map, int causal, const float* nl2, float* scratch,
+                    void* dk, void* dv, cudaStream_t s);
 
 // cuTensorMapEncodeTiled from the driver (psa_attention.cu)
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
