@@ -852,8 +852,11 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     const bool valid = row < p.b_q;
     const float l = valid ? lse[q_row0 + row] : -INFINITY;
     const bool live = l != -INFINITY;
-    const float lse2 = live ? l * 1.4426950408889634f : 0.f;
+    // -lse log2(e), -inf for a masked row: exp2 gives P = 0 without a per-column select
+    const float nl2 = live ? -l * 1.4426950408889634f : -INFINITY;
+    const float2 nl22 = make_float2(nl2, nl2);
     const float dd = valid ? drow[q_row0 + row] : 0.f;
+    const float2 ndd2 = make_float2(-dd, -dd);
     const float2 scale2 = make_float2(p.scale_log2, p.scale_log2);
     for (int t = 0; t < T; ++t) {
       const int st = t & 1, ms = t % kMetaRing;
@@ -881,8 +884,8 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         const float* y = reinterpret_cast<const float*>(&pv[e >> 5][e & 31]);
         const float2 bv = *reinterpret_cast<const float2*>(&sm.bias[ms][col]);
         float2 a = ffma2(make_float2(x[0], x[1]), scale2, bv);
-        a = fadd2(a, make_float2(-lse2, -lse2));
-        float p0 = live ? ex2_approx(a.x) : 0.f, p1 = live ? ex2_approx(a.y) : 0.f;
+        a = fadd2(a, nl22);
+        float p0 = ex2_approx(a.x), p1 = ex2_approx(a.y);
         if (p.causal) {
           const uint32_t w = sm.meta[ms][col >> 3];
           if (w & 1u) {
@@ -891,7 +894,8 @@ __global__ void __launch_bounds__(kPPThreads, 1)
             if (kp + 1 > qpos) p1 = 0.f;
           }
         }
-        pk[e >> 1] = pack_bf16x2(p0 * (y[0] - dd), p1 * (y[1] - dd));
+        const float2 ds = fmul2(make_float2(p0, p1), fadd2(make_float2(y[0], y[1]), ndd2));
+        pk[e >> 1] = pack_bf16x2(ds.x, ds.y);
       }
       if (lane == 0) mbar_arrive(&sm.meta_empty[ms]);
       if (t >= 1) mbar_wait(&sm.ds_free, (t - 1) & 1);  // dQ(t-1) has read the previous dS
