@@ -56,7 +56,11 @@ def _oracle(q, k, v, lm, b_q, b_k, causal):
 
 @pytest.mark.parametrize("n,d,b_q,b_k,hq,hkv,causal", [
     (1024, 64, 64, 64, 2, 2, False), (960, 128, 120, 120, 2, 1, False),
-    (1024, 128, 128, 64, 4, 2, True), (512, 64, 64, 64, 3, 3, True)])
+    (1024, 128, 128, 64, 4, 2, True), (512, 64, 64, 64, 3, 3, True),
+    # b_q % 4 != 0: lse / D rows staged by the producer warp instead of a bulk copy
+    (720, 128, 90, 120, 2, 2, False),
+    # n_k = 9: the last packed dK/dV unit of levels 2-4 holds fewer than 2^(h-1) blocks
+    (1152, 128, 128, 128, 2, 1, False)])
 def test_backward_matches_fp64_autograd(n, d, b_q, b_k, hq, hkv, causal):
     import paper_2512_04025_b200 as psa
     from paper_2512_04025_b200.attention import attention_backward
