@@ -624,8 +624,9 @@ static int launch_attn(const void* q, const void* k, const void* v, const void* 
 // dQ of the multi-level attention for a fixed mask (psa_backward.cu has the derivation): the
 // same work unit, plan walk and K/V producers as the forward, with
 //   S = Q K^T and dP = dO V^T (SS MMAs into TMEM), P = exp2(S c + (h-1) - lse2) (lse known: no
-//   running max), dS = P (dP - D) -> shared memory (128B-swizzled like P), dQ += dS K (K read
-//   MN-major like V in the forward's PV).
+//   running max), dS = P (dP - D) written back as bf16 pairs over the S columns it came from,
+//   dQ += dS K with dS as the TMEM A operand (tcgen05.mma TS form; K read MN-major like V in the
+//   forward's PV).
 // Two softmax warpgroups split the 128 key columns of a tile (no cross-warp exchange is needed
 // since the row statistics are final). TMEM: S0 | S1 | dP | dQ (512 columns at D = 128).
 struct BwdQSmem {
@@ -633,13 +634,12 @@ struct BwdQSmem {
   uint8_t dout[kTileRows * 128 * 2];
   uint8_t k[2][kTileRows * 128 * 2];
   uint8_t v[2][kTileRows * 128 * 2];
-  uint8_t ds[kTileRows * kTileRows * 2];
   float bias[kMetaRing][kTileRows];
   uint32_t meta[kMetaRing][kChunks];
   uint64_t q_full;
   uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
   uint64_t meta_full[kMetaRing], meta_empty[kMetaRing];
-  uint64_t s_full[2], sp_read, ds_full, ds_free, dq_done;
+  uint64_t s_full[2], sp_read, ds_full, dq_done;
   uint32_t tmem_base;
 };
 
@@ -683,7 +683,6 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     }
     mbar_init(&sm.sp_read, 8);
     mbar_init(&sm.ds_full, 8);
-    mbar_init(&sm.ds_free, 1);
     mbar_init(&sm.dq_done, 1);
     fence_barrier_init();
   }
@@ -789,7 +788,6 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         constexpr uint32_t idesc_q = umma_idesc_bf16(128, D, false, true);
         const uint64_t q_desc0 = umma_desc_sw128(smem_u32(sm.q), 16, 1024);
         const uint64_t do_desc0 = umma_desc_sw128(smem_u32(sm.dout), 16, 1024);
-        const uint64_t ds_desc0 = umma_desc_sw128(smem_u32(sm.ds), 16, 1024);
         auto issue_sd = [&](int t) {  // S(t) = Q K^T into S[t & 1], dP(t) = dO V^T
           const int st = t & 1;
           mbar_wait(&sm.k_full[st], (t >> 1) & 1);
@@ -828,14 +826,15 @@ __global__ void __launch_bounds__(kPPThreads, 1)
           tc_fence_after();
           const uint64_t kmn_desc0 = umma_desc_sw128(smem_u32(sm.k[st]), kTileRows * 128, 1024);
           if (elect_one()) {
+            // dS(t) (bf16 pairs) sits in S[t & 1]: key columns [64 g, 64 g + 64) packed into
+            // [64 g, 64 g + 32); the A operand comes from tensor memory
 #pragma unroll
             for (int kk = 0; kk < kTileRows / 16; ++kk) {
-              const uint32_t poff = ((kk >> 2) * kTileRows * 128 + (kk & 3) * 32) >> 4;
-              mma_bf16_ss(tmem + kDQ, ds_desc0 + poff, kmn_desc0 + ((kk * 16 * 128) >> 4),
-                          idesc_q, (t > 0 || kk > 0) ? 1u : 0u);
+              const uint32_t acol = st * 128 + 64 * (kk >> 2) + (kk & 3) * 8;
+              mma_bf16_ts(tmem + kDQ, tmem + acol, kmn_desc0 + ((kk * 16 * 128) >> 4), idesc_q,
+                          (t > 0 || kk > 0) ? 1u : 0u);
             }
             mma_commit(&sm.k_empty[st]);
-            mma_commit(&sm.ds_free);
             if (t + 1 == T) mma_commit(&sm.dq_done);
           }
           __syncwarp();
@@ -898,16 +897,10 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         pk[e >> 1] = pack_bf16x2(ds.x, ds.y);
       }
       if (lane == 0) mbar_arrive(&sm.meta_empty[ms]);
-      if (t >= 1) mbar_wait(&sm.ds_free, (t - 1) & 1);  // dQ(t-1) has read the previous dS
-      {  // dS (bf16) -> shared memory, K-major 128B-swizzled: [key half][row][128 B]
-        uint8_t* prow = sm.ds + g * kTileRows * 128 + row * 128;
-        const int sw = row & 7;
-#pragma unroll
-        for (int ch = 0; ch < 8; ++ch)
-          *reinterpret_cast<uint4*>(prow + ((ch ^ sw) << 4)) =
-              make_uint4(pk[ch * 4], pk[ch * 4 + 1], pk[ch * 4 + 2], pk[ch * 4 + 3]);
-      }
-      fence_proxy_async_smem();
+      // dS (bf16 pairs) over this warpgroup's (already read) S columns: the dQ MMA's A operand.
+      // S[t & 1] is next written by S(t + 2), which the MMA warp issues after dQ(t).
+      tmem_st32(t_lane + st * 128 + 64 * g, pk);
+      tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.ds_full);

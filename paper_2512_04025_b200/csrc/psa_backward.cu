@@ -18,8 +18,8 @@
 // scales with its pooled length like the forward's.
 //
 // At D = 128 both passes run on tcgen05 / TMEM (psa_attention.cu):
-//  - psa_bwd_dq_tc_kernel: the forward's producers and plan walk, S and dP in TMEM, dS through
-//    shared memory; 26 ms at cfg3;
+//  - psa_bwd_dq_tc_kernel: the forward's producers and plan walk, S and dP in TMEM, dS written
+//    back over S as the TMEM A operand of dQ += dS K; 26 ms at cfg3;
 //  - psa_bwd_dkv_tc_kernel: one CTA per (KV head, level, unit of 2^(h-1) blocks packed into one
 //    tile), S^T / dP^T in TMEM, P'^T / dS^T written back over them as the TMEM A operand of
 //    dV / dK, double-buffered Q / dO, per-level pooled fp32 slabs summed by bwd_unpool_kernel;
