@@ -1006,7 +1006,7 @@ struct BwdKVSmem {
   uint8_t dout[2][kTileRows * 128 * 2];
   float nl2[2][kTileRows];  // -lse log2(e) / D of the entry's query rows (double-buffered)
   float dd[2][kTileRows];
-  uint64_t kv_full, q_full[2], q_free[2], s_full[2], pds_full[2], acc_done;
+  uint64_t kv_full, q_full[2], q_free[2], s_full[2], pds_full[4], acc_done;
   uint32_t tmem_base;
   int n_ent;
   int warp_cnt[kPPThreads / 32];
@@ -1056,7 +1056,8 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       mbar_init(&sm.q_full[w], 1);
       mbar_init(&sm.q_free[w], 1);
       mbar_init(&sm.s_full[w], 1);   // query halves: one per softmax warpgroup
-      mbar_init(&sm.pds_full[w], 4);
+      mbar_init(&sm.pds_full[2 * w], 4);  // (half, 32-query chunk)
+      mbar_init(&sm.pds_full[2 * w + 1], 4);
     }
     mbar_init(&sm.acc_done, 1);
     fence_barrier_init();
@@ -1188,16 +1189,18 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         }
         __syncwarp();
       };
-      auto issue_acc = [&](int e, int half, bool zero) {  // dV += P'^T dO, dK += dS^T Q (half)
+      // dV += P'^T dO, dK += dS^T Q over the 32 queries of (half, chunk)
+      auto issue_acc = [&](int e, int half, int chunk, bool zero) {
         const int qb = e & 1;
         const uint64_t q_mn = umma_desc_sw128(smem_u32(sm.q[qb]), kTileRows * 128, 1024);
         const uint64_t do_mn = umma_desc_sw128(smem_u32(sm.dout[qb]), kTileRows * 128, 1024);
         if (elect_one()) {
           // P'^T / dS^T (bf16 pairs) sit in the first 32 S^T / dP^T columns of the half
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
+          for (int k2 = 0; k2 < 2; ++k2) {
+            const int kk = 2 * chunk + k2;
             const uint32_t boff = ((half * 64 + kk * 16) * 128) >> 4;
-            const uint32_t acc = (zero && kk == 0) ? 0u : 1u;
+            const uint32_t acc = (zero && k2 == 0) ? 0u : 1u;
             mma_bf16_ts(tmem + kDV, tmem + kST + 64 * half + kk * 8, do_mn + boff, idesc_o, acc);
             mma_bf16_ts(tmem + kDK, tmem + kDPT + 64 * half + kk * 8, q_mn + boff, idesc_o, acc);
           }
@@ -1213,15 +1216,21 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         const bool more = e + 1 < n_ent;
         mbar_wait(&sm.pds_full[0], e & 1);
         tc_fence_after();
-        issue_acc(e, 0, e == 0);
+        issue_acc(e, 0, 0, e == 0);
+        mbar_wait(&sm.pds_full[1], e & 1);
+        tc_fence_after();
+        issue_acc(e, 0, 1, false);
         if (more) {
           mbar_wait(&sm.q_full[(e + 1) & 1], ((e + 1) >> 1) & 1);
           tc_fence_after();
           issue_s(e + 1, 0);
         }
-        mbar_wait(&sm.pds_full[1], e & 1);
+        mbar_wait(&sm.pds_full[2], e & 1);
         tc_fence_after();
-        issue_acc(e, 1, false);
+        issue_acc(e, 1, 0, false);
+        mbar_wait(&sm.pds_full[3], e & 1);
+        tc_fence_after();
+        issue_acc(e, 1, 1, false);
         if (elect_one()) {
           mma_commit(&sm.q_free[e & 1]);
           if (!more) mma_commit(&sm.acc_done);
@@ -1248,17 +1257,23 @@ __global__ void __launch_bounds__(kPPThreads, 1)
           p.causal && h == 1 && static_cast<int64_t>(j0 + 1) * p.b_k - 1 > static_cast<int64_t>(iq) * p.b_q;
       const int kpos = j0 * p.b_k + row;
       const int qpos0 = iq * p.b_q + 64 * g;
-      uint32_t pp[32], sp[32];
       // rows of blocks this entry did not select at h: exp2(-inf) = 0 through the additive term
       const float kill = live ? 0.f : -INFINITY;
       const float2 kill2 = make_float2(kill, kill);
+      uint32_t sva[32], dva[32], svb[32], dvb[32];  // both 32-query chunks in flight at once
+      tmem_ld32(t_lane + kST + 64 * g, sva);
+      tmem_ld32(t_lane + kDPT + 64 * g, dva);
+      tmem_ld32(t_lane + kST + 64 * g + 32, svb);
+      tmem_ld32(t_lane + kDPT + 64 * g + 32, dvb);
+      tmem_ld_wait(sva);
+      tmem_ld_wait(dva);
+      tmem_ld_wait(svb);
+      tmem_ld_wait(dvb);
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {  // 32 query columns at a time (register pressure)
-        uint32_t sv2[32], dv2[32];
-        tmem_ld32(t_lane + kST + 64 * g + c * 32, sv2);
-        tmem_ld32(t_lane + kDPT + 64 * g + c * 32, dv2);
-        tmem_ld_wait(sv2);
-        tmem_ld_wait(dv2);
+      for (int c = 0; c < 2; ++c) {  // each chunk is handed to the MMA warp as soon as it is packed
+        uint32_t (&sv2)[32] = c == 0 ? sva : svb;
+        uint32_t (&dv2)[32] = c == 0 ? dva : dvb;
+        uint32_t pp[16], sp[16];
 #pragma unroll
         for (int e2 = 0; e2 < 32; e2 += 2) {
           const int cl = c * 32 + e2;  // column within this warpgroup's 64
@@ -1272,18 +1287,18 @@ __global__ void __launch_bounds__(kPPThreads, 1)
             if (kpos > qpos0 + cl) p0 = 0.f;
             if (kpos > qpos0 + cl + 1) p1 = 0.f;
           }
-          pp[cl >> 1] = pack_bf16x2(p0, p1);
-          sp[cl >> 1] = pack_bf16x2(p0 * (__uint_as_float(dv2[e2]) - d2.x),
+          pp[e2 >> 1] = pack_bf16x2(p0, p1);
+          sp[e2 >> 1] = pack_bf16x2(p0 * (__uint_as_float(dv2[e2]) - d2.x),
                                     p1 * (__uint_as_float(dv2[e2 + 1]) - d2.y));
         }
+        // P'^T / dS^T as bf16 pairs over already-read columns: chunk c -> [64 g + 16 c, + 16)
+        tmem_st16(t_lane + kST + 64 * g + 16 * c, pp);
+        tmem_st16(t_lane + kDPT + 64 * g + 16 * c, sp);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.pds_full[2 * g + c]);
       }
-      // P'^T / dS^T as bf16 pairs over the first 32 of this half's (already read) columns
-      tmem_st32(t_lane + kST + 64 * g, pp);
-      tmem_st32(t_lane + kDPT + 64 * g, sp);
-      tmem_st_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.pds_full[g]);
     }
     // ---- the unit's pooled rows -> the level-h slab (zeros when no entry selected them)
     if (n_ent > 0) {
