@@ -639,7 +639,7 @@ struct BwdQSmem {
   uint64_t q_full;
   uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
   uint64_t meta_full[kMetaRing], meta_empty[kMetaRing];
-  uint64_t s_full[2], sp_read, ds_full, dq_done;
+  uint64_t s_full[2], sp_read, ds_full[2], dq_done;
   uint32_t tmem_base;
 };
 
@@ -682,7 +682,8 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       mbar_init(&sm.meta_empty[s], 8);  // one arrive per softmax warp
     }
     mbar_init(&sm.sp_read, 8);
-    mbar_init(&sm.ds_full, 8);
+    mbar_init(&sm.ds_full[0], 4);  // one per softmax warpgroup (key half)
+    mbar_init(&sm.ds_full[1], 4);
     mbar_init(&sm.dq_done, 1);
     fence_barrier_init();
   }
@@ -822,18 +823,26 @@ __global__ void __launch_bounds__(kPPThreads, 1)
             mbar_wait(&sm.sp_read, t & 1);  // softmax read S(t) and dP(t)
             issue_sd(t + 1);
           }
-          mbar_wait(&sm.ds_full, t & 1);
-          tc_fence_after();
           const uint64_t kmn_desc0 = umma_desc_sw128(smem_u32(sm.k[st]), kTileRows * 128, 1024);
-          if (elect_one()) {
-            // dS(t) (bf16 pairs) sits in S[t & 1]: key columns [64 g, 64 g + 64) packed into
-            // [64 g, 64 g + 32); the A operand comes from tensor memory
+          // dS(t) (bf16 pairs) sits in S[t & 1]: key columns [64 g, 64 g + 64) packed into
+          // [64 g, 64 g + 32); the A operand comes from tensor memory. Each key half goes to the
+          // tensor core as soon as its warpgroup has packed it.
 #pragma unroll
-            for (int kk = 0; kk < kTileRows / 16; ++kk) {
-              const uint32_t acol = st * 128 + 64 * (kk >> 2) + (kk & 3) * 8;
-              mma_bf16_ts(tmem + kDQ, tmem + acol, kmn_desc0 + ((kk * 16 * 128) >> 4), idesc_q,
-                          (t > 0 || kk > 0) ? 1u : 0u);
+          for (int kh = 0; kh < 2; ++kh) {
+            mbar_wait(&sm.ds_full[kh], t & 1);
+            tc_fence_after();
+            if (elect_one()) {
+#pragma unroll
+              for (int k4 = 0; k4 < 4; ++k4) {
+                const int kk = 4 * kh + k4;
+                const uint32_t acol = st * 128 + 64 * kh + k4 * 8;
+                mma_bf16_ts(tmem + kDQ, tmem + acol, kmn_desc0 + ((kk * 16 * 128) >> 4), idesc_q,
+                            (t > 0 || kk > 0) ? 1u : 0u);
+              }
             }
+            __syncwarp();
+          }
+          if (elect_one()) {
             mma_commit(&sm.k_empty[st]);
             if (t + 1 == T) mma_commit(&sm.dq_done);
           }
@@ -903,7 +912,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.ds_full);
+      if (lane == 0) mbar_arrive(&sm.ds_full[g]);
     }
     if (T > 0) {
       mbar_wait(&sm.dq_done, 0);
