@@ -62,3 +62,15 @@ with profile(activities=[ProfilerActivity.CUDA]) as prof:
 for ev in prof.key_averages():
     if ev.device_type.name == "CUDA" and ev.count:
         print(f"  {ev.key[:60]:60s} x{ev.count:3d} {ev.device_time_total / ev.count / 1e3:9.3f} ms")
+
+# dK/dV row packing: MMA rows that carry a selected block, per level (live rows / tile rows)
+lm = res.plan.level_map.to(torch.int16)
+nk = lm.shape[-1]
+for h in range(1, cfg["levels"] + 1):
+    f = 1 << (h - 1)
+    pad = (-nk) % f
+    hit = torch.nn.functional.pad((lm == h).to(torch.int16), (0, pad)).view(*lm.shape[:-1], -1, f)
+    ent = int(hit.any(-1).sum())
+    live = int(hit.sum())
+    eff = live / max(ent * f, 1)
+    print(f"  level {h}: entries {ent:9d}  selected blocks {live:9d}  live-row fraction {eff:.3f}")
