@@ -632,16 +632,18 @@ static int launch_attn(const void* q, const void* k, const void* v, const void* 
 struct BwdQSmem {
   uint8_t q[kTileRows * 128 * 2];
   uint8_t dout[kTileRows * 128 * 2];
-  uint8_t k[2][kTileRows * 128 * 2];
+  uint8_t k[3][kTileRows * 128 * 2];  // K lives until dQ(t) has read it: one stage deeper than V
   uint8_t v[2][kTileRows * 128 * 2];
   float bias[kMetaRing][kTileRows];
   uint32_t meta[kMetaRing][kChunks];
   uint64_t q_full;
-  uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
+  uint64_t k_full[3], k_empty[3], v_full[2], v_empty[2];
   uint64_t meta_full[kMetaRing], meta_empty[kMetaRing];
   uint64_t s_full[2], sp_read, ds_full[2], dq_done;
   uint32_t tmem_base;
 };
+
+static_assert(sizeof(BwdQSmem) <= 227 * 1024, "dQ kernel shared memory exceeds the sm_100 limit");
 
 struct BwdQMaps {
   AttnMaps a;  // q, k[], v[]
@@ -670,9 +672,11 @@ __global__ void __launch_bounds__(kPPThreads, 1)
   if (threadIdx.x == 0) {
     if (smem_u32(smem_raw) & 1023u) __trap();
     mbar_init(&sm.q_full, 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < 3; ++s) {
       mbar_init(&sm.k_full[s], 1);
       mbar_init(&sm.k_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
       mbar_init(&sm.v_full[s], 1);
       mbar_init(&sm.v_empty[s], 1);
       mbar_init(&sm.s_full[s], 1);
@@ -693,7 +697,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
   }
   {  // K/V rows past the last filled slot of a tile are read by the MMAs: keep them finite
     uint4* z = reinterpret_cast<uint4*>(&sm.k[0][0]);
-    const int nvec = 4 * kTileRows * 128 * 2 / 16;
+    const int nvec = 5 * kTileRows * 128 * 2 / 16;  // k[3], v[2]
     for (int t = threadIdx.x; t < nvec; t += kPPThreads) z[t] = make_uint4(0, 0, 0, 0);
     fence_proxy_async_smem();
   }
@@ -718,9 +722,9 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         PlanCursor pc;
         pc.init(csr + unit * p.n_k, n_ent, lane);
         for (int t = 0; t < T; ++t) {
-          const int ks = t & 1;
+          const int ks = t % 3;
           const TileSeg sg = pc.next(p, bhkv, lane);
-          if (t >= 2) mbar_wait(&sm.k_empty[ks], ((t >> 1) - 1) & 1);
+          if (t >= 3) mbar_wait(&sm.k_empty[ks], ((t / 3) - 1) & 1);
           if (lane == 0) mbar_arrive_expect_tx(&sm.k_full[ks], static_cast<uint32_t>(sg.total) * D * 2);
           __syncwarp();
           if (sg.fits)
@@ -790,11 +794,11 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         const uint64_t q_desc0 = umma_desc_sw128(smem_u32(sm.q), 16, 1024);
         const uint64_t do_desc0 = umma_desc_sw128(smem_u32(sm.dout), 16, 1024);
         auto issue_sd = [&](int t) {  // S(t) = Q K^T into S[t & 1], dP(t) = dO V^T
-          const int st = t & 1;
-          mbar_wait(&sm.k_full[st], (t >> 1) & 1);
+          const int st = t & 1, kst = t % 3;
+          mbar_wait(&sm.k_full[kst], (t / 3) & 1);
           mbar_wait(&sm.v_full[st], (t >> 1) & 1);
           tc_fence_after();
-          const uint64_t k_desc0 = umma_desc_sw128(smem_u32(sm.k[st]), 16, 1024);
+          const uint64_t k_desc0 = umma_desc_sw128(smem_u32(sm.k[kst]), 16, 1024);
           const uint64_t v_desc0 = umma_desc_sw128(smem_u32(sm.v[st]), 16, 1024);
           if (elect_one()) {
 #pragma unroll
@@ -823,7 +827,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
             mbar_wait(&sm.sp_read, t & 1);  // softmax read S(t) and dP(t)
             issue_sd(t + 1);
           }
-          const uint64_t kmn_desc0 = umma_desc_sw128(smem_u32(sm.k[st]), kTileRows * 128, 1024);
+          const uint64_t kmn_desc0 = umma_desc_sw128(smem_u32(sm.k[t % 3]), kTileRows * 128, 1024);
           // dS(t) (bf16 pairs) sits in S[t & 1]: key columns [64 g, 64 g + 64) packed into
           // [64 g, 64 g + 32); the A operand comes from tensor memory. Each key half goes to the
           // tensor core as soon as its warpgroup has packed it.
@@ -843,7 +847,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
             __syncwarp();
           }
           if (elect_one()) {
-            mma_commit(&sm.k_empty[st]);
+            mma_commit(&sm.k_empty[t % 3]);
             if (t + 1 == T) mma_commit(&sm.dq_done);
           }
           __syncwarp();

@@ -19,13 +19,13 @@
 //
 // At D = 128 both passes run on tcgen05 / TMEM (psa_attention.cu):
 //  - psa_bwd_dq_tc_kernel: the forward's producers and plan walk, S and dP in TMEM, dS written
-//    back over S as the TMEM A operand of dQ += dS K; 26 ms at cfg3;
+//    back over S as the TMEM A operand of dQ += dS K, 3-stage K ring; 29 ms at cfg3;
 //  - psa_bwd_dkv_tc_kernel: one CTA per (KV head, level, unit of 2^(h-1) blocks packed into one
 //    tile), S^T / dP^T in TMEM, P'^T / dS^T written back over them as the TMEM A operand of
 //    dV / dK, double-buffered Q / dO, per-level pooled fp32 slabs summed by bwd_unpool_kernel;
 //    70 ms at cfg3.
 // D = 64 uses warp-level mma.sync kernels (m16n8k16 bf16, fp32 accumulate, ldmatrix fragments,
-// cp.async double-buffered tiles). cfg3 backward ~117 ms against a 34 ms forward.
+// cp.async double-buffered tiles). cfg3 backward ~109 ms against a 34 ms forward.
 #include "common.cuh"
 #include "psa_internal.h"
 
