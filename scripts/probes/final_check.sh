@@ -9,6 +9,6 @@ echo "bwd probe rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:psa_bwd_dkv_tc -s 2 -c 1 \
    -o gpurun_out/psa_bwd_dkv_tc_full -f python scripts/probes/bwd_probe.py > gpurun_out/ncu_bwd_dkv.log 2>&1
 echo "ncu bwd_dkv rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:psa_bwd_dq_tc -s 2 -c 1 \
-   -o gpurun_out/psa_bwd_dq_tc_full -f python scripts/probes/bwd_probe.py > gpurun_out/ncu_bwd_dq.log 2>&1
+timeout 600 ncu --section SpeedOfLight --section WarpStateStats --section ComputeWorkloadAnalysis --clock-control none -k regex:psa_bwd_dq_tc -s 2 -c 1 \
+   python scripts/probes/bwd_probe.py > gpurun_out/ncu_bwd_dq.log 2>&1
 echo "ncu bwd_dq rc=$?"
