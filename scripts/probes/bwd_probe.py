@@ -51,6 +51,8 @@ counts = res.plan.level_counts.cpu().tolist()
 sel_blocks = sum(counts[1:])
 flops = 2.5 * 4 * cfg["d"] * sel_blocks * cfg["b_q"] * cfg["b_k"]  # expanded blocks: S, dP, dV, dK, dQ
 print(f"cfg3 backward {ms:.2f} ms; selected blocks {sel_blocks}; {flops / ms / 1e9:.0f} TFLOP/s on expanded-block work")
+alg = 2.5 * bench.flops_from_counts(counts, cfg, cfg["B"] * cfg["Hq"])  # pooled work: 5 GEMMs vs 2
+print(f"cfg3 backward algorithmic work {alg / 1e12:.1f} TFLOP (2.5x the forward's): {alg / ms / 1e9:.0f} TFLOP/s")
 
 # per-kernel device times (CUPTI) of the same calls
 from torch.profiler import ProfilerActivity, profile  # noqa: E402
