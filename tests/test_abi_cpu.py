@@ -58,6 +58,11 @@ def test_argument_errors_map_to_validation_error():
     # n=1024, b_k=64, stride 4 -> per=16 (int8 path: one block per 16-key half -> 16 chunks)
     fp64 = 8 * 2 * 1024 * (16 + 16 + 2)
     assert lib.psa_antidiag_workspace_bytes(2, 2, 1024, 64, 64, 4) > fp64
+    # backward: D rows + -lse log2(e) per query row (64-padded each), then fp32 dK/dV slabs of all
+    # pyramid levels (< 2n pooled rows per KV head, psa_attention.cu psa_bwd_dkv_tc_kernel)
+    rows = 2 * 8 * 1000
+    pad = (rows + 63) // 64 * 64
+    assert lib.psa_attn_bwd_workspace_bytes(2, 8, 2, 1000, 128) == 4 * (2 * pad + 4 * 2 * 2 * 1000 * 128)
     # stride 1 -> per=64 > 16: fp64 path only, 64-key chunks -> 16 chunks
     assert lib.psa_antidiag_workspace_bytes(2, 2, 1024, 64, 64, 1) == fp64
 
