@@ -1266,6 +1266,9 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       const int iq = static_cast<int>(ents[e]) % p.n_q;
       const bool live = blk < nb && ((emask[e] >> blk) & 1u);
       const int qb = e & 1;
+      // nl2 / D rows of this entry: acquire them from their own transaction (already complete,
+      // since S^T read the Q tile of the same phase), not only through the MMA warp's commit
+      mbar_wait(&sm.q_full[qb], (e >> 1) & 1);
       const bool straddle =  // causal diagonal blocks are always level 1 (f = 1)
           p.causal && h == 1 && static_cast<int64_t>(j0 + 1) * p.b_k - 1 > static_cast<int64_t>(iq) * p.b_q;
       const int kpos = j0 * p.b_k + row;
