@@ -20,7 +20,9 @@ class _PSAFunction(torch.autograd.Function):
     def forward(ctx, q4, k4, v4, cfg):
         from .pipeline import psa_forward_4d
         res = psa_forward_4d(q4, k4, v4, cfg)
-        ctx.save_for_backward(q4, res.out, res.lse)
+        # K/V ride in the saved tensors too (the pyramid's level 1 is the caller's K/V), so an
+        # in-place edit between forward and backward trips autograd's version check
+        ctx.save_for_backward(q4, k4, v4, res.out, res.lse)
         ctx.pyr, ctx.plan, ctx.causal = res.pyramid, res.plan, cfg.causal
         ctx.mark_non_differentiable(res.lse)
         return res.out, res.lse
@@ -28,7 +30,7 @@ class _PSAFunction(torch.autograd.Function):
     @staticmethod
     def backward(ctx, dout, _dlse):
         from .attention import attention_backward
-        q4, out, lse = ctx.saved_tensors
+        q4, _k4, _v4, out, lse = ctx.saved_tensors
         dq, dk, dv = attention_backward(q4, ctx.pyr, ctx.plan, ctx.causal, out, lse, dout)
         return dq, dk, dv, None
 

@@ -1012,6 +1012,18 @@ int attn_bwd_dq_tc(const void* q, const void* k, const void* v, const void* k_py
 //   dV_h += P'^T dO and dK_h += dS^T Q (dO / Q read MN-major like V in the forward) in TMEM.
 // At the end of a level the pooled rows are spread over their 2^(h-1) raw rows into the CTA's
 // fp32 scratch rows; the last step writes bf16 dK (x scale) and dV. TMEM: S^T | dP^T | dV | dK.
+// dK/dV work unit: up to kDkvUnitBlocks KV blocks of one level packed into one tile
+// (2^(h-1) blocks of L = b_k >> (h-1) rows at level h, capped at 16 so that the per-entry block
+// mask fits its 16 bits for every level up to kMaxLevels).
+constexpr int kDkvUnitBlocks = 16;
+__host__ __device__ inline int dkv_unit_blocks(int h) {
+  return (1 << (h - 1)) < kDkvUnitBlocks ? (1 << (h - 1)) : kDkvUnitBlocks;
+}
+__host__ __device__ inline int dkv_level_units(int n_k, int h) {
+  const int f = dkv_unit_blocks(h);
+  return (n_k + f - 1) / f;
+}
+
 struct BwdKVSmem {
   uint8_t kt[kTileRows * 128 * 2];
   uint8_t vt[kTileRows * 128 * 2];
@@ -1049,12 +1061,12 @@ __global__ void __launch_bounds__(kPPThreads, 1)
   // blockIdx.x -> (level h, unit u): level h has ceil(n_k / 2^(h-1)) units
   int h = 1, u = blockIdx.x;
   int64_t slab = 0;  // pooled rows of the levels before h (scratch slab offset, per KV head)
-  while (u >= (p.n_k + (1 << (h - 1)) - 1) >> (h - 1)) {
-    u -= (p.n_k + (1 << (h - 1)) - 1) >> (h - 1);
+  while (u >= dkv_level_units(p.n_k, h)) {
+    u -= dkv_level_units(p.n_k, h);
     slab += p.n >> (h - 1);
     ++h;
   }
-  const int f = 1 << (h - 1);
+  const int f = dkv_unit_blocks(h);
   const int L = p.b_k >> (h - 1);
   const int j0 = u * f;
   const int nb = min(f, p.n_k - j0);  // blocks in this unit
@@ -1424,7 +1436,7 @@ int attn_bwd_dkv_tc(const void* q, const void* k, const void* v, const void* k_p
     if (rc) return rc;
     rc = encode_2d(&maps.a.v[h - 1], vb, rows, D, sz);
     if (rc) return rc;
-    units += (p.n_k + (1 << (h - 1)) - 1) >> (h - 1);
+    units += dkv_level_units(p.n_k, h);
   }
   const int cap = (hq / hkv) * p.n_q;
   const size_t smem = sizeof(BwdKVSmem) + static_cast<size_t>(cap) * 6;

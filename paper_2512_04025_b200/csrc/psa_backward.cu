@@ -638,6 +638,11 @@ extern "C" int psa_attn_bwd(const void* q, const void* k, const void* v, const v
   PSA_CHECK_ARG(levels == 1 || (k_pyr && v_pyr), "pyramid pointers required for levels > 1");
   PSA_CHECK_ARG(hq >= 1 && hkv >= 1 && hq % hkv == 0, "query heads must be a multiple of kv heads");
   PSA_CHECK_ARG(n / b_k <= 4096, "n_k must be <= 4096");
+  // same coordinate guards as the forward (TMA coordinates and row indices are 32-bit), and the
+  // dK/dV grid's y dimension is batch * hkv
+  PSA_CHECK_ARG(batch * hq * n < (int64_t(1) << 31), "too many rows for 32-bit TMA coordinates");
+  PSA_CHECK_ARG(n < (int64_t(1) << 23), "seq_len must be < 2^23");
+  PSA_CHECK_ARG(batch * hkv <= 65535, "batch * kv heads must be <= 65535 for the backward grid");
   BwdParams p{};
   p.n = n;
   p.bkv_total = batch * hkv;

@@ -105,3 +105,60 @@ def test_autograd_function_matches_direct_backward():
                                     g.to(torch.bfloat16)[None])
     for mine, ref in ((qd.grad, dq), (kd.grad, dk), (vd.grad, dv)):
         assert torch.equal(mine.to(torch.bfloat16), ref[0])
+
+
+@pytest.mark.parametrize("B,levels,taus", [
+    (2, 4, (0.25, 0.45, 0.6, 0.9)),
+    # deep pyramids: level-6..8 dK/dV units hold 16 of the 2^(h-1) blocks (per-entry 16-bit mask)
+    (1, 6, (0.1, 0.2, 0.3, 0.4, 0.5, 0.95)),
+    (1, 8, (0.08, 0.16, 0.24, 0.32, 0.4, 0.5, 0.6, 0.95))])
+def test_backward_batch_and_deep_levels(B, levels, taus):
+    import paper_2512_04025_b200 as psa
+    from paper_2512_04025_b200.attention import attention_backward
+    n, d, b, hq, hkv = 4096, 128, 128, 2, 1
+    qs, ks, vs = zip(*(gaussian_qkv(70 + bi, hq, n, d, hkv) for bi in range(B)))
+    q, k, v = (np.stack(x) for x in (qs, ks, vs))
+    g = np.random.default_rng(71).standard_normal((B, hq, n, d))
+    cfg = psa.RunConfig.from_dict(dict(n=n, d=d, b_q=b, b_k=b, levels=levels,
+                                       estimator="sampled-max", s_q=8, s_k=8, seed=0,
+                                       mask="threshold", thresholds=list(taus), tile_len=128))
+    q4, k4, v4 = (to_dev(x) for x in (q, k, v))
+    res = psa.psa_forward_4d(q4, k4, v4, cfg)
+    lm = res.plan.level_map.cpu().numpy()
+    assert (lm == levels).any() and (lm == 1).any()
+    dq, dk, dv = attention_backward(q4, res.pyramid, res.plan, False, res.out, res.lse, to_dev(g))
+    for bi in range(B):
+        qt, kt, vt = (torch.from_numpy(x[bi]).requires_grad_(True) for x in (q, k, v))
+        out = _oracle(qt, kt, vt, lm[bi], b, b, False)
+        assert rel_l2(res.out[bi].float().cpu().numpy(), out.detach().numpy()) <= 1e-2
+        (out * torch.from_numpy(g[bi])).sum().backward()
+        for mine, ref in ((dq, qt.grad), (dk, kt.grad), (dv, vt.grad)):
+            assert rel_l2(mine[bi].float().cpu().numpy(), ref.numpy()) <= 1e-2, (bi, levels)
+
+
+def test_autograd_causal_gqa_matches_fp64():
+    """psa_attention_differentiable with causal GQA (4 query heads on 2 KV heads): gradients on
+    the user's tensors against the fp64 autograd oracle with the same level map."""
+    import paper_2512_04025_b200 as psa
+    n, d, b_q, b_k, hq, hkv = 1024, 128, 128, 64, 4, 2
+    q, k, v = gaussian_qkv(73, hq, n, d, hkv)
+    g = np.random.default_rng(74).standard_normal((hq, n, d))
+    kw = dict(b_q=b_q, b_k=b_k, levels=4, estimator="sampled-max", s_q=8, s_k=8, seed=0,
+              mask="threshold", thresholds=[0.25, 0.45, 0.6, 0.9], tile_len=128, causal=True)
+    qd, kd, vd = (to_dev(x).requires_grad_(True) for x in (q, k, v))
+    out, _ = psa.psa_attention_differentiable(qd, kd, vd, **kw)
+    (out.float() * torch.from_numpy(g).float().cuda()).sum().backward()
+    cfg = psa.RunConfig.from_dict(dict(n=n, d=d, **kw))
+    res = psa.psa_forward_4d(*(x.detach()[None] for x in (qd, kd, vd)), cfg)
+    lm = res.plan.level_map[0].cpu().numpy()
+    qt, kt, vt = (torch.from_numpy(x).requires_grad_(True) for x in (q, k, v))
+    ref = _oracle(qt, kt, vt, lm, b_q, b_k, True)
+    (ref * torch.from_numpy(g)).sum().backward()
+    for mine, r in ((qd.grad, qt.grad), (kd.grad, kt.grad), (vd.grad, vt.grad)):
+        assert rel_l2(mine.float().cpu().numpy(), r.numpy()) <= 1e-2
+    # an in-place edit of K between forward and backward is caught by autograd
+    out2, _ = psa.psa_attention_differentiable(qd, kd, vd, **kw)
+    with torch.no_grad():
+        kd.add_(0)
+    with pytest.raises(RuntimeError):
+        out2.float().sum().backward()
