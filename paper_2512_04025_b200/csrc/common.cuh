@@ -210,6 +210,17 @@ PSA_DEV uint64_t umma_desc_sw128(uint32_t saddr, uint32_t lbo_bytes, uint32_t sb
   d |= static_cast<uint64_t>(2) << 61;  // SWIZZLE_128B
   return d;
 }
+// Shared-memory matrix descriptor, no swizzle, K-major: 8-row x 16-byte core matrices; LBO = byte
+// stride between core matrices adjacent in K, SBO = between core matrices adjacent in M/N
+// (measured, scripts/probes/umma_aug_probe.cu). A zero stride broadcasts one core matrix.
+PSA_DEV uint64_t umma_desc_noswz(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFFu) << 32;
+  d |= static_cast<uint64_t>(1) << 46;  // descriptor version (sm_100); layout 0 = no swizzle
+  return d;
+}
 // Instruction descriptor for kind::f16: bf16 A/B, fp32 D.
 __host__ __device__ constexpr uint32_t umma_idesc_bf16(int M, int N, bool a_mn_major,
                                                        bool b_mn_major) {

@@ -44,7 +44,13 @@ struct AttnParams {
   int hq, hkv, b_q, b_k, levels, n_q, n_k, causal;
   float scale_log2;
   const int64_t* out_rows;  // optional scatter: O/lse row i of a head goes to row out_rows[i]
+  // forward: the level bias (h-1)*ln2 of attention.py:39-44 in raw logit units, (h-1)/scale_log2,
+  // as three bf16 terms
+  // hi | mid << 16, lo, i.e. the first 8 bytes of a key's augmentation row (see kAugPad)
+  uint32_t aug[kMaxLevels][2];
 };
+// augmentation row of a pad key: -2^100 in the first column (S -> -1.3e30: exp2 -> 0, never the max)
+constexpr uint32_t kAugPad = 0xF180u;
 
 // Tile packing shared by the K and V producer warps: lane l (< 16) owns plan entry e + l; a
 // warp inclusive scan of the slot sizes gives each segment's row offset in the tile, and the
@@ -121,9 +127,17 @@ template <int D>
 struct PP2Cfg {
   static constexpr int kKStages = D == 128 ? 2 : 3;
   static constexpr int kVStages = D == 128 ? 2 : 3;
+  static constexpr int kAugStages = D == 128 ? 1 : 2;  // one 2 KB stage is all that fits at D=128
   static constexpr int kTileBytes = kTileRows * D * 2;
 };
 
+// The level bias enters S through the tensor core: S = [Q | Qa] [K | Ka]^T with one extra K=16
+// step, Qa = (1, 1, 1, 0, ...) for every query row and Ka = (hi, mid, lo, 0, ...) of the key's
+// bias (h-1)/scale_log2 (= (h-1) ln 2 after the softmax scale, exactly h-1 in the log2 domain)
+// split into three bf16 terms (pad keys: -2^100). The softmax then works on
+// raw S like dense attention (no per-column bias loads or adds; pad keys need no masking).
+// Ka: no-swizzle K-major, 16 B per key (its second 8-column core matrix aliases the first: LBO = 0,
+// matched by zeros in Qa's second core matrix); Qa: one core matrix broadcast to every row (SBO = 0).
 template <int D>
 struct PP2Smem {
   using C = PP2Cfg<D>;
@@ -131,11 +145,13 @@ struct PP2Smem {
   uint8_t k[C::kKStages][C::kTileBytes];
   uint8_t v[C::kVStages][C::kTileBytes];
   uint8_t p[2][kTileRows * kTileRows * 2];
-  float bias[kMetaRing][kTileRows];
+  uint8_t kaug[C::kAugStages][kTileRows * 16];
+  uint8_t qaug[256];
   uint32_t meta[kMetaRing][kChunks];
   uint64_t q_full;
   uint64_t k_full[C::kKStages], k_empty[C::kKStages];
   uint64_t v_full[C::kVStages], v_empty[C::kVStages];
+  uint64_t aug_full[C::kAugStages], aug_empty[C::kAugStages];
   uint64_t meta_full[kMetaRing], meta_empty[kMetaRing];
   uint64_t s_full[2], s_free[2], p_full[2], o_done[2];
   uint32_t tmem_base;
@@ -148,7 +164,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
                        uint16_t* __restrict__ out, float* __restrict__ lse,
                        int32_t* __restrict__ skipped) {
   using C = PP2Cfg<D>;
-  constexpr int KST = C::kKStages, VST = C::kVStages;
+  constexpr int KST = C::kKStages, VST = C::kVStages, AST = C::kAugStages;
   constexpr uint32_t kO0 = 256;  // O_L at kO0 + L * D
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   auto& sm = *reinterpret_cast<PP2Smem<D>*>(smem_raw);
@@ -173,6 +189,10 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     for (int s = 0; s < VST; ++s) {
       mbar_init(&sm.v_full[s], 1);
       mbar_init(&sm.v_empty[s], 1);
+    }
+    for (int s = 0; s < AST; ++s) {
+      mbar_init(&sm.aug_full[s], 1);
+      mbar_init(&sm.aug_empty[s], 1);
     }
     for (int s = 0; s < kMetaRing; ++s) {
       mbar_init(&sm.meta_full[s], 1);
@@ -201,6 +221,9 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     uint4* z = reinterpret_cast<uint4*>(&sm.k[0][0]);
     const int nvec = (KST + VST) * C::kTileBytes / 16;
     for (int t = threadIdx.x; t < nvec; t += kPPThreads) z[t] = make_uint4(0, 0, 0, 0);  // K, V
+    if (threadIdx.x < 16)  // Qa: core matrix 0 rows = (1, 1, 1, 0, 0, 0, 0, 0), core matrix 1 = 0
+      reinterpret_cast<uint4*>(sm.qaug)[threadIdx.x] =
+          threadIdx.x < 8 ? make_uint4(0x3F803F80u, 0x00003F80u, 0u, 0u) : make_uint4(0u, 0u, 0u, 0u);
     fence_proxy_async_smem();
   }
   tc_fence_before();
@@ -251,16 +274,16 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         }
       }
     } else if (warp == 2) {
-      // ============================================================ bias/meta producer
+      // ============================================================ bias rows (Ka) + causal meta
       if (T > 0) {
         const int64_t q_lo = static_cast<int64_t>(i) * p.b_q;
         PlanCursor pc;
         pc.init(csr + unit * p.n_k, n_ent, lane);
         for (int t = 0; t < T; ++t) {
-          const int ms = t % kMetaRing;
+          const int as = t % AST;
           const TileSeg sg = pc.next(p, bhkv, lane);
-          if (t >= kMetaRing) mbar_wait(&sm.meta_empty[ms], ((t / kMetaRing) - 1) & 1);
-          {
+          if (t >= AST) mbar_wait(&sm.aug_empty[as], ((t / AST) - 1) & 1);  // S(t - AST) done
+          {  // lane owns keys 4 lane .. 4 lane + 3 (one segment: slots are >= 8 rows, aligned)
             int g = 0;
             for (int q = 1; q < sg.nseg; ++q)
               if (__shfl_sync(0xffffffffu, sg.off, q) <= 4 * lane) g = q;
@@ -268,25 +291,33 @@ __global__ void __launch_bounds__(kPPThreads, 1)
             const int gL = __shfl_sync(0xffffffffu, sg.L, g);
             const int gh = __shfl_sync(0xffffffffu, sg.h, g);
             const int r0 = 4 * lane - goff;
-            const float bv = static_cast<float>(gh - 1);
-            float4 w = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
-            if (4 * lane < sg.total) {
-              w.x = r0 + 0 < gL ? bv : -INFINITY;
-              w.y = r0 + 1 < gL ? bv : -INFINITY;
-              w.z = r0 + 2 < gL ? bv : -INFINITY;
-              w.w = r0 + 3 < gL ? bv : -INFINITY;
-            }
-            *reinterpret_cast<float4*>(&sm.bias[ms][4 * lane]) = w;
+            const bool in_tile = 4 * lane < sg.total;
+            const uint4 live = make_uint4(p.aug[gh - 1][0], p.aug[gh - 1][1], 0u, 0u);
+            const uint4 pad = make_uint4(kAugPad, 0u, 0u, 0u);
+            uint4* row = reinterpret_cast<uint4*>(sm.kaug[as]) + 4 * lane;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) row[e] = in_tile && r0 + e < gL ? live : pad;
           }
-          if (p.causal && sg.fits) {
-            const bool straddle = static_cast<int64_t>(sg.j + 1) * p.b_k - 1 > q_lo;
-            for (int c = 0; c < sg.sz / 8; ++c)
-              sm.meta[ms][sg.off / 8 + c] =
-                  (straddle ? 1u : 0u) | (static_cast<uint32_t>(sg.j * p.b_k + c * 8) << 1);
-          }
-          if (p.causal && lane < kChunks && 8 * lane >= sg.total) sm.meta[ms][lane] = 0u;
+          fence_proxy_async_smem();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&sm.meta_full[ms]);
+          if (lane == 0) mbar_arrive(&sm.aug_full[as]);
+          if (p.causal) {
+            // per 8-key chunk: straddle flag, valid keys of the chunk (pad keys of a straddling
+            // chunk are masked too, so a row with no visible key stays empty), first key position
+            const int ms = t % kMetaRing;
+            if (t >= kMetaRing) mbar_wait(&sm.meta_empty[ms], ((t / kMetaRing) - 1) & 1);
+            if (sg.fits) {
+              const bool straddle = static_cast<int64_t>(sg.j + 1) * p.b_k - 1 > q_lo;
+              for (int c = 0; c < sg.sz / 8; ++c) {
+                const int nv = max(0, min(8, sg.L - 8 * c));
+                sm.meta[ms][sg.off / 8 + c] = (straddle ? 1u : 0u) | (static_cast<uint32_t>(nv) << 1) |
+                                              (static_cast<uint32_t>(sg.j * p.b_k + c * 8) << 5);
+              }
+            }
+            if (lane < kChunks && 8 * lane >= sg.total) sm.meta[ms][lane] = 0u;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.meta_full[ms]);
+          }
         }
       }
     } else {
@@ -295,12 +326,15 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128, false, false);
         constexpr uint32_t idesc_o = umma_idesc_bf16(128, D, false, true);
         const uint64_t q_desc0 = umma_desc_sw128(smem_u32(sm.q), 16, 1024);
+        const uint64_t qa_desc = umma_desc_noswz(smem_u32(sm.qaug), 128, 0);
         auto issue_s = [&](int t) {
-          const int ks = t % KST, L = t & 1;
+          const int ks = t % KST, as = t % AST, L = t & 1;
           mbar_wait(&sm.k_full[ks], (t / KST) & 1);
           if (t >= 2) mbar_wait(&sm.s_free[L], ((t >> 1) - 1) & 1);  // lane read S(t-2)
+          mbar_wait(&sm.aug_full[as], (t / AST) & 1);
           tc_fence_after();
           const uint64_t k_desc0 = umma_desc_sw128(smem_u32(sm.k[ks]), 16, 1024);
+          const uint64_t ka_desc = umma_desc_noswz(smem_u32(sm.kaug[as]), 0, 128);
           if (elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < D / 16; ++kk) {
@@ -308,7 +342,9 @@ __global__ void __launch_bounds__(kPPThreads, 1)
               mma_bf16_ss(tmem + L * 128, q_desc0 + koff, k_desc0 + koff, idesc_s,
                           kk > 0 ? 1u : 0u);
             }
+            mma_bf16_ss(tmem + L * 128, qa_desc, ka_desc, idesc_s, 1u);  // + level bias
             mma_commit(&sm.k_empty[ks]);
+            mma_commit(&sm.aug_empty[as]);
             mma_commit(&sm.s_full[L]);
           }
           __syncwarp();
@@ -365,33 +401,23 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.s_free[L]);  // S_L may take tile t+2 now
-      // y = s * scale + bias_col (bias: level-1 in log2 units; -inf on pad columns)
-      mbar_wait(&sm.meta_full[ms], (t / kMetaRing) & 1);
+      // raw logits with the level bias already added by the tensor core (pad keys ~ -1.3e30)
       float y[128];
-      const float4* bias4 = reinterpret_cast<const float4*>(&sm.bias[ms][0]);
 #pragma unroll
-      for (int q4 = 0; q4 < 32; ++q4) {
-        const float4 bv = bias4[q4];
-        const float* x = reinterpret_cast<const float*>(&s[q4 >> 3][(q4 & 7) * 4]);
-        const float2 a = ffma2(make_float2(x[0], x[1]), scale2, make_float2(bv.x, bv.y));
-        const float2 c = ffma2(make_float2(x[2], x[3]), scale2, make_float2(bv.z, bv.w));
-        y[q4 * 4 + 0] = a.x;
-        y[q4 * 4 + 1] = a.y;
-        y[q4 * 4 + 2] = c.x;
-        y[q4 * 4 + 3] = c.y;
-      }
+      for (int e = 0; e < 128; ++e) y[e] = __uint_as_float(s[e >> 5][e & 31]);
       if (p.causal) {  // token-level mask on straddling level-1 chunks (attention.py:88-108)
+        mbar_wait(&sm.meta_full[ms], (t / kMetaRing) & 1);
 #pragma unroll
         for (int c = 0; c < kChunks; ++c) {
           const uint32_t w = sm.meta[ms][c];
           if (w & 1u) {
-            const int lim = qpos - static_cast<int>(w >> 1);
+            const int lim = min(qpos - static_cast<int>(w >> 5), static_cast<int>((w >> 1) & 15u) - 1);
 #pragma unroll
             for (int e = 0; e < 8; ++e) y[c * 8 + e] = (e <= lim) ? y[c * 8 + e] : -INFINITY;
           }
         }
+        mbar_arrive(&sm.meta_empty[ms]);
       }
-      mbar_arrive(&sm.meta_empty[ms]);
 
       float mx[4] = {fmax3(y[0], y[1], y[2]), fmax3(y[3], y[4], y[5]), fmax3(y[6], y[7], y[8]),
                      fmax3(y[9], y[10], y[11])};
@@ -404,7 +430,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       }
       mx[0] = fmax3(mx[0], y[124], y[125]);
       mx[1] = fmax3(mx[1], y[126], y[127]);
-      const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+      const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * p.scale_log2;
       const float m_new = fmaxf(m_run, mt);
       const bool resc = m_new > m_run + kRescaleThreshold;
       float alpha = 1.f;
@@ -418,8 +444,8 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       uint32_t pk[64];
 #pragma unroll
       for (int e = 0; e < 128; e += 4) {
-        float2 a = fadd2(make_float2(y[e], y[e + 1]), negm);
-        float2 c = fadd2(make_float2(y[e + 2], y[e + 3]), negm);
+        float2 a = ffma2(make_float2(y[e], y[e + 1]), scale2, negm);
+        float2 c = ffma2(make_float2(y[e + 2], y[e + 3]), scale2, negm);
         // every exp on MUFU: an FMA-pipe polynomial for the last 16/32/48/64 columns measured
         // 26.7/26.5/27.6/28.2 ms against 25.9 ms at cfg3 (the lanes are issue-bound, not MUFU-bound)
         a.x = ex2_approx(a.x);
@@ -544,6 +570,19 @@ __global__ void __launch_bounds__(kPPThreads, 1)
   }
 }
 // ------------------------------------------------------------------ host side
+static uint32_t host_bf16_rne(double x) {  // finite x in bf16 range: fp32 then RNE to bf16
+  const float f = static_cast<float>(x);
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  return (u + 0x7FFFu + ((u >> 16) & 1u)) >> 16;
+}
+static double host_bf16_to_double(uint32_t b) {
+  const uint32_t u = b << 16;
+  float f;
+  memcpy(&f, &u, 4);
+  return f;
+}
+
 EncodeTiledFn get_encode_fn() {
   static EncodeTiledFn fn = nullptr;
   if (fn == nullptr) {
@@ -593,6 +632,16 @@ static int launch_attn(const void* q, const void* k, const void* v, const void* 
   p.causal = causal;
   p.scale_log2 = static_cast<float>(1.4426950408889634 / sqrt(static_cast<double>(D)));
   p.out_rows = out_rows;
+  for (int h = 1; h <= levels; ++h) {  // bias (h-1)/scale_log2 as hi + mid + lo (bf16 terms)
+    double r = (h - 1) / static_cast<double>(p.scale_log2);
+    uint32_t t[3];
+    for (int e = 0; e < 3; ++e) {
+      t[e] = host_bf16_rne(r);
+      r -= host_bf16_to_double(t[e]);
+    }
+    p.aug[h - 1][0] = t[0] | (t[1] << 16);
+    p.aug[h - 1][1] = t[2];
+  }
   const int64_t bhkv = batch * hkv;
   int rc = encode_2d(&maps.q, q, static_cast<uint64_t>(batch * hq * n), D, kTileRows);
   if (rc) return rc;
