@@ -13,7 +13,10 @@ from pathlib import Path
 
 from .errors import NumericError, ValidationError
 
-LIB_PATH = Path(__file__).with_name("libpsa.so")
+import os
+
+# PSA_LIB_PATH: an alternative build of the same library (instrumented probe builds only)
+LIB_PATH = Path(os.environ.get("PSA_LIB_PATH") or Path(__file__).with_name("libpsa.so"))
 _lib = None
 
 PSA_OK, PSA_EINVAL, PSA_ENUMERIC, PSA_ECUDA = 0, -2, -4, -5

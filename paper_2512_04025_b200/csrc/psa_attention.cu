@@ -118,6 +118,44 @@ struct PlanCursor {
 // softmax warpgroups 216 (128*64 + 256*216 <= 384*168, else the increase never completes).
 constexpr int kPPThreads = 384;
 
+// Ka rows of a tile for the keys 4 lane .. 4 lane + 3 (one segment: slots are >= 8 rows, aligned)
+// and whether any row differs from the previous tile's (warp-uniform; tile 0 always "changes").
+PSA_DEV bool aug_rows(const TileSeg& sg, const AttnParams& p, int lane, int t, uint4 (&rows)[4],
+                      uint4 (&prev)[4]) {
+  int g = 0;
+  for (int q = 1; q < sg.nseg; ++q)
+    if (__shfl_sync(0xffffffffu, sg.off, q) <= 4 * lane) g = q;
+  const int goff = __shfl_sync(0xffffffffu, sg.off, g);
+  const int gL = __shfl_sync(0xffffffffu, sg.L, g);
+  const int gh = __shfl_sync(0xffffffffu, sg.h, g);
+  const int r0 = 4 * lane - goff;
+  const bool in_tile = 4 * lane < sg.total;
+  const uint4 live = make_uint4(p.aug[gh - 1][0], p.aug[gh - 1][1], 0u, 0u);
+  const uint4 pad = make_uint4(kAugPad, 0u, 0u, 0u);
+  bool diff = t == 0;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    rows[e] = in_tile && r0 + e < gL ? live : pad;
+    diff |= rows[e].x != prev[e].x || rows[e].y != prev[e].y;
+    prev[e] = rows[e];
+  }
+  return __any_sync(0xffffffffu, diff);
+}
+
+#ifdef PSA_TRACE
+// probe builds only (scripts/probes/pp2_trace2.py): clock64 stamps of 8 CTAs, 8 events x 256 tiles
+__device__ long long g_pp2_trace[8][16][256];
+PSA_DEV int trace_slot(int64_t unit) {
+  for (int s = 0; s < 8; ++s)
+    if (unit == 1234 + 3000 * s) return s;
+  return -1;
+}
+#define PSA_STAMP(ev, t) \
+  do { if (tslot >= 0 && (t) < 256) g_pp2_trace[tslot][ev][t] = clock64(); } while (0)
+#else
+#define PSA_STAMP(ev, t) do { } while (0)
+#endif
+
 template <uint32_t N>
 PSA_DEV void regs_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N)); }
 template <uint32_t N>
@@ -127,7 +165,6 @@ template <int D>
 struct PP2Cfg {
   static constexpr int kKStages = D == 128 ? 2 : 3;
   static constexpr int kVStages = D == 128 ? 2 : 3;
-  static constexpr int kAugStages = D == 128 ? 1 : 2;  // one 2 KB stage is all that fits at D=128
   static constexpr int kTileBytes = kTileRows * D * 2;
 };
 
@@ -138,6 +175,12 @@ struct PP2Cfg {
 // raw S like dense attention (no per-column bias loads or adds; pad keys need no masking).
 // Ka: no-swizzle K-major, 16 B per key (its second 8-column core matrix aliases the first: LBO = 0,
 // matched by zeros in Qa's second core matrix); Qa: one core matrix broadcast to every row (SBO = 0).
+// Only one 2 KB Ka buffer fits next to Q, K, V and P at D = 128, and consecutive tiles of a level
+// have identical Ka rows (same slots, same pads), so Ka is rewritten only when a tile's rows differ
+// from the previous tile's (a handful of times per unit): the bias warp and the MMA warp both walk
+// the plan, detects the changes and tells the MMA warp through a 4-slot flag ring; at a change the
+// MMA warp commits aug_empty (completes when every MMA issued so far, incl. the previous S, is done),
+// the bias warp rewrites Ka and arrives aug_full.
 template <int D>
 struct PP2Smem {
   using C = PP2Cfg<D>;
@@ -145,13 +188,15 @@ struct PP2Smem {
   uint8_t k[C::kKStages][C::kTileBytes];
   uint8_t v[C::kVStages][C::kTileBytes];
   uint8_t p[2][kTileRows * kTileRows * 2];
-  uint8_t kaug[C::kAugStages][kTileRows * 16];
+  uint8_t kaug[kTileRows * 16];
   uint8_t qaug[256];
   uint32_t meta[kMetaRing][kChunks];
   uint64_t q_full;
   uint64_t k_full[C::kKStages], k_empty[C::kKStages];
   uint64_t v_full[C::kVStages], v_empty[C::kVStages];
-  uint64_t aug_full[C::kAugStages], aug_empty[C::kAugStages];
+  uint64_t aug_full, aug_empty;
+  uint64_t flag_full[kMetaRing], flag_empty[kMetaRing];
+  uint32_t flag[kMetaRing];
   uint64_t meta_full[kMetaRing], meta_empty[kMetaRing];
   uint64_t s_full[2], s_free[2], p_full[2], o_done[2];
   uint32_t tmem_base;
@@ -164,7 +209,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
                        uint16_t* __restrict__ out, float* __restrict__ lse,
                        int32_t* __restrict__ skipped) {
   using C = PP2Cfg<D>;
-  constexpr int KST = C::kKStages, VST = C::kVStages, AST = C::kAugStages;
+  constexpr int KST = C::kKStages, VST = C::kVStages;
   constexpr uint32_t kO0 = 256;  // O_L at kO0 + L * D
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   auto& sm = *reinterpret_cast<PP2Smem<D>*>(smem_raw);
@@ -178,6 +223,9 @@ __global__ void __launch_bounds__(kPPThreads, 1)
   const int n_ent = info[unit * 2 + 0];
   const int T = (info[unit * 2 + 1] + kTileRows - 1) / kTileRows;  // 128-row KV tiles
   const int64_t q_row0 = static_cast<int64_t>(bhq) * p.n + static_cast<int64_t>(i) * p.b_q;
+#ifdef PSA_TRACE
+  const int tslot = trace_slot(unit);
+#endif
 
   if (threadIdx.x == 0) {
     if (smem_u32(smem_raw) & 1023u) __trap();
@@ -190,9 +238,11 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       mbar_init(&sm.v_full[s], 1);
       mbar_init(&sm.v_empty[s], 1);
     }
-    for (int s = 0; s < AST; ++s) {
-      mbar_init(&sm.aug_full[s], 1);
-      mbar_init(&sm.aug_empty[s], 1);
+    mbar_init(&sm.aug_full, 1);
+    mbar_init(&sm.aug_empty, 1);
+    for (int s = 0; s < kMetaRing; ++s) {
+      mbar_init(&sm.flag_full[s], 1);
+      mbar_init(&sm.flag_empty[s], 1);
     }
     for (int s = 0; s < kMetaRing; ++s) {
       mbar_init(&sm.meta_full[s], 1);
@@ -249,11 +299,25 @@ __global__ void __launch_bounds__(kPPThreads, 1)
           const TileSeg sg = pc.next(p, bhkv, lane);
           if (t >= KST) mbar_wait(&sm.k_empty[ks], ((t / KST) - 1) & 1);
           if (lane == 0) mbar_arrive_expect_tx(&sm.k_full[ks], static_cast<uint32_t>(sg.total) * D * 2);
+          if (lane == 0) PSA_STAMP(8, t);
           __syncwarp();
-          if (sg.fits)
-            for (int c = 0; c < D / 64; ++c)
-              tma_load_2d(&maps.k[sg.h - 1], &sm.k_full[ks],
-                          sm.k[ks] + c * kTileRows * 128 + sg.off * 128, c * 64, sg.row);
+          {  // one TMA box per lane: (segment lane / NH, 64-column chunk lane % NH); a thread's own
+             // TMA loads complete one after another (scripts/probes/tma_l2_probe.cu)
+            constexpr int NH = D / 64;
+            const int sl = lane / NH, c = lane % NH;
+            const int h = __shfl_sync(0xffffffffu, sg.h, sl);
+            const int off = __shfl_sync(0xffffffffu, sg.off, sl);
+            const int row = __shfl_sync(0xffffffffu, sg.row, sl);
+            if (sl < sg.nseg)
+              tma_load_2d(&maps.k[h - 1], &sm.k_full[ks], sm.k[ks] + c * kTileRows * 128 + off * 128,
+                          c * 64, row);
+          }
+#ifdef PSA_TRACE_KLAND
+          if (tslot >= 0) {  // landing time of K(t) as seen by its producer (trace builds only)
+            mbar_wait(&sm.k_full[ks], (t / KST) & 1);
+            if (lane == 0) PSA_STAMP(9, t);
+          }
+#endif
         }
       }
     } else if (warp == 3) {
@@ -267,10 +331,16 @@ __global__ void __launch_bounds__(kPPThreads, 1)
           if (t >= VST) mbar_wait(&sm.v_empty[vs], ((t / VST) - 1) & 1);
           if (lane == 0) mbar_arrive_expect_tx(&sm.v_full[vs], static_cast<uint32_t>(sg.total) * D * 2);
           __syncwarp();
-          if (sg.fits)
-            for (int c = 0; c < D / 64; ++c)
-              tma_load_2d(&maps.v[sg.h - 1], &sm.v_full[vs],
-                          sm.v[vs] + c * kTileRows * 128 + sg.off * 128, c * 64, sg.row);
+          {  // one TMA box per lane, as for K
+            constexpr int NH = D / 64;
+            const int sl = lane / NH, c = lane % NH;
+            const int h = __shfl_sync(0xffffffffu, sg.h, sl);
+            const int off = __shfl_sync(0xffffffffu, sg.off, sl);
+            const int row = __shfl_sync(0xffffffffu, sg.row, sl);
+            if (sl < sg.nseg)
+              tma_load_2d(&maps.v[h - 1], &sm.v_full[vs], sm.v[vs] + c * kTileRows * 128 + off * 128,
+                          c * 64, row);
+          }
         }
       }
     } else if (warp == 2) {
@@ -279,28 +349,30 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         const int64_t q_lo = static_cast<int64_t>(i) * p.b_q;
         PlanCursor pc;
         pc.init(csr + unit * p.n_k, n_ent, lane);
+        uint4 prev[4] = {};
+        int n_change = 0;
         for (int t = 0; t < T; ++t) {
-          const int as = t % AST;
           const TileSeg sg = pc.next(p, bhkv, lane);
-          if (t >= AST) mbar_wait(&sm.aug_empty[as], ((t / AST) - 1) & 1);  // S(t - AST) done
-          {  // lane owns keys 4 lane .. 4 lane + 3 (one segment: slots are >= 8 rows, aligned)
-            int g = 0;
-            for (int q = 1; q < sg.nseg; ++q)
-              if (__shfl_sync(0xffffffffu, sg.off, q) <= 4 * lane) g = q;
-            const int goff = __shfl_sync(0xffffffffu, sg.off, g);
-            const int gL = __shfl_sync(0xffffffffu, sg.L, g);
-            const int gh = __shfl_sync(0xffffffffu, sg.h, g);
-            const int r0 = 4 * lane - goff;
-            const bool in_tile = 4 * lane < sg.total;
-            const uint4 live = make_uint4(p.aug[gh - 1][0], p.aug[gh - 1][1], 0u, 0u);
-            const uint4 pad = make_uint4(kAugPad, 0u, 0u, 0u);
-            uint4* row = reinterpret_cast<uint4*>(sm.kaug[as]) + 4 * lane;
-#pragma unroll
-            for (int e = 0; e < 4; ++e) row[e] = in_tile && r0 + e < gL ? live : pad;
+          uint4 rows[4];
+          const bool change = aug_rows(sg, p, lane, t, rows, prev);
+          {  // tell the MMA warp whether S(t) needs new Ka rows
+            const int fs = t % kMetaRing;
+            if (t >= kMetaRing) mbar_wait(&sm.flag_empty[fs], ((t / kMetaRing) - 1) & 1);
+            if (lane == 0) {
+              sm.flag[fs] = change ? 1u : 0u;
+              mbar_arrive(&sm.flag_full[fs]);
+            }
           }
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&sm.aug_full[as]);
+          if (change) {  // rewrite Ka once the MMAs reading the previous rows are done
+            if (n_change > 0) mbar_wait(&sm.aug_empty, (n_change - 1) & 1);
+            uint4* dst = reinterpret_cast<uint4*>(sm.kaug) + 4 * lane;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) dst[e] = rows[e];
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.aug_full);
+            ++n_change;
+          }
           if (p.causal) {
             // per 8-key chunk: straddle flag, valid keys of the chunk (pad keys of a straddling
             // chunk are masked too, so a row with no visible key stays empty), first key position
@@ -327,14 +399,29 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         constexpr uint32_t idesc_o = umma_idesc_bf16(128, D, false, true);
         const uint64_t q_desc0 = umma_desc_sw128(smem_u32(sm.q), 16, 1024);
         const uint64_t qa_desc = umma_desc_noswz(smem_u32(sm.qaug), 128, 0);
+        const uint64_t ka_desc = umma_desc_noswz(smem_u32(sm.kaug), 0, 128);
+        int n_change = 0;
         auto issue_s = [&](int t) {
-          const int ks = t % KST, as = t % AST, L = t & 1;
+          const int ks = t % KST, L = t & 1;
+          if (lane == 0) PSA_STAMP(10, t);
+          const int fs = t % kMetaRing;
+          mbar_wait(&sm.flag_full[fs], (t / kMetaRing) & 1);
+          const bool change = sm.flag[fs] != 0u;
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.flag_empty[fs]);
           mbar_wait(&sm.k_full[ks], (t / KST) & 1);
+          if (lane == 0) PSA_STAMP(11, t);
           if (t >= 2) mbar_wait(&sm.s_free[L], ((t >> 1) - 1) & 1);  // lane read S(t-2)
-          mbar_wait(&sm.aug_full[as], (t / AST) & 1);
+          if (change) {
+            if (n_change > 0) {  // the previous Ka may be overwritten once everything so far is done
+              if (elect_one()) mma_commit(&sm.aug_empty);
+              __syncwarp();
+            }
+            mbar_wait(&sm.aug_full, n_change & 1);
+            ++n_change;
+          }
           tc_fence_after();
           const uint64_t k_desc0 = umma_desc_sw128(smem_u32(sm.k[ks]), 16, 1024);
-          const uint64_t ka_desc = umma_desc_noswz(smem_u32(sm.kaug[as]), 0, 128);
           if (elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < D / 16; ++kk) {
@@ -343,15 +430,17 @@ __global__ void __launch_bounds__(kPPThreads, 1)
                           kk > 0 ? 1u : 0u);
             }
             mma_bf16_ss(tmem + L * 128, qa_desc, ka_desc, idesc_s, 1u);  // + level bias
+            PSA_STAMP(6, t);
             mma_commit(&sm.k_empty[ks]);
-            mma_commit(&sm.aug_empty[as]);
             mma_commit(&sm.s_full[L]);
           }
           __syncwarp();
         };
         auto issue_pv = [&](int t) {
           const int vs = t % VST, L = t & 1;
+          if (lane == 0) PSA_STAMP(13, t);
           mbar_wait(&sm.v_full[vs], (t / VST) & 1);
+          if (lane == 0) PSA_STAMP(12, t);
           mbar_wait(&sm.p_full[L], (t >> 1) & 1);
           tc_fence_after();
           const uint64_t v_desc0 = umma_desc_sw128(smem_u32(sm.v[vs]), kTileRows * 128, 1024);
@@ -363,6 +452,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
               mma_bf16_ss(tmem + kO0 + L * D, p_desc0 + poff, v_desc0 + ((kk * 16 * 128) >> 4),
                           idesc_o, (t >= 2 || kk > 0) ? 1u : 0u);
             }
+            PSA_STAMP(7, t);
             mma_commit(&sm.v_empty[vs]);
             mma_commit(&sm.o_done[L]);
           }
@@ -389,15 +479,21 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     const int qpos = i * p.b_q + row;
     const float2 scale2 = make_float2(p.scale_log2, p.scale_log2);
     float m_run = -INFINITY, l_run = 0.f;
+#ifdef PSA_TRACE
+    const int tslot = (wq == 0 && lane == 0) ? trace_slot(unit) : -1;
+#endif
     for (int t = L; t < T; t += 2) {
       const int ms = t % kMetaRing;
+      PSA_STAMP(0, t);
       mbar_wait(&sm.s_full[L], (t >> 1) & 1);
+      PSA_STAMP(1, t);
       tc_fence_after();
       uint32_t s[4][32];
 #pragma unroll
       for (int c = 0; c < 4; ++c) tmem_ld32(t_s + c * 32, s[c]);
 #pragma unroll
       for (int c = 0; c < 4; ++c) tmem_ld_wait(s[c]);
+      PSA_STAMP(2, t);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.s_free[L]);  // S_L may take tile t+2 now
@@ -432,6 +528,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       mx[1] = fmax3(mx[1], y[126], y[127]);
       const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * p.scale_log2;
       const float m_new = fmaxf(m_run, mt);
+      PSA_STAMP(3, t);
       const bool resc = m_new > m_run + kRescaleThreshold;
       float alpha = 1.f;
       if (resc) {
@@ -459,6 +556,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       }
       const float2 ls = fadd2(ls0, ls1);
       l_run = l_run * alpha + (ls.x + ls.y);
+      PSA_STAMP(4, t);
       // PV(t-2) done: P_L is free and O_L is stable
       if (t >= 2) {
         mbar_wait(&sm.o_done[L], ((t >> 1) - 1) & 1);
@@ -491,6 +589,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.p_full[L]);
+      PSA_STAMP(5, t);
     }
 
     // ---------------------------------------------------------------- merge + epilogue
@@ -1533,6 +1632,11 @@ extern "C" int psa_attn_fwd_scatter(const void* q, const void* k, const void* v,
                          plan_info, causal, out, lse, skipped_rows, out_rows, s);
 }
 
+#ifdef PSA_TRACE
+extern "C" int psa_debug_pp2_trace(long long* host) {
+  return cudaMemcpyFromSymbol(host, psa::g_pp2_trace, sizeof(psa::g_pp2_trace)) == cudaSuccess ? 0 : -5;
+}
+#endif
 extern "C" int psa_attn_fwd(const void* q, const void* k, const void* v, const void* k_pyr,
                             const void* v_pyr, int64_t batch, int hq, int hkv, int64_t n, int d,
                             int b_q, int b_k, int levels, const uint16_t* plan_csr,
