@@ -51,11 +51,12 @@ struct MmaSmem {
   uint8_t b[128 * 64 * 2];
   uint8_t scratch[8][32 * 16 * 16];  // per-store-warp 8 KB
   uint64_t done;
+  uint64_t dummy[2];
   uint32_t tmem;
 };
 
 // MODE 0: SS; MODE 1: TS (A from TMEM). STORES: 8 warps stream 16-byte shared stores meanwhile.
-template <int MODE, bool STORES>
+template <int MODE, int STORES>
 __global__ void __launch_bounds__(384, 1) mma_kernel(long long* cyc, int iters) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   auto& sm = *reinterpret_cast<MmaSmem*>(smem_raw);
@@ -66,6 +67,8 @@ __global__ void __launch_bounds__(384, 1) mma_kernel(long long* cyc, int iters) 
   }
   if (threadIdx.x == 0) {
     mbar_init(&sm.done, 1);
+    mbar_init(&sm.dummy[0], 1 << 20);
+    mbar_init(&sm.dummy[1], 1 << 20);
     fence_barrier_init();
   }
   if (warp == 0) {
@@ -90,10 +93,14 @@ __global__ void __launch_bounds__(384, 1) mma_kernel(long long* cyc, int iters) 
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
           const uint32_t koff = (kk * 32) >> 4;
-          if (MODE == 0)
+          if (MODE == 0 || MODE == 2)
             mma_bf16_ss(tmem, ad + koff, bd + koff, idesc, 1u);
           else
             mma_bf16_ts(tmem, tmem + 256 + kk * 8, bd + koff, idesc, 1u);
+        }
+        if (MODE == 2 && (it % 2 == 1)) {  // 8 MMAs then 2 commits, like the attention kernel
+          mma_commit(&sm.dummy[0]);
+          mma_commit(&sm.dummy[1]);
         }
       }
       mma_commit(&sm.done);
@@ -105,7 +112,20 @@ __global__ void __launch_bounds__(384, 1) mma_kernel(long long* cyc, int iters) 
       cyc[blockIdx.x] = t1 - t0;
       stop = 1;
     }
-  } else if (STORES && warp >= 4) {
+  } else if (STORES == 2 && (warp == 5 || warp == 9 || warp == 6 || warp == 10)) {
+    // TMEM traffic of softmax warps on the MMA warp's sub-partition (warp 1 -> SMSP 1): LDTM x32
+    // of S and STTM x32 of P in a loop (lanes of this warp's TMEM quarter)
+    const uint32_t tl = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + 384;
+    uint32_t v[32];
+    for (int e = 0; e < 32; ++e) v[e] = e;
+    while (!stop) {
+      tmem_ld32(tl, v);
+      tmem_ld_wait(v);
+      for (int e = 0; e < 32; ++e) v[e] += 1;
+      tmem_st32(tl + 64, v);
+      tmem_st_wait();
+    }
+  } else if (STORES == 1 && warp >= 4) {
     uint4* dst = reinterpret_cast<uint4*>(sm.scratch[warp - 4]);
     uint4 v = make_uint4(threadIdx.x, 1, 2, 3);
     while (!stop) {
@@ -153,7 +173,7 @@ void run_mufu(const char* name, int warps_per_smsp) {
   cudaFree(cyc);
 }
 
-template <int MODE, bool STORES>
+template <int MODE, int STORES>
 void run_mma(const char* name) {
   const int iters = 4096;
   long long* cyc;
@@ -183,9 +203,11 @@ int main() {
   run_mufu<1>("f16x2", 2);
   run_mufu<2>("bf16x2", 1);
   run_mufu<2>("bf16x2", 2);
-  run_mma<0, false>("SS");
-  run_mma<1, false>("TS");
-  run_mma<0, true>("SS + 8 warps STS.128");
-  run_mma<1, true>("TS + 8 warps STS.128");
+  run_mma<0, 0>("SS");
+  run_mma<1, 0>("TS");
+  run_mma<2, 0>("SS + 2 commits / 8 MMAs");
+  run_mma<0, 1>("SS + 8 warps STS.128");
+  run_mma<0, 2>("SS + TMEM ld/st warps (SMSP1,2)");
+  run_mma<2, 2>("SS+commits + TMEM ld/st");
   return 0;
 }

@@ -37,6 +37,7 @@ assert lib.psa_debug_pp2_trace(buf.ctypes.data) == 0
 rows = plan.info[:, 1].cpu().numpy()
 os.makedirs("gpurun_out", exist_ok=True)
 np.savez("gpurun_out/pp2_trace2.npz", trace=buf, rows=np.array([rows[1234 + 3000 * s] for s in range(8)]))
+dump = os.environ.get("DUMP")
 names = ["wait->S ready", "S ready->LDTM done", "LDTM->max done", "max->exps done", "exps->P arrived"]
 for s in range(8):
     T = (int(rows[1234 + 3000 * s]) + 127) // 128
@@ -55,3 +56,11 @@ for s in range(8):
     print(f"   K TMA issue->landed {kland:.0f} | MMA cursor {cur:.0f} | K(t) TMA issue - S(t-2) ready {k_after:.0f}")
     print(f"cta {s}: T={T} lane period {period:.0f} cyc | " + " | ".join(f"{n} {v:.0f}" for n, v in zip(names, ph))
           + f" | S issue->ready {s_issue_to_ready:.0f} | P->PV issue {pv_issue_after_p:.0f}")
+
+if dump:
+    s = 2
+    t0 = buf[s, 5, 40]
+    print("t  Kloop  kempty  Kissue  TMAdone in_s  kfull  Sissd  Srdy  Pdone  in_pv  vfull  PVissd")
+    for t in range(40, 50):
+        e = buf[s, :, t] - t0
+        print(t, e[15], e[14], e[8], e[9], e[10], e[11], e[6], e[1], e[5], e[13], e[12], e[7])
