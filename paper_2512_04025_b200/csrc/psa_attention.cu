@@ -105,114 +105,57 @@ struct PlanCursor {
   }
 };
 
-// ====================================================================== two softmax lanes
-// The two softmax warpgroups are "lanes" that take ALTERNATE KV tiles of the unit (full 128-column
-// rows, one query row per thread), so each SM sub-partition always has a second softmax warp to
-// issue from while one waits. Each lane has its own S buffer in TMEM (a lane releases S right after
-// tcgen05.ld, and the tensor core computes its NEXT S(t+2) while its softmax of tile t runs) and
-// its own P buffer in TMEM (the A operand of the PV MMA, TS form: P never touches shared memory).
-// Both lanes accumulate into ONE O with a shared running max: lane t&1 takes the reference max
-// m(t-1) published by the other lane, raises it to its tile's max only when that exceeds it by
-// more than 2^8 (lazy rescaling; then it rescales O after PV(t-1) and before PV(t)), publishes m(t)
-// and forms P(t) relative to it. Each lane keeps its own row sum, rescaled to the final max in the
-// epilogue.
-// TMEM: S_0 | S_1 | P_0 | P_1 (bf16 pairs) | O (512 columns at D = 128).
-// SMEM at D=128: Q 32K + K 3 x 32K + V 2 x 32K; the epilogue's (l) exchange reuses Q's buffer.
+// ====================================================================== ping-pong lanes
+// The two softmax warpgroups are independent "lanes" that take ALTERNATE KV tiles of the unit,
+// each with full 128-column rows, its own running (max, sum) and its own O accumulator in TMEM;
+// the lanes merge once in the epilogue. While one lane runs its softmax, the tensor core
+// computes the other lane's S and PV. P goes to shared memory, so a lane releases S right after
+// tcgen05.ld and the tensor core computes the lane's NEXT S(t+2) while its softmax of tile t is
+// still running; PV reads P with a shared-memory descriptor (K-major, 128B swizzle).
+// TMEM: S0 | S1 | O0 | O1 (512 columns at D=128). SMEM at D=128: Q 32K + K 2x32K + V 2x32K +
+// P 2x32K; the lanes' final (max, sum) exchange reuses their P buffers.
 // Register split via setmaxnreg within the CTA pool of 384 x 168: producer/MMA warpgroup 64,
 // softmax warpgroups 216 (128*64 + 256*216 <= 384*168, else the increase never completes).
 constexpr int kPPThreads = 384;
-
-// Ka rows of a tile for the keys 4 lane .. 4 lane + 3 (one segment: slots are >= 8 rows, aligned)
-// and whether any row differs from the previous tile's (warp-uniform; tile 0 always "changes").
-PSA_DEV bool aug_rows(const TileSeg& sg, const AttnParams& p, int lane, int t, uint4 (&rows)[4],
-                      uint4 (&prev)[4]) {
-  int g = 0;
-  for (int q = 1; q < sg.nseg; ++q)
-    if (__shfl_sync(0xffffffffu, sg.off, q) <= 4 * lane) g = q;
-  const int goff = __shfl_sync(0xffffffffu, sg.off, g);
-  const int gL = __shfl_sync(0xffffffffu, sg.L, g);
-  const int gh = __shfl_sync(0xffffffffu, sg.h, g);
-  const int r0 = 4 * lane - goff;
-  const bool in_tile = 4 * lane < sg.total;
-  const uint4 live = make_uint4(p.aug[gh - 1][0], p.aug[gh - 1][1], 0u, 0u);
-  const uint4 pad = make_uint4(kAugPad, 0u, 0u, 0u);
-  bool diff = t == 0;
-#pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    rows[e] = in_tile && r0 + e < gL ? live : pad;
-    diff |= rows[e].x != prev[e].x || rows[e].y != prev[e].y;
-    prev[e] = rows[e];
-  }
-  return __any_sync(0xffffffffu, diff);
-}
-
-#ifdef PSA_TRACE
-// probe builds only (scripts/probes/pp2_trace2.py): clock64 stamps of 8 CTAs, 8 events x 256 tiles
-__device__ long long g_pp2_trace[8][16][256];
-PSA_DEV int trace_slot(int64_t unit) {
-  for (int s = 0; s < 8; ++s)
-    if (unit == 1234 + 3000 * s) return s;
-  return -1;
-}
-#define PSA_STAMP(ev, t) \
-  do { if (tslot >= 0 && (t) < 256) g_pp2_trace[tslot][ev][t] = clock64(); } while (0)
-#else
-#define PSA_STAMP(ev, t) do { } while (0)
-#endif
 
 template <uint32_t N>
 PSA_DEV void regs_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N)); }
 template <uint32_t N>
 PSA_DEV void regs_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N)); }
 
-
-// Warp roles: 0 K TMA producer (+ Q); 1 MMA issuer (one elected thread): S(t) = [Q|Qa][K|Ka]^T
-// into S_(t&1), then O += P_(t&1) V(t); 2 bias rows Ka, the MMA warp's Ka-change flags, causal
-// chunk metadata (+ TMEM allocation); 3 V TMA producer; 4-7 / 8-11 softmax lanes 0 / 1.
-// MMA issue order: S(0), S(1), then per t: S(t+2) (needs lane t&1 to have read S(t), K(t+2)),
-// PV(t) (needs P(t), V(t)).
 template <int D>
 struct PP2Cfg {
-  static constexpr int kKStages = 3;
-  static constexpr int kVStages = 2;
+  static constexpr int kKStages = D == 128 ? 2 : 3;
+  static constexpr int kVStages = D == 128 ? 2 : 3;
+  static constexpr int kAugStages = D == 128 ? 1 : 2;  // one 2 KB stage is all that fits at D=128
   static constexpr int kTileBytes = kTileRows * D * 2;
-  static constexpr uint32_t kS = 0, kP = 256, kO = 384;  // TMEM columns: S_L (128) | P_L (64) | O
 };
 
 // The level bias enters S through the tensor core: S = [Q | Qa] [K | Ka]^T with one extra K=16
 // step, Qa = (1, 1, 1, 0, ...) for every query row and Ka = (hi, mid, lo, 0, ...) of the key's
 // bias (h-1)/scale_log2 (= (h-1) ln 2 after the softmax scale, exactly h-1 in the log2 domain)
-// split into three bf16 terms (pad keys: -2^100). The softmax then works on raw S like dense
-// attention (no per-column bias loads or adds; pad keys need no masking).
+// split into three bf16 terms (pad keys: -2^100). The softmax then works on
+// raw S like dense attention (no per-column bias loads or adds; pad keys need no masking).
 // Ka: no-swizzle K-major, 16 B per key (its second 8-column core matrix aliases the first: LBO = 0,
 // matched by zeros in Qa's second core matrix); Qa: one core matrix broadcast to every row (SBO = 0).
-// Consecutive tiles of a level have identical Ka rows (same slots, same pads), so Ka is rewritten
-// only when a tile's rows differ from the previous tile's (a handful of times per unit): the bias
-// warp walks the plan, detects the changes and tells the MMA warp through a 4-slot flag ring; at a
-// change the MMA warp commits aug_empty (completes when every MMA issued so far, incl. the
-// previous S, is done), the bias warp rewrites Ka and arrives aug_full.
 template <int D>
 struct PP2Smem {
   using C = PP2Cfg<D>;
   uint8_t q[kTileRows * D * 2];
   uint8_t k[C::kKStages][C::kTileBytes];
   uint8_t v[C::kVStages][C::kTileBytes];
-  uint8_t kaug[kTileRows * 16];
+  uint8_t p[2][kTileRows * kTileRows * 2];
+  uint8_t kaug[C::kAugStages][kTileRows * 16];
   uint8_t qaug[256];
   uint32_t meta[kMetaRing][kChunks];
-  float mref[kTileRows];  // the shared running max m(t) of the last published tile (log2 units)
-  uint32_t flag[kMetaRing];
   uint64_t q_full;
   uint64_t k_full[C::kKStages], k_empty[C::kKStages];
   uint64_t v_full[C::kVStages], v_empty[C::kVStages];
-  uint64_t aug_full, aug_empty;
-  uint64_t flag_full[kMetaRing], flag_empty[kMetaRing];
+  uint64_t aug_full[C::kAugStages], aug_empty[C::kAugStages];
   uint64_t meta_full[kMetaRing], meta_empty[kMetaRing];
-  uint64_t s_full[2], s_free[2], p_full[2], o_done[2], m_full;
+  uint64_t s_full[2], s_free[2], p_full[2], o_done[2];
   uint32_t tmem_base;
 };
-
-static_assert(sizeof(PP2Smem<128>) <= 227 * 1024, "attention shared memory exceeds the sm_100 limit");
 
 template <int D>
 __global__ void __launch_bounds__(kPPThreads, 1)
@@ -221,7 +164,8 @@ __global__ void __launch_bounds__(kPPThreads, 1)
                        uint16_t* __restrict__ out, float* __restrict__ lse,
                        int32_t* __restrict__ skipped) {
   using C = PP2Cfg<D>;
-  constexpr int KST = C::kKStages, VST = C::kVStages;
+  constexpr int KST = C::kKStages, VST = C::kVStages, AST = C::kAugStages;
+  constexpr uint32_t kO0 = 256;  // O_L at kO0 + L * D
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   auto& sm = *reinterpret_cast<PP2Smem<D>*>(smem_raw);
 
@@ -234,9 +178,6 @@ __global__ void __launch_bounds__(kPPThreads, 1)
   const int n_ent = info[unit * 2 + 0];
   const int T = (info[unit * 2 + 1] + kTileRows - 1) / kTileRows;  // 128-row KV tiles
   const int64_t q_row0 = static_cast<int64_t>(bhq) * p.n + static_cast<int64_t>(i) * p.b_q;
-#ifdef PSA_TRACE
-  const int tslot = trace_slot(unit);
-#endif
 
   if (threadIdx.x == 0) {
     if (smem_u32(smem_raw) & 1023u) __trap();
@@ -249,11 +190,11 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       mbar_init(&sm.v_full[s], 1);
       mbar_init(&sm.v_empty[s], 1);
     }
-    mbar_init(&sm.aug_full, 1);
-    mbar_init(&sm.aug_empty, 1);
+    for (int s = 0; s < AST; ++s) {
+      mbar_init(&sm.aug_full[s], 1);
+      mbar_init(&sm.aug_empty[s], 1);
+    }
     for (int s = 0; s < kMetaRing; ++s) {
-      mbar_init(&sm.flag_full[s], 1);
-      mbar_init(&sm.flag_empty[s], 1);
       mbar_init(&sm.meta_full[s], 1);
       mbar_init(&sm.meta_empty[s], kTileRows);  // one lane (128 threads) consumes a tile
     }
@@ -263,7 +204,6 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       mbar_init(&sm.p_full[s], 4);
       mbar_init(&sm.o_done[s], 1);
     }
-    mbar_init(&sm.m_full, 4);  // the publishing lane's 4 warps
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -309,18 +249,11 @@ __global__ void __launch_bounds__(kPPThreads, 1)
           const TileSeg sg = pc.next(p, bhkv, lane);
           if (t >= KST) mbar_wait(&sm.k_empty[ks], ((t / KST) - 1) & 1);
           if (lane == 0) mbar_arrive_expect_tx(&sm.k_full[ks], static_cast<uint32_t>(sg.total) * D * 2);
-          if (lane == 0) PSA_STAMP(8, t);
           __syncwarp();
-          {  // one TMA box per lane: (segment lane / NH, 64-column chunk lane % NH)
-            constexpr int NH = D / 64;
-            const int sl = lane / NH, c = lane % NH;
-            const int h = __shfl_sync(0xffffffffu, sg.h, sl);
-            const int off = __shfl_sync(0xffffffffu, sg.off, sl);
-            const int row = __shfl_sync(0xffffffffu, sg.row, sl);
-            if (sl < sg.nseg)
-              tma_load_2d(&maps.k[h - 1], &sm.k_full[ks], sm.k[ks] + c * kTileRows * 128 + off * 128,
-                          c * 64, row);
-          }
+          if (sg.fits)
+            for (int c = 0; c < D / 64; ++c)
+              tma_load_2d(&maps.k[sg.h - 1], &sm.k_full[ks],
+                          sm.k[ks] + c * kTileRows * 128 + sg.off * 128, c * 64, sg.row);
         }
       }
     } else if (warp == 3) {
@@ -334,48 +267,40 @@ __global__ void __launch_bounds__(kPPThreads, 1)
           if (t >= VST) mbar_wait(&sm.v_empty[vs], ((t / VST) - 1) & 1);
           if (lane == 0) mbar_arrive_expect_tx(&sm.v_full[vs], static_cast<uint32_t>(sg.total) * D * 2);
           __syncwarp();
-          {
-            constexpr int NH = D / 64;
-            const int sl = lane / NH, c = lane % NH;
-            const int h = __shfl_sync(0xffffffffu, sg.h, sl);
-            const int off = __shfl_sync(0xffffffffu, sg.off, sl);
-            const int row = __shfl_sync(0xffffffffu, sg.row, sl);
-            if (sl < sg.nseg)
-              tma_load_2d(&maps.v[h - 1], &sm.v_full[vs], sm.v[vs] + c * kTileRows * 128 + off * 128,
-                          c * 64, row);
-          }
+          if (sg.fits)
+            for (int c = 0; c < D / 64; ++c)
+              tma_load_2d(&maps.v[sg.h - 1], &sm.v_full[vs],
+                          sm.v[vs] + c * kTileRows * 128 + sg.off * 128, c * 64, sg.row);
         }
       }
     } else if (warp == 2) {
-      // ============================================================ bias rows (Ka), flags, causal meta
+      // ============================================================ bias rows (Ka) + causal meta
       if (T > 0) {
         const int64_t q_lo = static_cast<int64_t>(i) * p.b_q;
         PlanCursor pc;
         pc.init(csr + unit * p.n_k, n_ent, lane);
-        uint4 prev[4] = {};
-        int n_change = 0;
         for (int t = 0; t < T; ++t) {
+          const int as = t % AST;
           const TileSeg sg = pc.next(p, bhkv, lane);
-          uint4 rows[4];
-          const bool change = aug_rows(sg, p, lane, t, rows, prev);
-          {  // tell the MMA warp whether S(t) needs new Ka rows
-            const int fs = t % kMetaRing;
-            if (t >= kMetaRing) mbar_wait(&sm.flag_empty[fs], ((t / kMetaRing) - 1) & 1);
-            if (lane == 0) {
-              sm.flag[fs] = change ? 1u : 0u;
-              mbar_arrive(&sm.flag_full[fs]);
-            }
-          }
-          if (change) {  // rewrite Ka once the MMAs reading the previous rows are done
-            if (n_change > 0) mbar_wait(&sm.aug_empty, (n_change - 1) & 1);
-            uint4* dst = reinterpret_cast<uint4*>(sm.kaug) + 4 * lane;
+          if (t >= AST) mbar_wait(&sm.aug_empty[as], ((t / AST) - 1) & 1);  // S(t - AST) done
+          {  // lane owns keys 4 lane .. 4 lane + 3 (one segment: slots are >= 8 rows, aligned)
+            int g = 0;
+            for (int q = 1; q < sg.nseg; ++q)
+              if (__shfl_sync(0xffffffffu, sg.off, q) <= 4 * lane) g = q;
+            const int goff = __shfl_sync(0xffffffffu, sg.off, g);
+            const int gL = __shfl_sync(0xffffffffu, sg.L, g);
+            const int gh = __shfl_sync(0xffffffffu, sg.h, g);
+            const int r0 = 4 * lane - goff;
+            const bool in_tile = 4 * lane < sg.total;
+            const uint4 live = make_uint4(p.aug[gh - 1][0], p.aug[gh - 1][1], 0u, 0u);
+            const uint4 pad = make_uint4(kAugPad, 0u, 0u, 0u);
+            uint4* row = reinterpret_cast<uint4*>(sm.kaug[as]) + 4 * lane;
 #pragma unroll
-            for (int e = 0; e < 4; ++e) dst[e] = rows[e];
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.aug_full);
-            ++n_change;
+            for (int e = 0; e < 4; ++e) row[e] = in_tile && r0 + e < gL ? live : pad;
           }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.aug_full[as]);
           if (p.causal) {
             // per 8-key chunk: straddle flag, valid keys of the chunk (pad keys of a straddling
             // chunk are masked too, so a row with no visible key stays empty), first key position
@@ -402,57 +327,42 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         constexpr uint32_t idesc_o = umma_idesc_bf16(128, D, false, true);
         const uint64_t q_desc0 = umma_desc_sw128(smem_u32(sm.q), 16, 1024);
         const uint64_t qa_desc = umma_desc_noswz(smem_u32(sm.qaug), 128, 0);
-        const uint64_t ka_desc = umma_desc_noswz(smem_u32(sm.kaug), 0, 128);
-        int n_change = 0;
         auto issue_s = [&](int t) {
-          const int ks = t % KST, L = t & 1;
-          if (lane == 0) PSA_STAMP(10, t);
-          const int fs = t % kMetaRing;
-          mbar_wait(&sm.flag_full[fs], (t / kMetaRing) & 1);
-          const bool change = sm.flag[fs] != 0u;
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&sm.flag_empty[fs]);
+          const int ks = t % KST, as = t % AST, L = t & 1;
           mbar_wait(&sm.k_full[ks], (t / KST) & 1);
-          if (lane == 0) PSA_STAMP(11, t);
-          if (t >= 2) mbar_wait(&sm.s_free[L], ((t >> 1) - 1) & 1);  // lane L has read S(t-2)
-          if (change) {
-            if (n_change > 0) {  // the previous Ka may be overwritten once everything so far is done
-              if (elect_one()) mma_commit(&sm.aug_empty);
-              __syncwarp();
-            }
-            mbar_wait(&sm.aug_full, n_change & 1);
-            ++n_change;
-          }
+          if (t >= 2) mbar_wait(&sm.s_free[L], ((t >> 1) - 1) & 1);  // lane read S(t-2)
+          mbar_wait(&sm.aug_full[as], (t / AST) & 1);
           tc_fence_after();
           const uint64_t k_desc0 = umma_desc_sw128(smem_u32(sm.k[ks]), 16, 1024);
+          const uint64_t ka_desc = umma_desc_noswz(smem_u32(sm.kaug[as]), 0, 128);
           if (elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < D / 16; ++kk) {
               const uint32_t koff = ((kk >> 2) * kTileRows * 128 + (kk & 3) * 32) >> 4;
-              mma_bf16_ss(tmem + C::kS + L * 128, q_desc0 + koff, k_desc0 + koff, idesc_s,
+              mma_bf16_ss(tmem + L * 128, q_desc0 + koff, k_desc0 + koff, idesc_s,
                           kk > 0 ? 1u : 0u);
             }
-            mma_bf16_ss(tmem + C::kS + L * 128, qa_desc, ka_desc, idesc_s, 1u);  // + level bias
-            PSA_STAMP(6, t);
+            mma_bf16_ss(tmem + L * 128, qa_desc, ka_desc, idesc_s, 1u);  // + level bias
             mma_commit(&sm.k_empty[ks]);
+            mma_commit(&sm.aug_empty[as]);
             mma_commit(&sm.s_full[L]);
           }
           __syncwarp();
         };
         auto issue_pv = [&](int t) {
           const int vs = t % VST, L = t & 1;
-          if (lane == 0) PSA_STAMP(13, t);
           mbar_wait(&sm.v_full[vs], (t / VST) & 1);
-          if (lane == 0) PSA_STAMP(12, t);
           mbar_wait(&sm.p_full[L], (t >> 1) & 1);
           tc_fence_after();
           const uint64_t v_desc0 = umma_desc_sw128(smem_u32(sm.v[vs]), kTileRows * 128, 1024);
+          const uint64_t p_desc0 = umma_desc_sw128(smem_u32(sm.p[L]), 16, 1024);
           if (elect_one()) {
 #pragma unroll
-            for (int kk = 0; kk < kTileRows / 16; ++kk)  // O += P_L V: P from TMEM (TS form)
-              mma_bf16_ts(tmem + C::kO, tmem + C::kP + L * 64 + kk * 8,
-                          v_desc0 + ((kk * 16 * 128) >> 4), idesc_o, (t > 0 || kk > 0) ? 1u : 0u);
-            PSA_STAMP(7, t);
+            for (int kk = 0; kk < kTileRows / 16; ++kk) {
+              const uint32_t poff = ((kk >> 2) * kTileRows * 128 + (kk & 3) * 32) >> 4;
+              mma_bf16_ss(tmem + kO0 + L * D, p_desc0 + poff, v_desc0 + ((kk * 16 * 128) >> 4),
+                          idesc_o, (t >= 2 || kk > 0) ? 1u : 0u);
+            }
             mma_commit(&sm.v_empty[vs]);
             mma_commit(&sm.o_done[L]);
           }
@@ -475,26 +385,19 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     const int wq = warp & 3;
     const int row = wq * 32 + lane;
     const uint32_t t_lane = tmem + (static_cast<uint32_t>(wq * 32) << 16);
-    const uint32_t t_s = t_lane + C::kS + L * 128;
-    const uint32_t t_o = t_lane + C::kO;
+    const uint32_t t_s = t_lane + L * 128;
     const int qpos = i * p.b_q + row;
     const float2 scale2 = make_float2(p.scale_log2, p.scale_log2);
-    float m_used = -INFINITY, l_run = 0.f;  // this lane's row sum is relative to m_used
-#ifdef PSA_TRACE
-    const int tslot = (wq == 0 && lane == 0) ? trace_slot(unit) : -1;
-#endif
+    float m_run = -INFINITY, l_run = 0.f;
     for (int t = L; t < T; t += 2) {
       const int ms = t % kMetaRing;
-      PSA_STAMP(0, t);
       mbar_wait(&sm.s_full[L], (t >> 1) & 1);
-      PSA_STAMP(1, t);
       tc_fence_after();
       uint32_t s[4][32];
 #pragma unroll
       for (int c = 0; c < 4; ++c) tmem_ld32(t_s + c * 32, s[c]);
 #pragma unroll
       for (int c = 0; c < 4; ++c) tmem_ld_wait(s[c]);
-      PSA_STAMP(2, t);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.s_free[L]);  // S_L may take tile t+2 now
@@ -527,25 +430,15 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       }
       mx[0] = fmax3(mx[0], y[124], y[125]);
       mx[1] = fmax3(mx[1], y[126], y[127]);
-      float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * p.scale_log2;
-      if (mt < -1e28f) mt = -INFINITY;  // only pad keys (S ~ -2^100): the row has no key in the tile
-      // shared reference max: m(t-1) from the other lane, raised lazily to this tile's max
-      float m_prev = -INFINITY;
-      if (t > 0) {
-        mbar_wait(&sm.m_full, (t - 1) & 1);
-        m_prev = sm.mref[row];
+      const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * p.scale_log2;
+      const float m_new = fmaxf(m_run, mt);
+      const bool resc = m_new > m_run + kRescaleThreshold;
+      float alpha = 1.f;
+      if (resc) {
+        alpha = ex2_approx(m_run - m_new);
+        m_run = m_new;
       }
-      const bool raise = mt > m_prev + kRescaleThreshold;
-      const float m_t = raise ? mt : m_prev;
-      sm.mref[row] = m_t;
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.m_full);
-      PSA_STAMP(3, t);
-      if (m_t != m_used) {  // this lane's row sum follows the reference
-        l_run = m_used == -INFINITY ? 0.f : l_run * ex2_approx(m_used - m_t);
-        m_used = m_t;
-      }
-      const float m_use = (m_t == -INFINITY) ? 0.f : m_t;
+      const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
       const float2 negm = make_float2(-m_use, -m_use);
       float2 ls0 = make_float2(0.f, 0.f), ls1 = make_float2(0.f, 0.f);
       uint32_t pk[64];
@@ -553,6 +446,8 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       for (int e = 0; e < 128; e += 4) {
         float2 a = ffma2(make_float2(y[e], y[e + 1]), scale2, negm);
         float2 c = ffma2(make_float2(y[e + 2], y[e + 3]), scale2, negm);
+        // every exp on MUFU: an FMA-pipe polynomial for the last 16/32/48/64 columns measured
+        // 26.7/26.5/27.6/28.2 ms against 25.9 ms at cfg3 (the lanes are issue-bound, not MUFU-bound)
         a.x = ex2_approx(a.x);
         a.y = ex2_approx(a.y);
         c.x = ex2_approx(c.x);
@@ -563,63 +458,64 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         pk[e / 2 + 1] = pack_bf16x2(c.x, c.y);
       }
       const float2 ls = fadd2(ls0, ls1);
-      l_run += ls.x + ls.y;
-      PSA_STAMP(4, t);
-      // O must follow a raised reference before PV(t): rescale it once PV(t-1) is done
-      if (t > 0 && __any_sync(0xffffffffu, raise)) {
-        mbar_wait(&sm.o_done[L ^ 1], ((t - 1) >> 1) & 1);
-        tc_fence_after();
-        const float alpha = m_prev == -INFINITY ? 0.f : ex2_approx(m_prev - m_t);
-        if (__any_sync(0xffffffffu, raise && alpha != 1.f)) {
-#pragma unroll
-          for (int c4 = 0; c4 < D / 32; ++c4) {
-            uint32_t o[32];
-            tmem_ld32(t_o + c4 * 32, o);
-            tmem_ld_wait(o);
-#pragma unroll
-            for (int e = 0; e < 32; ++e)
-              o[e] = __float_as_uint(raise ? __uint_as_float(o[e]) * alpha : __uint_as_float(o[e]));
-            tmem_st32(t_o + c4 * 32, o);
-          }
-        }
-      }
-      // P_L is free once PV(t-2) has read it
+      l_run = l_run * alpha + (ls.x + ls.y);
+      // PV(t-2) done: P_L is free and O_L is stable
       if (t >= 2) {
         mbar_wait(&sm.o_done[L], ((t >> 1) - 1) & 1);
         tc_fence_after();
       }
-      {  // P (bf16 pairs, key 2c / 2c+1 in column c) -> the lane's TMEM P columns
-        uint32_t (&p0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&pk[0]);
-        uint32_t (&p1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&pk[32]);
-        tmem_st32(t_lane + C::kP + L * 64, p0);
-        tmem_st32(t_lane + C::kP + L * 64 + 32, p1);
+      if (t >= 2 && __any_sync(0xffffffffu, resc)) {
+#pragma unroll
+        for (int c4 = 0; c4 < D / 32; ++c4) {
+          uint32_t o[32];
+          tmem_ld32(t_lane + kO0 + L * D + c4 * 32, o);
+          tmem_ld_wait(o);
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+          tmem_st32(t_lane + kO0 + L * D + c4 * 32, o);
+        }
       }
-      tmem_st_wait();  // O rescale + P stores
+      {  // P (bf16) -> shared memory, UMMA K-major 128B-swizzled: [key half][row][128 B]
+        uint8_t* prow = sm.p[L] + row * 128;
+        const int sw = row & 7;
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int ch = 0; ch < 8; ++ch)
+            *reinterpret_cast<uint4*>(prow + c * kTileRows * 128 + ((ch ^ sw) << 4)) =
+                make_uint4(pk[c * 32 + ch * 4], pk[c * 32 + ch * 4 + 1], pk[c * 32 + ch * 4 + 2],
+                           pk[c * 32 + ch * 4 + 3]);
+      }
+      tmem_st_wait();  // O rescale stores
+      fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.p_full[L]);
-      PSA_STAMP(5, t);
     }
 
     // ---------------------------------------------------------------- merge + epilogue
     const int cnt0 = (T + 1) >> 1, cnt1 = T >> 1;  // tiles of lane 0 / lane 1
-    float m_fin = -INFINITY;
-    if (T > 0) {  // the reference max of the last tile
-      mbar_wait(&sm.m_full, (T - 1) & 1);
-      m_fin = sm.mref[row];
-    }
-    const float l_me = (m_used == -INFINITY || m_fin == -INFINITY) ? 0.f : l_run * ex2_approx(m_used - m_fin);
-    // every MMA has completed once both lanes' last PVs have (in-order pipe): Q's buffer is free
+    const int cnt_me = L == 0 ? cnt0 : cnt1;
+    if (cnt_me > 0) mbar_wait(&sm.o_done[L], (cnt_me - 1) & 1);  // P_L no longer read
+    float* red = reinterpret_cast<float*>(sm.p[L]);
+    red[row] = m_run;
+    red[kTileRows + row] = l_run;
+    named_bar_sync(1, 2 * kTileRows);
+    const float* red0 = reinterpret_cast<const float*>(sm.p[0]);
+    const float* red1 = reinterpret_cast<const float*>(sm.p[1]);
+    const float m0 = red0[row], m1 = red1[row];
+    const float l0 = red0[kTileRows + row], l1 = red1[kTileRows + row];
+    const float m = fmaxf(m0, m1);
+    const float a0 = (cnt0 > 0 && m0 != -INFINITY) ? ex2_approx(m0 - m) : 0.f;
+    const float a1 = (cnt1 > 0 && m1 != -INFINITY) ? ex2_approx(m1 - m) : 0.f;
+    const float l_tot = l0 * a0 + l1 * a1;
     if (cnt0 > 0) mbar_wait(&sm.o_done[0], (cnt0 - 1) & 1);
     if (cnt1 > 0) mbar_wait(&sm.o_done[1], (cnt1 - 1) & 1);
     tc_fence_after();
-    float* red = reinterpret_cast<float*>(sm.q);
-    red[L * kTileRows + row] = l_me;
-    named_bar_sync(1, 2 * kTileRows);
-    const float l_tot = red[row] + red[kTileRows + row];
     const bool valid = row < p.b_q;
     const bool alive = l_tot > 0.f;
     const float inv = alive ? 1.f / l_tot : 0.f;
+    const float w0 = a0 * inv, w1 = a1 * inv;
     constexpr int OC = D / 2;  // output columns per lane
     // unpermute (pipeline.py:312-313) fused into the store: row i of the head -> out_rows[i]
     const int64_t o_row = p.out_rows == nullptr || !valid
@@ -628,16 +524,30 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     uint16_t* orow = out + o_row * D + L * OC;
 #pragma unroll
     for (int c4 = 0; c4 < OC / 32; ++c4) {
-      uint32_t o[32];
-      if (T > 0) {
-        tmem_ld32(t_o + L * OC + c4 * 32, o);
-        tmem_ld_wait(o);
+      uint32_t o0[32], o1[32];
+      const uint32_t col = L * OC + c4 * 32;
+      if (cnt0 > 0) {
+        tmem_ld32(t_lane + kO0 + col, o0);
+        tmem_ld_wait(o0);
+      }
+      if (cnt1 > 0) {
+        tmem_ld32(t_lane + kO0 + D + col, o1);
+        tmem_ld_wait(o1);
       }
       uint32_t pkd[16];
 #pragma unroll
-      for (int e = 0; e < 16; ++e)
-        pkd[e] = T > 0 ? pack_bf16x2(__uint_as_float(o[2 * e]) * inv, __uint_as_float(o[2 * e + 1]) * inv)
-                       : 0u;
+      for (int e = 0; e < 16; ++e) {
+        float v0 = 0.f, v1 = 0.f;
+        if (cnt0 > 0) {
+          v0 = __uint_as_float(o0[2 * e]) * w0;
+          v1 = __uint_as_float(o0[2 * e + 1]) * w0;
+        }
+        if (cnt1 > 0) {
+          v0 = fmaf(__uint_as_float(o1[2 * e]), w1, v0);
+          v1 = fmaf(__uint_as_float(o1[2 * e + 1]), w1, v1);
+        }
+        pkd[e] = pack_bf16x2(v0, v1);
+      }
       if (valid) {
 #pragma unroll
         for (int v4 = 0; v4 < 4; ++v4)
@@ -646,7 +556,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       }
     }
     if (L == 0) {
-      if (valid) lse[o_row] = alive ? (m_fin + log2f(l_tot)) * 0.69314718055994530942f : -INFINITY;
+      if (valid) lse[o_row] = alive ? (m + log2f(l_tot)) * 0.69314718055994530942f : -INFINITY;
       const unsigned dead = __ballot_sync(0xffffffffu, valid && !alive);
       if (lane == 0 && dead) atomicAdd(skipped, __popc(dead));
     }
@@ -1623,11 +1533,6 @@ extern "C" int psa_attn_fwd_scatter(const void* q, const void* k, const void* v,
                          plan_info, causal, out, lse, skipped_rows, out_rows, s);
 }
 
-#ifdef PSA_TRACE
-extern "C" int psa_debug_pp2_trace(long long* host) {
-  return cudaMemcpyFromSymbol(host, psa::g_pp2_trace, sizeof(psa::g_pp2_trace)) == cudaSuccess ? 0 : -5;
-}
-#endif
 extern "C" int psa_attn_fwd(const void* q, const void* k, const void* v, const void* k_pyr,
                             const void* v_pyr, int64_t batch, int hq, int hkv, int64_t n, int d,
                             int b_q, int b_k, int levels, const uint16_t* plan_csr,
