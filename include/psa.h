@@ -195,6 +195,45 @@ int psa_attn_bwd(const void* q, const void* k, const void* v, const void* k_pyr,
 int psa_gather_rows(const void* src, int64_t bh, int64_t n, int row_bytes, const int64_t* index,
                     void* dst, void* stream);
 
+/*
+ * Query-block work units (a rank owns (batch, head, query-block set); the
+ * reference's query blocks are independent given K/V, pkg/src/pyrattn/attention.py:187 and
+ * importance.py:52-132 / mask.py:128-151 row by row).  Each *_rows entry point runs its
+ * counterpart above on the n_qsel query blocks listed in qblk (DEVICE int32 [n_qsel], any order,
+ * the same list for every head of the call); the per-block outputs are compact:
+ *   psa_importance_sampled_rows:    q_rows holds the n_qsel * s_q sample rows of the listed
+ *                                   blocks (block-major, the reference table's rows of those
+ *                                   blocks); scores fp64 [batch*hq, n_qsel, n_k].  (The row list
+ *                                   is the table itself, so no qblk is needed.)
+ *   psa_importance_antidiagonal_rows: scores fp64 [batch*hq, n_qsel, n_k]; workspace
+ *                                   psa_antidiag_workspace_bytes_rows(..., n_qsel) bytes.
+ *   psa_assign_levels_rows:         scores / level map / plan rows are the listed blocks (n_q =
+ *                                   n_qsel); qblk gives the causal pre-pass the true positions.
+ *   psa_attn_fwd_rows:              plan units = batch*hq*n_qsel; out bf16 [batch, hq,
+ *                                   n_qsel*b_q, d], lse fp32 [batch, hq, n_qsel*b_q] (compact).
+ * Results are bit-identical to the same rows of the full-head call.
+ */
+int psa_importance_sampled_rows(const void* q, const void* k, int64_t batch, int hq, int hkv,
+                                int64_t n, int d, int b_q, int b_k, const int32_t* q_rows,
+                                const int32_t* k_rows, int s_q, int s_k, int reducer, int flags,
+                                int n_qsel, double* scores, void* workspace, void* stream);
+size_t psa_antidiag_workspace_bytes_rows(int64_t bhq, int64_t bkv, int64_t n, int b_q, int b_k,
+                                         int stride, int n_qsel);
+int psa_importance_antidiagonal_rows(const void* q, const void* k, int64_t batch, int hq, int hkv,
+                                     int64_t n, int d, int b_q, int b_k, int stride, int flags,
+                                     const int32_t* qblk, int n_qsel, double* scores,
+                                     void* workspace, void* stream);
+int psa_assign_levels_rows(const double* scores, int64_t batch, int hq, int hkv, int n_q, int n_k,
+                           int mode, const double* taus, const int32_t* counts, int n_cuts,
+                           const int8_t* caps, int causal, int b_q, int b_k, int levels,
+                           const int32_t* qblk, int8_t* level_map, uint16_t* plan_csr,
+                           int32_t* plan_info, unsigned long long* level_counts, void* stream);
+int psa_attn_fwd_rows(const void* q, const void* k, const void* v, const void* k_pyr,
+                      const void* v_pyr, int64_t batch, int hq, int hkv, int64_t n, int d,
+                      int b_q, int b_k, int levels, const uint16_t* plan_csr,
+                      const int32_t* plan_info, int causal, const int32_t* qblk, int n_qsel,
+                      void* out, float* lse, int32_t* skipped_rows, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

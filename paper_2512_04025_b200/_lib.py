@@ -58,6 +58,21 @@ _SIGNATURES = {
     "psa_pyramid_build_gather": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int, c_int, c_int,
                                          c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                          c_void_p, c_void_p]),
+    "psa_importance_sampled_rows": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int, c_int64,
+                                            c_int, c_int, c_int, c_void_p, c_void_p, c_int, c_int,
+                                            c_int, c_int, c_int, c_void_p, c_void_p, c_void_p]),
+    "psa_antidiag_workspace_bytes_rows": (c_size_t, [c_int64, c_int64, c_int64, c_int, c_int, c_int,
+                                                     c_int]),
+    "psa_importance_antidiagonal_rows": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int,
+                                                 c_int64, c_int, c_int, c_int, c_int, c_int,
+                                                 c_void_p, c_int, c_void_p, c_void_p, c_void_p]),
+    "psa_assign_levels_rows": (c_int, [c_void_p, c_int64, c_int, c_int, c_int, c_int, c_int,
+                                       c_void_p, c_void_p, c_int, c_void_p, c_int, c_int, c_int,
+                                       c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                       c_void_p]),
+    "psa_attn_fwd_rows": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int,
+                                  c_int, c_int64, c_int, c_int, c_int, c_int, c_void_p, c_void_p,
+                                  c_int, c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
 }
 
 EXPORTED = tuple(_SIGNATURES)

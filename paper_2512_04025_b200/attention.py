@@ -44,9 +44,12 @@ def level_bias(level: int, max_level: int | None = None) -> float:
 
 def attention_forward(q4: torch.Tensor, pyr: PyramidKV, plan: MaskPlan, causal: bool,
                       out: torch.Tensor | None = None, lse: torch.Tensor | None = None,
-                      skipped: torch.Tensor | None = None, out_rows: torch.Tensor | None = None):
+                      skipped: torch.Tensor | None = None, out_rows: torch.Tensor | None = None,
+                      qblocks: torch.Tensor | None = None):
     """Launch psa_attn_fwd on device tensors; returns (out, lse, skipped-counter). ``out_rows``
-    (device int64 [n]): store O/lse row i of every head at row out_rows[i] (fused unpermute)."""
+    (device int64 [n]): store O/lse row i of every head at row out_rows[i] (fused unpermute).
+    ``qblocks`` (device int32): only these query blocks (the plan's rows); O/lse are then
+    compact, [B, Hq, len(qblocks) * b_q, ...]."""
     lay = pyr.layout
     B, Hq, n, d = q4.shape
     Hkv = pyr.k_raw.shape[1]
@@ -54,6 +57,22 @@ def attention_forward(q4: torch.Tensor, pyr: PyramidKV, plan: MaskPlan, causal: 
         raise ValidationError(f"Q heads {Hq} / batch {B} incompatible with K/V "
                               f"{tuple(pyr.k_raw.shape)}")
     dev = q4.device
+    if qblocks is not None:
+        if out_rows is not None:
+            raise ValidationError("the row scatter and query-block subsets are exclusive")
+        rows = qblocks.numel() * lay.q_block
+        out = torch.empty(B, Hq, rows, d, dtype=q4.dtype, device=dev) if out is None else out
+        lse = torch.empty(B, Hq, rows, dtype=torch.float32, device=dev) if lse is None else lse
+        if skipped is None:
+            skipped = torch.zeros(1, dtype=torch.int32, device=dev)
+        rc = _lib.load().psa_attn_fwd_rows(
+            q4.data_ptr(), pyr.k_raw.data_ptr(), pyr.v_raw.data_ptr(), _lib.ptr(pyr.k_pyr),
+            _lib.ptr(pyr.v_pyr), B, Hq, Hkv, n, d, lay.q_block, lay.k_block, lay.levels,
+            plan.csr.data_ptr(), plan.info.data_ptr(), int(causal), qblocks.data_ptr(),
+            qblocks.numel(), out.data_ptr(), lse.data_ptr(), skipped.data_ptr(),
+            stream_handle(dev))
+        _lib.check(rc, "psa_attn_fwd")
+        return out, lse, skipped
     out = torch.empty_like(q4) if out is None else out
     lse = torch.empty(B, Hq, n, dtype=torch.float32, device=dev) if lse is None else lse
     if skipped is None:

@@ -25,6 +25,7 @@ namespace psa {
 struct AssignParams {
   LevelRule rule;
   int n_q, n_k, hq, hkv, b_q, b_k, levels, causal, n_pad;
+  const int32_t* qblk;  // optional: score row i is query block qblk[i] of the head (work units)
 };
 
 // Bits [lo, lo + cnt) (cnt <= 53) of a 256-bit little-endian limb array; bits below 0 read 0.
@@ -299,7 +300,8 @@ __global__ void __launch_bounds__(128) assign_levels_kernel(
 
   const int b = static_cast<int>(bhq / p.hq), h = static_cast<int>(bhq % p.hq);
   const int64_t bhkv = static_cast<int64_t>(b) * p.hkv + h / (p.hq / p.hkv);
-  const int64_t q_lo = static_cast<int64_t>(i) * p.b_q, q_hi = q_lo + p.b_q - 1;
+  const int iq = p.qblk != nullptr ? p.qblk[i] : i;
+  const int64_t q_lo = static_cast<int64_t>(iq) * p.b_q, q_hi = q_lo + p.b_q - 1;
   for (int j = threadIdx.x; j < p.n_k; j += blockDim.x) {
     int L = lvl[j];
     if (caps) L = min(L, static_cast<int>(caps[bhkv * p.n_k + j]));
@@ -350,12 +352,34 @@ __global__ void __launch_bounds__(128) mask_to_plan_kernel(
 
 using namespace psa;
 
+extern "C" int psa_assign_levels_rows(const double* scores, int64_t batch, int hq, int hkv,
+                                      int n_q, int n_k, int mode, const double* taus,
+                                      const int32_t* counts, int n_cuts, const int8_t* caps,
+                                      int causal, int b_q, int b_k, int levels,
+                                      const int32_t* qblk, int8_t* level_map, uint16_t* plan_csr,
+                                      int32_t* plan_info, unsigned long long* level_counts,
+                                      void* stream);
+
 extern "C" int psa_assign_levels(const double* scores, int64_t batch, int hq, int hkv, int n_q,
                                  int n_k, int mode, const double* taus, const int32_t* counts,
                                  int n_cuts, const int8_t* caps, int causal, int b_q, int b_k,
                                  int levels, int8_t* level_map, uint16_t* plan_csr,
                                  int32_t* plan_info, unsigned long long* level_counts,
                                  void* stream) {
+  return psa_assign_levels_rows(scores, batch, hq, hkv, n_q, n_k, mode, taus, counts, n_cuts, caps,
+                                causal, b_q, b_k, levels, nullptr, level_map, plan_csr, plan_info,
+                                level_counts, stream);
+}
+
+// qblk (optional, device int32 [n_q]): score row i of every head is query block qblk[i] of the
+// head, for the causal pre-pass (the q-block work units of the multi-GPU partition).
+extern "C" int psa_assign_levels_rows(const double* scores, int64_t batch, int hq, int hkv,
+                                      int n_q, int n_k, int mode, const double* taus,
+                                      const int32_t* counts, int n_cuts, const int8_t* caps,
+                                      int causal, int b_q, int b_k, int levels,
+                                      const int32_t* qblk, int8_t* level_map, uint16_t* plan_csr,
+                                      int32_t* plan_info, unsigned long long* level_counts,
+                                      void* stream) {
   PSA_CHECK_ARG(scores && level_map && plan_csr && plan_info, "null pointer argument");
   PSA_CHECK_ARG(mode == 0 || mode == 1, "mode must be 0 (threshold) or 1 (quantile)");
   PSA_CHECK_ARG(n_cuts >= 1 && n_cuts <= kMaxCuts, "need 1..16 thresholds/cutpoints");
@@ -384,6 +408,7 @@ extern "C" int psa_assign_levels(const double* scores, int64_t batch, int hq, in
   p.b_k = b_k;
   p.levels = levels;
   p.causal = causal;
+  p.qblk = qblk;
   static const int kIpt[] = {1, 2, 3, 4, 5, 6, 8, 10, 12, 16, 20, 24, 32};
   int ipt = 32;
   for (int v : kIpt)

@@ -44,6 +44,10 @@ struct AttnParams {
   int hq, hkv, b_q, b_k, levels, n_q, n_k, causal;
   float scale_log2;
   const int64_t* out_rows;  // optional scatter: O/lse row i of a head goes to row out_rows[i]
+  // optional q-block work units: unit u of head bhq is query block qblk[u % n_qs]; O/lse rows are
+  // then compact, [bhq, n_qs * b_q) (NULL: n_qs = n_q, every block, rows in place)
+  const int32_t* qblk;
+  int n_qs;
   // forward: the level bias (h-1)*ln2 of attention.py:39-44 in raw logit units, (h-1)/scale_log2,
   // as three bf16 terms
   // hi | mid << 16, lo, i.e. the first 8 bytes of a key's augmentation row (see kAugPad)
@@ -171,8 +175,9 @@ __global__ void __launch_bounds__(kPPThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t unit = blockIdx.x;
-  const int bhq = static_cast<int>(unit / p.n_q);
-  const int i = static_cast<int>(unit % p.n_q);
+  const int bhq = static_cast<int>(unit / p.n_qs);
+  const int il = static_cast<int>(unit % p.n_qs);
+  const int i = p.qblk != nullptr ? p.qblk[il] : il;
   const int b = bhq / p.hq, hh = bhq % p.hq;
   const int64_t bhkv = static_cast<int64_t>(b) * p.hkv + hh / (p.hq / p.hkv);
   const int n_ent = info[unit * 2 + 0];
@@ -518,9 +523,11 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     const float w0 = a0 * inv, w1 = a1 * inv;
     constexpr int OC = D / 2;  // output columns per lane
     // unpermute (pipeline.py:312-313) fused into the store: row i of the head -> out_rows[i]
-    const int64_t o_row = p.out_rows == nullptr || !valid
-                              ? q_row0 + row
-                              : static_cast<int64_t>(bhq) * p.n + p.out_rows[i * p.b_q + row];
+    const int64_t o_row =
+        p.qblk != nullptr ? (static_cast<int64_t>(bhq) * p.n_qs + il) * p.b_q + row
+        : p.out_rows == nullptr || !valid
+            ? q_row0 + row
+            : static_cast<int64_t>(bhq) * p.n + p.out_rows[i * p.b_q + row];
     uint16_t* orow = out + o_row * D + L * OC;
 #pragma unroll
     for (int c4 = 0; c4 < OC / 32; ++c4) {
@@ -617,10 +624,12 @@ static int launch_attn(const void* q, const void* k, const void* v, const void* 
                        const void* v_pyr, int64_t batch, int hq, int hkv, int64_t n, int b_q,
                        int b_k, int levels, const uint16_t* csr, const int32_t* info, int causal,
                        void* out, float* lse, int32_t* skipped, const int64_t* out_rows,
-                       cudaStream_t s) {
+                       const int32_t* qblk, int n_qs, cudaStream_t s) {
   AttnMaps maps;
   memset(&maps, 0, sizeof(maps));
   AttnParams p{};
+  p.qblk = qblk;
+  p.n_qs = n_qs;
   p.n = n;
   p.hq = hq;
   p.hkv = hkv;
@@ -659,7 +668,7 @@ static int launch_attn(const void* q, const void* k, const void* v, const void* 
     rc = encode_2d(&maps.v[h - 1], vb, rows, D, sz);
     if (rc) return rc;
   }
-  const int64_t units = batch * hq * p.n_q;
+  const int64_t units = batch * hq * p.n_qs;
   const size_t smem2 = sizeof(PP2Smem<D>);
   auto kern2 = psa_attn_pp2_kernel<D>;
   cudaFuncSetAttribute(kern2, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem2));
@@ -1507,12 +1516,12 @@ int attn_bwd_dkv_tc(const void* q, const void* k, const void* v, const void* k_p
 
 using namespace psa;
 
-extern "C" int psa_attn_fwd_scatter(const void* q, const void* k, const void* v,
-                                    const void* k_pyr, const void* v_pyr, int64_t batch, int hq,
-                                    int hkv, int64_t n, int d, int b_q, int b_k, int levels,
-                                    const uint16_t* plan_csr, const int32_t* plan_info, int causal,
-                                    void* out, float* lse, int32_t* skipped_rows,
-                                    const int64_t* out_rows, void* stream) {
+static int attn_fwd_impl(const void* q, const void* k, const void* v, const void* k_pyr,
+                         const void* v_pyr, int64_t batch, int hq, int hkv, int64_t n, int d,
+                         int b_q, int b_k, int levels, const uint16_t* plan_csr,
+                         const int32_t* plan_info, int causal, void* out, float* lse,
+                         int32_t* skipped_rows, const int64_t* out_rows, const int32_t* qblk,
+                         int n_qs, void* stream) {
   PSA_CHECK_ARG(q && k && v && plan_csr && plan_info && out && lse && skipped_rows,
                 "null pointer argument");
   PSA_CHECK_ARG(d == 64 || d == 128, "head_dim must be 64 or 128 for the sm_100a path");
@@ -1525,12 +1534,39 @@ extern "C" int psa_attn_fwd_scatter(const void* q, const void* k, const void* v,
   PSA_CHECK_ARG(n / b_k <= 4096, "n_k must be <= 4096");
   PSA_CHECK_ARG(batch * hq * n < (int64_t(1) << 31), "too many rows for 32-bit TMA coordinates");
   PSA_CHECK_ARG(n < (int64_t(1) << 23), "seq_len must be < 2^23");
+  PSA_CHECK_ARG(n_qs >= 1 && n_qs <= n / b_q, "query-block count outside 1..n_q");
+  PSA_CHECK_ARG(qblk != nullptr || n_qs == n / b_q, "a query-block subset needs its block list");
+  PSA_CHECK_ARG(qblk == nullptr || out_rows == nullptr,
+                "the output row scatter and query-block subsets are exclusive");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (d == 128)
     return launch_attn<128>(q, k, v, k_pyr, v_pyr, batch, hq, hkv, n, b_q, b_k, levels, plan_csr,
-                            plan_info, causal, out, lse, skipped_rows, out_rows, s);
+                            plan_info, causal, out, lse, skipped_rows, out_rows, qblk, n_qs, s);
   return launch_attn<64>(q, k, v, k_pyr, v_pyr, batch, hq, hkv, n, b_q, b_k, levels, plan_csr,
-                         plan_info, causal, out, lse, skipped_rows, out_rows, s);
+                         plan_info, causal, out, lse, skipped_rows, out_rows, qblk, n_qs, s);
+}
+
+extern "C" int psa_attn_fwd_scatter(const void* q, const void* k, const void* v,
+                                    const void* k_pyr, const void* v_pyr, int64_t batch, int hq,
+                                    int hkv, int64_t n, int d, int b_q, int b_k, int levels,
+                                    const uint16_t* plan_csr, const int32_t* plan_info, int causal,
+                                    void* out, float* lse, int32_t* skipped_rows,
+                                    const int64_t* out_rows, void* stream) {
+  PSA_CHECK_ARG(b_q >= 1 && n % b_q == 0, "layout does not divide seq_len");
+  return attn_fwd_impl(q, k, v, k_pyr, v_pyr, batch, hq, hkv, n, d, b_q, b_k, levels, plan_csr,
+                       plan_info, causal, out, lse, skipped_rows, out_rows, nullptr,
+                       static_cast<int>(n / b_q), stream);
+}
+
+extern "C" int psa_attn_fwd_rows(const void* q, const void* k, const void* v, const void* k_pyr,
+                                 const void* v_pyr, int64_t batch, int hq, int hkv, int64_t n,
+                                 int d, int b_q, int b_k, int levels, const uint16_t* plan_csr,
+                                 const int32_t* plan_info, int causal, const int32_t* qblk,
+                                 int n_qsel, void* out, float* lse, int32_t* skipped_rows,
+                                 void* stream) {
+  PSA_CHECK_ARG(qblk != nullptr, "null query-block list");
+  return attn_fwd_impl(q, k, v, k_pyr, v_pyr, batch, hq, hkv, n, d, b_q, b_k, levels, plan_csr,
+                       plan_info, causal, out, lse, skipped_rows, nullptr, qblk, n_qsel, stream);
 }
 
 extern "C" int psa_attn_fwd(const void* q, const void* k, const void* v, const void* k_pyr,

@@ -44,8 +44,10 @@ struct TableRows {  // importance_sampled: rows drawn by the reference's generat
 };
 struct StridedRows {  // antidiagonal: element a of class r = block (a / per) offset r + (a % per)*stride
   int per, block, r, stride;
+  const int32_t* blocks;  // optional list of the call's blocks (query side of q-block work units)
   PSA_DEV int64_t operator()(int a) const {
-    return static_cast<int64_t>(a / per) * block + r + (a % per) * stride;
+    const int bi = blocks != nullptr ? blocks[a / per] : a / per;
+    return static_cast<int64_t>(bi) * block + r + (a % per) * stride;
   }
 };
 
@@ -272,7 +274,8 @@ template <int D>
 __global__ void __launch_bounds__(kImpThreads, 2)
     antidiag_stats_kernel(const uint16_t* __restrict__ q, const uint16_t* __restrict__ k,
                           int hq, int hkv, int64_t n, int b_q, int b_k, int stride, int n_k,
-                          double scale, int bpc, int n_chunks, double* __restrict__ E,
+                          double scale, int bpc, int n_chunks, int n_q,
+                          const int32_t* __restrict__ qblk, double* __restrict__ E,
                           double* __restrict__ Mc, double* __restrict__ mstat,
                           double* __restrict__ lstat, const int32_t* __restrict__ qflag,
                           const int32_t* __restrict__ kflag) {
@@ -283,7 +286,6 @@ __global__ void __launch_bounds__(kImpThreads, 2)
 
   const int r = blockIdx.z;
   const int c_r = r < b_q ? (b_q - r + stride - 1) / stride : 0;  // rows of class r per block
-  const int n_q = static_cast<int>(n / b_q);
   const int R = n_q * c_r;
   const int a0 = blockIdx.x * kImpRows;
   if (a0 >= R) return;
@@ -296,8 +298,8 @@ __global__ void __launch_bounds__(kImpThreads, 2)
   const uint16_t* kh = k + (static_cast<int64_t>(b) * hkv + hk) * n * D;
   const int per = b_k / stride;
   const int kr = (stride - r % stride) % stride;
-  const StridedRows qmap{c_r, b_q, r, stride};
-  const StridedRows kmap{per, b_k, kr, stride};
+  const StridedRows qmap{c_r, b_q, r, stride, qblk};
+  const StridedRows kmap{per, b_k, kr, stride, nullptr};
 
   {
     uint4 buf[kPer];
@@ -362,8 +364,9 @@ __global__ void __launch_bounds__(kImpThreads, 2)
 __global__ void __launch_bounds__(128) antidiag_finalize_kernel(
     const double* __restrict__ E, const double* __restrict__ Mc, const double* __restrict__ mstat,
     const double* __restrict__ lstat, int64_t n, int b_q, int n_q, int n_k, int bpc, int n_chunks,
-    double* __restrict__ S) {
-  const int i = blockIdx.x;
+    const int32_t* __restrict__ qblk, double* __restrict__ S) {
+  const int il = blockIdx.x;  // the call's query block il = block qblk[il] of the head
+  const int i = qblk != nullptr ? qblk[il] : il;
   const int64_t bhq = blockIdx.y;
   constexpr int kMaxBpc = 8;  // blocks per work item (a chunk of bpc > 8 blocks spans several)
   const int subs = (bpc + kMaxBpc - 1) / kMaxBpc;
@@ -384,7 +387,7 @@ __global__ void __launch_bounds__(128) antidiag_finalize_kernel(
     }
 #pragma unroll
     for (int u = 0; u < kMaxBpc; ++u)
-      if (u < nb) S[(bhq * n_q + i) * n_k + j0 + u] = __ddiv_rn(acc[u], static_cast<double>(b_q));
+      if (u < nb) S[(bhq * n_q + il) * n_k + j0 + u] = __ddiv_rn(acc[u], static_cast<double>(b_q));
   }
 }
 
@@ -395,11 +398,11 @@ struct AdGeom {
   XlGeometry xl;
 };
 static AdGeom ad_geometry(int64_t bhq, int64_t bkv, int64_t n, int b_q, int b_k, int stride,
-                          bool allow_xl) {
+                          int n_q, bool allow_xl) {
   AdGeom a{};
   a.per = b_k / stride;
   a.c_max = (b_q + stride - 1) / stride;
-  const int n_q = static_cast<int>(n / b_q), n_k = static_cast<int>(n / b_k);
+  const int n_k = static_cast<int>(n / b_k);
   a.xl = xl_geometry(bhq, bkv, n_q, n_k, stride, n_q * a.c_max, a.per, bhq * n);
   a.xl.ok = a.xl.ok && allow_xl;
   a.bpc = a.xl.ok ? a.xl.bpt : kImpCols / a.per;
@@ -409,19 +412,20 @@ static AdGeom ad_geometry(int64_t bhq, int64_t bkv, int64_t n, int b_q, int b_k,
 
 template <int D>
 static int launch_antidiag_dmma(const void* q, const void* k, int64_t batch, int hq, int hkv,
-                                int64_t n, int b_q, int b_k, int stride, const AdGeom& g,
-                                double* E, double* Mc, double* mstat, double* lstat,
-                                const int32_t* qflag, const int32_t* kflag, cudaStream_t s) {
+                                int64_t n, int b_q, int b_k, int stride, int n_q,
+                                const int32_t* qblk, const AdGeom& g, double* E, double* Mc,
+                                double* mstat, double* lstat, const int32_t* qflag,
+                                const int32_t* kflag, cudaStream_t s) {
   const int64_t bhq = batch * hq;
-  const int n_q = static_cast<int>(n / b_q), n_k = static_cast<int>(n / b_k);
+  const int n_k = static_cast<int>(n / b_k);
   const size_t smem = sizeof(ImpSmem<D>);
   cudaFuncSetAttribute(antidiag_stats_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(smem));
   dim3 grid((n_q * g.c_max + kImpRows - 1) / kImpRows, static_cast<unsigned>(bhq), stride);
   antidiag_stats_kernel<D><<<grid, kImpThreads, smem, s>>>(
       static_cast<const uint16_t*>(q), static_cast<const uint16_t*>(k), hq, hkv, n, b_q, b_k,
-      stride, n_k, 1.0 / sqrt(static_cast<double>(D)), g.bpc, g.n_chunks, E, Mc, mstat, lstat,
-      qflag, kflag);
+      stride, n_k, 1.0 / sqrt(static_cast<double>(D)), g.bpc, g.n_chunks, n_q, qblk, E, Mc, mstat,
+      lstat, qflag, kflag);
   return psa_check_launch("antidiag_stats_kernel");
 }
 
@@ -433,18 +437,42 @@ static size_t ad_fp64_bytes(int64_t bhq, int64_t n, int n_k, int n_chunks) {
   return static_cast<size_t>(bhq * n * (n_k + n_chunks + 2)) * sizeof(double);
 }
 
-extern "C" size_t psa_antidiag_workspace_bytes(int64_t bhq, int64_t bkv, int64_t n, int b_q,
-                                               int b_k, int stride) {
-  if (stride < 1 || b_q < 1 || b_k % stride || b_k / stride > kImpCols || n % b_k || n % b_q)
+extern "C" size_t psa_antidiag_workspace_bytes_rows(int64_t bhq, int64_t bkv, int64_t n, int b_q,
+                                                    int b_k, int stride, int n_qsel) {
+  if (stride < 1 || b_q < 1 || b_k % stride || b_k / stride > kImpCols || n % b_k || n % b_q ||
+      n_qsel < 1)
     return 0;
-  const AdGeom g = ad_geometry(bhq, bkv, n, b_q, b_k, stride, true);
+  const AdGeom g = ad_geometry(bhq, bkv, n, b_q, b_k, stride, n_qsel, true);
   return ad_fp64_bytes(bhq, n, static_cast<int>(n / b_k), g.n_chunks) + (g.xl.ok ? g.xl.bytes : 0);
 }
+
+extern "C" size_t psa_antidiag_workspace_bytes(int64_t bhq, int64_t bkv, int64_t n, int b_q,
+                                               int b_k, int stride) {
+  if (b_q < 1 || n % b_q) return 0;
+  return psa_antidiag_workspace_bytes_rows(bhq, bkv, n, b_q, b_k, stride, static_cast<int>(n / b_q));
+}
+
+extern "C" int psa_importance_antidiagonal_rows(const void* q, const void* k, int64_t batch,
+                                                int hq, int hkv, int64_t n, int d, int b_q, int b_k,
+                                                int stride, int flags, const int32_t* qblk,
+                                                int n_qsel, double* scores, void* workspace,
+                                                void* stream);
 
 extern "C" int psa_importance_antidiagonal(const void* q, const void* k, int64_t batch, int hq,
                                            int hkv, int64_t n, int d, int b_q, int b_k,
                                            int stride, int flags, double* scores,
                                            void* workspace, void* stream) {
+  PSA_CHECK_ARG(b_q >= 1 && n % b_q == 0, "layout does not divide seq_len");
+  return psa_importance_antidiagonal_rows(q, k, batch, hq, hkv, n, d, b_q, b_k, stride, flags,
+                                          nullptr, static_cast<int>(n / b_q), scores, workspace,
+                                          stream);
+}
+
+extern "C" int psa_importance_antidiagonal_rows(const void* q, const void* k, int64_t batch,
+                                                int hq, int hkv, int64_t n, int d, int b_q, int b_k,
+                                                int stride, int flags, const int32_t* qblk,
+                                                int n_qsel, double* scores, void* workspace,
+                                                void* stream) {
   PSA_CHECK_ARG(q && k && scores && workspace, "null pointer argument");
   PSA_CHECK_ARG(d == 64 || d == 128, "head_dim must be 64 or 128 for the sm_100a path");
   PSA_CHECK_ARG(hq >= 1 && hkv >= 1 && hq % hkv == 0, "query heads must be a multiple of kv heads");
@@ -452,10 +480,12 @@ extern "C" int psa_importance_antidiagonal(const void* q, const void* k, int64_t
   PSA_CHECK_ARG(stride >= 1 && b_k % stride == 0, "stride must divide k_block");
   PSA_CHECK_ARG(b_k / stride <= kImpCols,
                 "k_block / stride > 64 is not supported by the sm_100a antidiagonal kernel");
+  PSA_CHECK_ARG(n_qsel >= 1 && n_qsel <= n / b_q, "query-block count outside 1..n_q");
+  PSA_CHECK_ARG(qblk != nullptr || n_qsel == n / b_q, "a query-block subset needs its block list");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t bhq = batch * hq, bkv = batch * hkv;
-  const int n_q = static_cast<int>(n / b_q), n_k = static_cast<int>(n / b_k);
-  const AdGeom g = ad_geometry(bhq, bkv, n, b_q, b_k, stride, !(flags & PSA_IMP_FP64_ONLY));
+  const int n_q = n_qsel, n_k = static_cast<int>(n / b_k);
+  const AdGeom g = ad_geometry(bhq, bkv, n, b_q, b_k, stride, n_q, !(flags & PSA_IMP_FP64_ONLY));
   double* E = static_cast<double*>(workspace);
   double* Mc = E + bhq * n * n_k;
   double* mstat = Mc + bhq * n * g.n_chunks;
@@ -465,19 +495,19 @@ extern "C" int psa_importance_antidiagonal(const void* q, const void* k, int64_t
   int rc = PSA_OK;
   if (g.xl.ok) {
     void* xws = static_cast<uint8_t*>(workspace) + ad_fp64_bytes(bhq, n, n_k, g.n_chunks);
-    rc = xl_antidiag(q, k, batch, hq, hkv, n, d, b_q, b_k, stride, g.xl, xws, E, Mc, mstat,
-                     lstat, s);
+    rc = xl_antidiag(q, k, batch, hq, hkv, n, d, b_q, b_k, stride, n_q, qblk, g.xl, xws, E, Mc,
+                     mstat, lstat, s);
     if (rc) return rc;
     qflag = xl_qflags(g.xl, xws);
     kflag = qflag + bhq;
   }
-  rc = d == 128 ? launch_antidiag_dmma<128>(q, k, batch, hq, hkv, n, b_q, b_k, stride, g, E, Mc,
-                                            mstat, lstat, qflag, kflag, s)
-                : launch_antidiag_dmma<64>(q, k, batch, hq, hkv, n, b_q, b_k, stride, g, E, Mc,
-                                           mstat, lstat, qflag, kflag, s);
+  rc = d == 128 ? launch_antidiag_dmma<128>(q, k, batch, hq, hkv, n, b_q, b_k, stride, n_q, qblk,
+                                            g, E, Mc, mstat, lstat, qflag, kflag, s)
+                : launch_antidiag_dmma<64>(q, k, batch, hq, hkv, n, b_q, b_k, stride, n_q, qblk,
+                                           g, E, Mc, mstat, lstat, qflag, kflag, s);
   if (rc) return rc;
   antidiag_finalize_kernel<<<dim3(n_q, bhq), 128, 0, s>>>(E, Mc, mstat, lstat, n, b_q, n_q, n_k,
-                                                          g.bpc, g.n_chunks, scores);
+                                                          g.bpc, g.n_chunks, qblk, scores);
   return psa_check_launch("antidiag_finalize_kernel");
 }
 
@@ -502,8 +532,8 @@ extern "C" size_t psa_importance_workspace_bytes(int64_t bhq, int64_t bkv, int n
 
 template <int D>
 static int launch_importance(const void* q, const void* k, int64_t batch, int hq, int hkv,
-                             int64_t n, const int32_t* q_rows, const int32_t* k_rows, int R,
-                             int s_q, int s_k, int n_q, int n_k, int reducer, int flags,
+                             int64_t n, int b_q, const int32_t* q_rows, const int32_t* k_rows,
+                             int R, int s_q, int s_k, int n_q, int n_k, int reducer, int flags,
                              double* scores, void* ws, cudaStream_t s) {
   const int64_t bhq = batch * hq, bkv = batch * hkv;
   double* M = static_cast<double*>(ws);
@@ -516,9 +546,8 @@ static int launch_importance(const void* q, const void* k, int64_t batch, int hq
                                            reducer == 0 && !(flags & PSA_IMP_FP64_ONLY));
   if (g.ok) {  // exact logits on the int8 tensor cores; DMMA only for the heads it flags
     void* xws = static_cast<uint8_t*>(ws) + sampled_fp64_bytes(bhq, n_q, s_q, n_k);
-    rc = xl_sampled_max(q, k, batch, hq, hkv, n, D, static_cast<int>(n / n_q),
-                        static_cast<int>(n / n_k), q_rows, k_rows, s_q, s_k, g, xws, M, mstat,
-                        lstat, s);
+    rc = xl_sampled_max(q, k, batch, hq, hkv, n, D, b_q, static_cast<int>(n / n_k), n_q, q_rows,
+                        k_rows, s_q, s_k, g, xws, M, mstat, lstat, s);
     if (rc) return rc;
     qflag = xl_qflags(g, xws);
     kflag = qflag + bhq;
@@ -551,11 +580,30 @@ static int launch_importance(const void* q, const void* k, int64_t batch, int hq
   return psa_check_launch("importance_finalize_kernel");
 }
 
+extern "C" int psa_importance_sampled_rows(const void* q, const void* k, int64_t batch, int hq,
+                                           int hkv, int64_t n, int d, int b_q, int b_k,
+                                           const int32_t* q_rows, const int32_t* k_rows, int s_q,
+                                           int s_k, int reducer, int flags, int n_qsel,
+                                           double* scores, void* workspace, void* stream);
+
 extern "C" int psa_importance_sampled(const void* q, const void* k, int64_t batch, int hq,
                                       int hkv, int64_t n, int d, int b_q, int b_k,
                                       const int32_t* q_rows, const int32_t* k_rows, int s_q,
                                       int s_k, int reducer, int flags, double* scores,
                                       void* workspace, void* stream) {
+  PSA_CHECK_ARG(b_q >= 1 && n % b_q == 0, "layout does not divide seq_len");
+  return psa_importance_sampled_rows(q, k, batch, hq, hkv, n, d, b_q, b_k, q_rows, k_rows, s_q,
+                                     s_k, reducer, flags, static_cast<int>(n / b_q), scores,
+                                     workspace, stream);
+}
+
+// q_rows: the sample rows of the call's n_qsel query blocks (n_qsel * s_q entries, block-major);
+// scores: fp64 [batch*hq, n_qsel, n_k] (the q-block work units of the multi-GPU partition).
+extern "C" int psa_importance_sampled_rows(const void* q, const void* k, int64_t batch, int hq,
+                                           int hkv, int64_t n, int d, int b_q, int b_k,
+                                           const int32_t* q_rows, const int32_t* k_rows, int s_q,
+                                           int s_k, int reducer, int flags, int n_qsel,
+                                           double* scores, void* workspace, void* stream) {
   PSA_CHECK_ARG(q && k && q_rows && k_rows && scores && workspace, "null pointer argument");
   PSA_CHECK_ARG(d == 64 || d == 128, "head_dim must be 64 or 128 for the sm_100a path");
   PSA_CHECK_ARG(hq >= 1 && hkv >= 1 && hq % hkv == 0, "query heads must be a multiple of kv heads");
@@ -564,12 +612,13 @@ extern "C" int psa_importance_sampled(const void* q, const void* k, int64_t batc
   PSA_CHECK_ARG(s_k >= 1 && s_k <= b_k, "s_k outside 1..k_block");
   PSA_CHECK_ARG(s_k <= kImpCols, "s_k > 64 is not supported by the sm_100a importance kernel");
   PSA_CHECK_ARG(reducer == 0 || reducer == 1, "reducer must be 0 (max) or 1 (mean)");
-  const int n_q = static_cast<int>(n / b_q), n_k = static_cast<int>(n / b_k);
+  PSA_CHECK_ARG(n_qsel >= 1 && n_qsel <= n / b_q, "query-block count outside 1..n_q");
+  const int n_q = n_qsel, n_k = static_cast<int>(n / b_k);
   const int R = n_q * s_q;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (d == 128)
-    return launch_importance<128>(q, k, batch, hq, hkv, n, q_rows, k_rows, R, s_q, s_k, n_q, n_k,
-                                  reducer, flags, scores, workspace, s);
-  return launch_importance<64>(q, k, batch, hq, hkv, n, q_rows, k_rows, R, s_q, s_k, n_q, n_k,
-                               reducer, flags, scores, workspace, s);
+    return launch_importance<128>(q, k, batch, hq, hkv, n, b_q, q_rows, k_rows, R, s_q, s_k, n_q,
+                                  n_k, reducer, flags, scores, workspace, s);
+  return launch_importance<64>(q, k, batch, hq, hkv, n, b_q, q_rows, k_rows, R, s_q, s_k, n_q,
+                               n_k, reducer, flags, scores, workspace, s);
 }

@@ -36,13 +36,15 @@ struct XlGeometry {
 };
 XlGeometry xl_geometry(int64_t bhq, int64_t bkv, int n_q, int n_k, int classes, int rows_per_class,
                        int per, int64_t out_rows);
+// n_q: query blocks of the call (the q_rows table holds n_q * s_q rows); qblk: optional list of
+// the call's query blocks (antidiagonal; NULL = blocks 0..n_q-1)
 int xl_sampled_max(const void* q, const void* k, int64_t batch, int hq, int hkv, int64_t n, int d,
-                   int b_q, int b_k, const int32_t* q_rows, const int32_t* k_rows, int s_q,
+                   int b_q, int b_k, int n_q, const int32_t* q_rows, const int32_t* k_rows, int s_q,
                    int s_k, const XlGeometry& g, void* ws, double* M, double* mstat,
                    double* lstat, cudaStream_t s);
 int xl_antidiag(const void* q, const void* k, int64_t batch, int hq, int hkv, int64_t n, int d,
-                int b_q, int b_k, int stride, const XlGeometry& g, void* ws, double* E,
-                double* Mc, double* mstat, double* lstat, cudaStream_t s);
+                int b_q, int b_k, int stride, int n_q, const int32_t* qblk, const XlGeometry& g,
+                void* ws, double* E, double* Mc, double* mstat, double* lstat, cudaStream_t s);
 // device flags [bhq] then [bkv]: heads the int8 path could not represent exactly
 const int32_t* xl_qflags(const XlGeometry& g, const void* ws);
 

@@ -157,8 +157,9 @@ struct XlTableRows {  // sampled rows (host table of the reference's generator),
   PSA_DEV int count(int total) const { return total; }
   PSA_DEV int64_t operator()(int a) const { return rows[a]; }
 };
-struct XlQueryClass {  // antidiagonal query rows p = r (mod stride) of every query block
+struct XlQueryClass {  // antidiagonal query rows p = r (mod stride) of every (listed) query block
   int r, c_r, block, stride, n_blocks;
+  const int32_t* blocks;  // optional: the query blocks of this call (q-block work units)
   PSA_DEV void set_class(int cls, int stride_, int block_) {
     r = cls;
     stride = stride_;
@@ -167,7 +168,8 @@ struct XlQueryClass {  // antidiagonal query rows p = r (mod stride) of every qu
   }
   PSA_DEV int count(int) const { return n_blocks * c_r; }
   PSA_DEV int64_t operator()(int a) const {
-    return static_cast<int64_t>(a / c_r) * block + r + (a % c_r) * stride;
+    const int bi = blocks != nullptr ? blocks[a / c_r] : a / c_r;
+    return static_cast<int64_t>(bi) * block + r + (a % c_r) * stride;
   }
 };
 struct XlKeyClass {  // antidiagonal key columns c = kr (mod stride) of every KV block
@@ -883,10 +885,10 @@ static int xl_launch(const void* q, const void* k, int64_t batch, int hq, int hk
 }
 
 int xl_sampled_max(const void* q, const void* k, int64_t batch, int hq, int hkv, int64_t n, int d,
-                   int b_q, int b_k, const int32_t* q_rows, const int32_t* k_rows, int s_q,
+                   int b_q, int b_k, int n_q, const int32_t* q_rows, const int32_t* k_rows, int s_q,
                    int s_k, const XlGeometry& g, void* ws, double* M, double* mstat,
                    double* lstat, cudaStream_t s) {
-  const int n_q = static_cast<int>(n / b_q), n_k = static_cast<int>(n / b_k);
+  const int n_k = static_cast<int>(n / b_k);
   XlTableRows qr{q_rows}, kr{k_rows};
   if (d == 128)
     return xl_launch<128, kXlMax>(q, k, batch, hq, hkv, n, b_q, b_k, 1, g, qr, kr, n_q * s_q,
@@ -896,11 +898,12 @@ int xl_sampled_max(const void* q, const void* k, int64_t batch, int hq, int hkv,
 }
 
 int xl_antidiag(const void* q, const void* k, int64_t batch, int hq, int hkv, int64_t n, int d,
-                int b_q, int b_k, int stride, const XlGeometry& g, void* ws, double* E,
-                double* Mc, double* mstat, double* lstat, cudaStream_t s) {
-  const int n_q = static_cast<int>(n / b_q), n_k = static_cast<int>(n / b_k);
+                int b_q, int b_k, int stride, int n_q, const int32_t* qblk, const XlGeometry& g,
+                void* ws, double* E, double* Mc, double* mstat, double* lstat, cudaStream_t s) {
+  const int n_k = static_cast<int>(n / b_k);
   XlQueryClass qr{};
   qr.n_blocks = n_q;
+  qr.blocks = qblk;
   XlKeyClass kr{};
   kr.n_blocks = n_k;
   if (d == 128)

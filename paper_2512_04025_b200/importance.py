@@ -48,13 +48,28 @@ def _flags(fp64_only: bool) -> int:
     return _lib.PSA_IMP_FP64_ONLY if fp64_only else 0
 
 
+def query_blocks(qblocks, layout: BlockLayout, device) -> torch.Tensor | None:
+    """Validate a query-block subset (the (b, h, q-block set) work units of parallel.py) and
+    return it as a device int32 tensor, or None for every block."""
+    if qblocks is None:
+        return None
+    blk = torch.as_tensor(qblocks, dtype=torch.int64).reshape(-1).cpu()
+    if blk.numel() == 0 or int(blk.min()) < 0 or int(blk.max()) >= layout.n_q:
+        raise ValidationError(f"query blocks must be a non-empty subset of 0..{layout.n_q - 1}")
+    if torch.unique(blk).numel() != blk.numel():
+        raise ValidationError("query blocks must be distinct")
+    return blk.to(torch.int32).to(device)
+
+
 def importance_scores(q4: torch.Tensor, k4: torch.Tensor, layout: BlockLayout,
                       cfg: SamplerConfig, reducer: str = "max",
-                      fp64_only: bool = False) -> torch.Tensor:
+                      fp64_only: bool = False, qblocks=None) -> torch.Tensor:
     """fp64 scores [B, Hq, n_q, n_k] from bf16 [B, H, N, d] device tensors.
 
     Logits are exact (int8-sliced tensor cores, psa_xlogits.cu); ``fp64_only`` forces the fp64
-    DMMA kernel instead (same values; used to cross-check the two paths)."""
+    DMMA kernel instead (same values; used to cross-check the two paths). ``qblocks``: only
+    these query blocks (rows of the result, in that order; the reference's sample rows of those
+    blocks, so each row equals the full call's)."""
     if reducer not in ("max", "mean"):
         raise ValidationError(f"reducer must be 'max' or 'mean', got {reducer!r}")
     cfg.validate(layout)
@@ -66,16 +81,21 @@ def importance_scores(q4: torch.Tensor, k4: torch.Tensor, layout: BlockLayout,
         raise ValidationError(f"query heads {Hq} not a multiple of kv heads {Hkv}")
     dev = q4.device
     q_rows, k_rows = sample_tables(layout, cfg, dev)
+    blk = query_blocks(qblocks, layout, dev)
+    n_sel = layout.n_q
+    if blk is not None:  # the table rows of the listed blocks, block-major
+        n_sel = blk.numel()
+        q_rows = q_rows.view(layout.n_q, cfg.s_q)[blk.long()].reshape(-1).contiguous()
     lib = _lib.load()
-    ws_bytes = lib.psa_importance_workspace_bytes(B * Hq, B * Hkv, layout.n_q, cfg.s_q,
+    ws_bytes = lib.psa_importance_workspace_bytes(B * Hq, B * Hkv, n_sel, cfg.s_q,
                                                   layout.n_k, cfg.s_k)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
-    scores = torch.empty(B, Hq, layout.n_q, layout.n_k, dtype=torch.float64, device=dev)
-    rc = lib.psa_importance_sampled(q4.data_ptr(), k4.data_ptr(), B, Hq, Hkv, n, d,
-                                    layout.q_block, layout.k_block, q_rows.data_ptr(),
-                                    k_rows.data_ptr(), cfg.s_q, cfg.s_k,
-                                    0 if reducer == "max" else 1, _flags(fp64_only),
-                                    scores.data_ptr(), ws.data_ptr(), stream_handle(dev))
+    scores = torch.empty(B, Hq, n_sel, layout.n_k, dtype=torch.float64, device=dev)
+    rc = lib.psa_importance_sampled_rows(q4.data_ptr(), k4.data_ptr(), B, Hq, Hkv, n, d,
+                                         layout.q_block, layout.k_block, q_rows.data_ptr(),
+                                         k_rows.data_ptr(), cfg.s_q, cfg.s_k,
+                                         0 if reducer == "max" else 1, _flags(fp64_only), n_sel,
+                                         scores.data_ptr(), ws.data_ptr(), stream_handle(dev))
     _lib.check(rc, "psa_importance_sampled")
     return scores
 
@@ -104,8 +124,9 @@ def antidiagonal_selection(b_q: int, b_k: int, stride: int) -> torch.Tensor:
 
 
 def antidiagonal_scores(q4: torch.Tensor, k4: torch.Tensor, layout: BlockLayout,
-                        stride: int, fp64_only: bool = False) -> torch.Tensor:
-    """fp64 antidiagonal scores [B, Hq, n_q, n_k] from bf16 [B, H, N, d] device tensors."""
+                        stride: int, fp64_only: bool = False, qblocks=None) -> torch.Tensor:
+    """fp64 antidiagonal scores [B, Hq, n_q, n_k] from bf16 [B, H, N, d] device tensors
+    (``qblocks``: only these query blocks, rows in that order)."""
     if stride is None or int(stride) < 1 or layout.k_block % int(stride):
         raise ValidationError(f"stride {stride} must divide k_block {layout.k_block}")
     stride = int(stride)
@@ -117,15 +138,18 @@ def antidiagonal_scores(q4: torch.Tensor, k4: torch.Tensor, layout: BlockLayout,
     if Hq % Hkv:
         raise ValidationError(f"query heads {Hq} not a multiple of kv heads {Hkv}")
     dev = q4.device
+    blk = query_blocks(qblocks, layout, dev)
+    n_sel = layout.n_q if blk is None else blk.numel()
     lib = _lib.load()
-    ws = torch.empty(lib.psa_antidiag_workspace_bytes(B * Hq, B * Hkv, n, layout.q_block,
-                                                      layout.k_block, stride),
+    ws = torch.empty(lib.psa_antidiag_workspace_bytes_rows(B * Hq, B * Hkv, n, layout.q_block,
+                                                           layout.k_block, stride, n_sel),
                      dtype=torch.uint8, device=dev)
-    scores = torch.empty(B, Hq, layout.n_q, layout.n_k, dtype=torch.float64, device=dev)
-    rc = lib.psa_importance_antidiagonal(q4.data_ptr(), k4.data_ptr(), B, Hq, Hkv, n, d,
-                                         layout.q_block, layout.k_block, stride,
-                                         _flags(fp64_only), scores.data_ptr(), ws.data_ptr(),
-                                         stream_handle(dev))
+    scores = torch.empty(B, Hq, n_sel, layout.n_k, dtype=torch.float64, device=dev)
+    rc = lib.psa_importance_antidiagonal_rows(q4.data_ptr(), k4.data_ptr(), B, Hq, Hkv, n, d,
+                                              layout.q_block, layout.k_block, stride,
+                                              _flags(fp64_only), _lib.ptr(blk), n_sel,
+                                              scores.data_ptr(), ws.data_ptr(),
+                                              stream_handle(dev))
     _lib.check(rc, "psa_importance_antidiagonal")
     return scores
 

@@ -56,9 +56,11 @@ def _alloc_plan(B: int, Hq: int, n_q: int, n_k: int, levels: int, dev) -> MaskPl
 
 def assign_levels_device(scores: torch.Tensor, *, mode: str, rule, levels: int,
                          b_q: int = 1, b_k: int = 1, hkv: int | None = None,
-                         caps: torch.Tensor | None = None, causal: bool = False) -> MaskPlan:
+                         caps: torch.Tensor | None = None, causal: bool = False,
+                         qblocks: torch.Tensor | None = None) -> MaskPlan:
     """scores fp64 [B, Hq, n_q, n_k] (device) -> MaskPlan. ``rule`` is LevelThresholds
-    (mode 'threshold') or QuantileCutpoints (mode 'quantile')."""
+    (mode 'threshold') or QuantileCutpoints (mode 'quantile'). ``qblocks`` (device int32
+    [n_q]): score row i is query block qblocks[i] of the head (q-block work units)."""
     B, Hq, n_q, n_k = scores.shape
     hkv = Hq if hkv is None else hkv
     dev = scores.device
@@ -69,11 +71,13 @@ def assign_levels_device(scores: torch.Tensor, *, mode: str, rule, levels: int,
         taus, counts, m = _lib.host_doubles(rule.taus), None, 0
     else:
         taus, counts, m = None, _lib.host_ints(rule.counts(n_k)), 1
-    rc = _lib.load().psa_assign_levels(
+    if qblocks is not None and qblocks.numel() != n_q:
+        raise ValidationError(f"{qblocks.numel()} query blocks for {n_q} score rows")
+    rc = _lib.load().psa_assign_levels_rows(
         scores.data_ptr(), B, Hq, hkv, n_q, n_k, m, taus, counts, len(rule),
-        _lib.ptr(caps), int(causal), b_q, b_k, levels, plan.level_map.data_ptr(),
-        plan.csr.data_ptr(), plan.info.data_ptr(), plan.level_counts.data_ptr(),
-        stream_handle(dev))
+        _lib.ptr(caps), int(causal), b_q, b_k, levels, _lib.ptr(qblocks),
+        plan.level_map.data_ptr(), plan.csr.data_ptr(), plan.info.data_ptr(),
+        plan.level_counts.data_ptr(), stream_handle(dev))
     _lib.check(rc, "psa_assign_levels")
     return plan
 

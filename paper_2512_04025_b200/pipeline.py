@@ -21,7 +21,7 @@ import torch
 from ._tensors import as_bhnd, restore
 from .attention import attention_forward
 from .errors import NumericError, ValidationError
-from .importance import antidiagonal_scores, importance_scores
+from .importance import antidiagonal_scores, importance_scores, query_blocks
 from .layout import (PRESET_CUTPOINTS, LevelThresholds, QuantileCutpoints, SamplerConfig,
                      SimThresholds, make_layout)
 from .mask import MaskPlan, assign_levels_device
@@ -166,11 +166,17 @@ def _mask_rule(cfg: RunConfig, levels: int):
 
 
 def psa_forward_4d(q4, k4, v4, cfg: RunConfig, keep_scores: bool = False,
-                   out: torch.Tensor | None = None, lse: torch.Tensor | None = None) -> PSAResult:
+                   out: torch.Tensor | None = None, lse: torch.Tensor | None = None,
+                   qblocks=None) -> PSAResult:
     """Fused PSA forward on contiguous bf16 [B, H, N, d] device tensors (``out``/``lse``:
-    optional preallocated device outputs)."""
+    optional preallocated device outputs). ``qblocks``: run only these query blocks of every
+    head (a (b, h, q-block set) work unit of parallel.py); importance rows, level map, plan, O
+    and lse then hold those blocks in that order (compact), each identical to the full call's."""
     lay = cfg.layout()
     lay.check_gpu()
+    blk = _stage("partition", query_blocks, qblocks, lay, q4.device)
+    if blk is not None and cfg.grid is not None:
+        raise ValidationError("query-block subsets are not supported with grid permutations")
     perm = order = None
     if cfg.grid is not None:  # pipeline.py:257-263: curve order applied to Q, K and V
         perm = _stage("permutation", hilbert_order, cfg.grid)
@@ -185,20 +191,22 @@ def psa_forward_4d(q4, k4, v4, cfg: RunConfig, keep_scores: bool = False,
     B, Hq = q4.shape[:2]
     Hkv = k4.shape[1]
     if cfg.estimator == "antidiagonal":  # pipeline._estimate (pipeline.py:239-244)
-        scores = _stage("importance", antidiagonal_scores, q4, k4, lay, cfg.stride)
+        scores = _stage("importance", antidiagonal_scores, q4, k4, lay, cfg.stride, qblocks=blk)
     else:
         sampler = SamplerConfig(s_q=cfg.s_q, s_k=cfg.s_k, seed=cfg.seed)
         reducer = "max" if cfg.estimator == "sampled-max" else "mean"
-        scores = _stage("importance", importance_scores, q4, k4, lay, sampler, reducer)
+        scores = _stage("importance", importance_scores, q4, k4, lay, sampler, reducer,
+                        qblocks=blk)
     caps = None
     if cfg.sim_thresholds is not None:
         caps = _stage("similarity-cap", similarity_caps, k4, lay, SimThresholds(cfg.sim_thresholds))
     plan = _stage("mask", assign_levels_device, scores, mode=mode, rule=rule, levels=lay.levels,
-                  b_q=lay.q_block, b_k=lay.k_block, hkv=Hkv, caps=caps, causal=cfg.causal)
+                  b_q=lay.q_block, b_k=lay.k_block, hkv=Hkv, caps=caps, causal=cfg.causal,
+                  qblocks=blk)
     # pipeline.py:312-313 (back to the caller's token order) fused into the attention epilogue
     scatter = order if perm is not None and cfg.unpermute else None
     out, lse, skipped = _stage("executor", attention_forward, q4, pyr, plan, cfg.causal, out, lse,
-                               None, scatter)
+                               None, scatter, blk)
     return PSAResult(out=out, lse=lse, plan=plan, skipped=skipped,
                      scores=scores if keep_scores else None, pyramid=pyr)
 
@@ -217,7 +225,7 @@ def resolve_config(cfg: RunConfig | None, n: int, d: int, overrides: dict) -> Ru
 
 
 def psa_attention(q, k, v, cfg: RunConfig | None = None, *, keep_scores: bool = False,
-                  **overrides) -> PSAResult:
+                  qblocks=None, **overrides) -> PSAResult:
     """Pyramid sparse attention forward.
 
     ``q``: (n, d), (Hq, n, d) or (B, Hq, n, d); ``k``/``v``: same with Hkv heads (Hq % Hkv == 0).
@@ -228,10 +236,13 @@ def psa_attention(q, k, v, cfg: RunConfig | None = None, *, keep_scores: bool = 
     ``staging.psa_attention_staged``: head groups are copied in, computed and copied back on
     three overlapped streams, and the result lives in host memory (the reference's
     arrays-in/arrays-out contract); the compute is the same sm_100a path, never a CPU one.
+    ``qblocks``: only these query blocks of every head (a work unit of parallel.partition); the
+    outputs then hold those blocks' rows (compact).
     """
     if isinstance(q, torch.Tensor) and not q.is_cuda:
         from .staging import psa_attention_staged  # host tensors: pipelined staging onto the GPU
-        return psa_attention_staged(q, k, v, cfg, keep_scores=keep_scores, **overrides)
+        return psa_attention_staged(q, k, v, cfg, keep_scores=keep_scores, qblocks=qblocks,
+                                    **overrides)
     q4, lead = as_bhnd(q, "Q")
     k4, _ = as_bhnd(k, "K", q4.shape[2], q4.shape[3])
     v4, _ = as_bhnd(v, "V", q4.shape[2], q4.shape[3])
@@ -239,9 +250,10 @@ def psa_attention(q, k, v, cfg: RunConfig | None = None, *, keep_scores: bool = 
         raise ValidationError(f"Q/K/V shapes differ: {tuple(q4.shape)}/{tuple(k4.shape)}/"
                               f"{tuple(v4.shape)}")
     cfg = resolve_config(cfg, q4.shape[2], q4.shape[3], overrides)
-    res = psa_forward_4d(q4, k4, v4, cfg, keep_scores=keep_scores)
-    res.out = restore(res.out, lead)
-    res.lse = res.lse.reshape(lead + (cfg.n,))
+    res = psa_forward_4d(q4, k4, v4, cfg, keep_scores=keep_scores, qblocks=qblocks)
+    rows = res.out.shape[2]
+    res.out = res.out.reshape(lead + (rows, q4.shape[3]))
+    res.lse = res.lse.reshape(lead + (rows,))
     return res
 
 

@@ -72,7 +72,7 @@ def _group_sizes(n: int) -> list:
 def psa_attention_staged(q, k, v, cfg=None, *, device=None, kv_heads_per_group: int | None = None,
                          out: torch.Tensor | None = None, lse: torch.Tensor | None = None,
                          keep_level_map: bool = False, keep_scores: bool = False,
-                         **overrides) -> StagedResult:
+                         qblocks=None, **overrides) -> StagedResult:
     """PSA forward of host tensors on ``device`` (default: the current CUDA device).
 
     ``out`` / ``lse``: optional preallocated (ideally pinned) host outputs of shapes
@@ -99,6 +99,9 @@ def psa_attention_staged(q, k, v, cfg=None, *, device=None, kv_heads_per_group: 
     cfg = resolve_config(cfg, n, d, overrides)
     lay = cfg.layout()
     group = Hq // Hkv
+    # query-block work unit (parallel.partition): outputs hold the listed blocks' rows, compact
+    n_sel = lay.n_q if qblocks is None else len(list(qblocks))
+    rows = n_sel * lay.q_block
     if kv_heads_per_group is None:
         sizes = _group_sizes(Hkv) if B == 1 else [max(1, math.ceil(B * Hkv / 8))]
     else:
@@ -106,14 +109,14 @@ def psa_attention_staged(q, k, v, cfg=None, *, device=None, kv_heads_per_group: 
     g = max(sizes)
 
     if out is None:
-        out = torch.empty(q4.shape, dtype=torch.bfloat16, pin_memory=True)
+        out = torch.empty(B, Hq, rows, d, dtype=torch.bfloat16, pin_memory=True)
     if lse is None:
-        lse = torch.empty(B, Hq, n, dtype=torch.float32, pin_memory=True)
-    out4 = out.reshape(B, Hq, n, d)
-    lse3 = lse.reshape(B, Hq, n)
+        lse = torch.empty(B, Hq, rows, dtype=torch.float32, pin_memory=True)
+    out4 = out.reshape(B, Hq, rows, d)
+    lse3 = lse.reshape(B, Hq, rows)
     if out4.dtype != torch.bfloat16 or lse3.dtype != torch.float32 or out4.is_cuda or lse3.is_cuda:
         raise ValidationError("out must be a bf16 and lse an fp32 host tensor")
-    lmap = (torch.empty(B, Hq, lay.n_q, lay.n_k, dtype=torch.int8, pin_memory=True)
+    lmap = (torch.empty(B, Hq, n_sel, lay.n_k, dtype=torch.int8, pin_memory=True)
             if keep_level_map else None)
 
     groups = []
@@ -134,8 +137,8 @@ def psa_attention_staged(q, k, v, cfg=None, *, device=None, kv_heads_per_group: 
                 "q": torch.empty(1, g * group, n, d, dtype=torch.bfloat16, device=dev),
                 "k": torch.empty(1, g, n, d, dtype=torch.bfloat16, device=dev),
                 "v": torch.empty(1, g, n, d, dtype=torch.bfloat16, device=dev),
-                "o": torch.empty(1, g * group, n, d, dtype=torch.bfloat16, device=dev),
-                "l": torch.empty(1, g * group, n, dtype=torch.float32, device=dev),
+                "o": torch.empty(1, g * group, rows, d, dtype=torch.bfloat16, device=dev),
+                "l": torch.empty(1, g * group, rows, dtype=torch.float32, device=dev),
                 "free_in": None, "free_out": None,
             })
         counts = torch.zeros(lay.levels + 1, dtype=torch.int64, device=dev)
@@ -156,7 +159,7 @@ def psa_attention_staged(q, k, v, cfg=None, *, device=None, kv_heads_per_group: 
             s_cmp.wait_event(ready)
             if sl["free_out"] is not None:
                 s_cmp.wait_event(sl["free_out"])
-            res = psa_forward_4d(qs, ks, vs, cfg, out=os_, lse=ls)
+            res = psa_forward_4d(qs, ks, vs, cfg, out=os_, lse=ls, qblocks=qblocks)
             counts += res.plan.level_counts
             skipped += res.skipped
             done = torch.cuda.Event()
@@ -175,6 +178,6 @@ def psa_attention_staged(q, k, v, cfg=None, *, device=None, kv_heads_per_group: 
         cur.wait_stream(s_out)
         s_out.synchronize()
         tail = torch.cat([counts, skipped]).cpu().tolist()
-    return StagedResult(out=out4.reshape(lead + (n, d)),
-                        lse=lse3.reshape(lead + (n,)), level_counts=[int(c) for c in tail[:-1]],
+    return StagedResult(out=out4.reshape(lead + (rows, d)),
+                        lse=lse3.reshape(lead + (rows,)), level_counts=[int(c) for c in tail[:-1]],
                         skipped=int(tail[-1]), level_map=lmap)

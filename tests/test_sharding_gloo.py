@@ -74,3 +74,39 @@ def test_gather_world2_gloo(hq, hkv):
         p.join(120)
     res = [q.get(timeout=5) for _ in range(2)]
     assert all(res) and all(p.exitcode == 0 for p in procs)
+
+
+def _part_worker(rank, world, port, hq, hkv, n_q, b_q, causal, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2512_04025_b200.parallel import gather_partitioned, partition
+        full = torch.arange(2 * hq * n_q * b_q * 3, dtype=torch.float32).reshape(2, hq, n_q * b_q, 3)
+        pieces = []
+        for q_lo, q_hi, _, _, blocks in partition(hq, hkv, n_q, world, rank, causal):
+            x = full[:, q_lo:q_hi].reshape(2, q_hi - q_lo, n_q, b_q, 3)
+            if blocks is not None:
+                x = x[:, :, blocks]
+            pieces.append(x.reshape(2, q_hi - q_lo, -1, 3) * 1.0)
+        got = gather_partitioned(pieces, hq, hkv, n_q, b_q, causal, dst=0)
+        q.put(bool(torch.equal(got, full)) if rank == 0 else got is None)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("hq,hkv,n_q,causal,world", [(3, 3, 10, False, 2), (4, 2, 9, True, 3),
+                                                     (12, 12, 17, False, 8)])
+def test_gather_partitioned_gloo(hq, hkv, n_q, causal, world):
+    """(batch, head, query-block set) pieces of every rank reassemble the full output on rank 0."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_part_worker, args=(r, world, port, hq, hkv, n_q, 4, causal, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(180)
+    res = [q.get(timeout=5) for _ in range(world)]
+    assert all(res) and all(p.exitcode == 0 for p in procs)
