@@ -16,8 +16,41 @@ def require_cuda(x: torch.Tensor, name: str) -> None:
                               "only implementation (no CPU fallback)")
 
 
-def as_bhnd(x: torch.Tensor, name: str, n: int | None = None, d: int | None = None):
-    """Return (x as contiguous bf16 [B, H, N, d], original leading shape)."""
+def to_device(x, name: str) -> torch.Tensor:
+    """Array-likes and host tensors (the reference accepts anything as_matrix converts,
+    pkg/src/pyrattn/linalg.py:15-24) are staged onto the current CUDA device; CUDA tensors pass
+    through. Without a CUDA device this raises: there is no CPU implementation."""
+    if isinstance(x, torch.Tensor) and x.is_cuda:
+        return x
+    if not torch.cuda.is_available():
+        raise ValidationError(f"{name} must live on a CUDA device: the sm_100a kernels are the only "
+                              "implementation (no CPU fallback)")
+    if not isinstance(x, torch.Tensor):
+        import numpy as np
+        try:
+            arr = np.asarray(x)
+        except Exception as exc:  # noqa: BLE001
+            raise ValidationError(f"{name} is not array-like: {exc}") from exc
+        if arr.dtype == object or not (np.issubdtype(arr.dtype, np.floating)
+                                       or np.issubdtype(arr.dtype, np.integer)
+                                       or arr.dtype == np.bool_):
+            raise ValidationError(f"{name} must be a numeric array, got dtype {arr.dtype}")
+        x = torch.from_numpy(np.ascontiguousarray(arr))
+    return x.to(torch.device("cuda", torch.cuda.current_device()))
+
+
+def check_finite(name: str, *xs: torch.Tensor) -> None:
+    """ValidationError on NaN / Inf entries, as the reference's as_matrix (linalg.py:15-24)."""
+    for x in xs:
+        if not bool(torch.isfinite(x).all()):
+            raise ValidationError(f"{name} contains NaN or Inf entries")
+
+
+def as_bhnd(x, name: str, n: int | None = None, d: int | None = None, stage: bool = False):
+    """Return (x as contiguous bf16 [B, H, N, d], original leading shape). ``stage``: accept
+    array-likes / host tensors and copy them to the current CUDA device."""
+    if stage:
+        x = to_device(x, name)
     require_cuda(x, name)
     if x.ndim not in (2, 3, 4):
         raise ValidationError(f"{name} must be (n, d), (heads, n, d) or (batch, heads, n, d), "

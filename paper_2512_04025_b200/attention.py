@@ -15,7 +15,7 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from ._tensors import as_bhnd, restore, stream_handle
+from ._tensors import as_bhnd, check_finite, restore, stream_handle, to_device
 from .errors import ValidationError
 from .layout import BlockLayout, make_layout
 from .mask import MaskPlan, causal_premask, plan_from_mask
@@ -123,7 +123,9 @@ def psa_streaming(q, pyramid: PyramidKV, mask, causal: bool = False) -> Attentio
     """
     lay = pyramid.layout
     lay.check_gpu()
-    q4, lead = as_bhnd(q, "Q", lay.seq_len, lay.head_dim)
+    q4, lead = as_bhnd(q, "Q", lay.seq_len, lay.head_dim, stage=True)
+    check_finite("Q", q4)
+    mask = to_device(mask, "mask")
     B, Hq = q4.shape[:2]
     if tuple(mask.shape[-2:]) != (lay.n_q, lay.n_k) or mask.numel() != B * Hq * lay.n_q * lay.n_k:
         raise ValidationError(f"mask shape {tuple(mask.shape)} does not match layout "
@@ -149,9 +151,10 @@ def _dense_layout(n: int, d: int) -> BlockLayout:
 
 
 def _dense(q, k, v, causal: bool) -> AttentionOutput:
-    q4, lead = as_bhnd(q, "Q")
-    k4, _ = as_bhnd(k, "K", q4.shape[2], q4.shape[3])
-    v4, _ = as_bhnd(v, "V", q4.shape[2], q4.shape[3])
+    q4, lead = as_bhnd(q, "Q", stage=True)
+    k4, _ = as_bhnd(k, "K", q4.shape[2], q4.shape[3], stage=True)
+    v4, _ = as_bhnd(v, "V", q4.shape[2], q4.shape[3], stage=True)
+    check_finite("Q / K / V", q4, k4, v4)
     if k4.shape != v4.shape:
         raise ValidationError(f"incompatible shapes K{tuple(k4.shape)} V{tuple(v4.shape)}")
     lay = _dense_layout(q4.shape[2], q4.shape[3])

@@ -16,7 +16,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._tensors import as_bhnd, stream_handle
+from ._tensors import as_bhnd, check_finite, stream_handle
 from .errors import ValidationError
 from .layout import BlockLayout, SamplerConfig
 
@@ -107,8 +107,9 @@ def importance_sampled(q, k, layout: BlockLayout, cfg: SamplerConfig,
     Shape (n_q, n_k) for (n, d) inputs, else [..., n_q, n_k] following q's leading dims.
     """
     layout.check_gpu()
-    q4, lead = as_bhnd(q, "Q", layout.seq_len, layout.head_dim)
-    k4, _ = as_bhnd(k, "K", layout.seq_len, layout.head_dim)
+    q4, lead = as_bhnd(q, "Q", layout.seq_len, layout.head_dim, stage=True)
+    k4, _ = as_bhnd(k, "K", layout.seq_len, layout.head_dim, stage=True)
+    check_finite("Q / K", q4, k4)
     s = importance_scores(q4, k4, layout, cfg, reducer)
     return s.reshape(lead + (layout.n_q, layout.n_k))
 
@@ -160,7 +161,8 @@ def importance_antidiagonal(q, k, layout: BlockLayout, stride: int) -> torch.Ten
     Shape (n_q, n_k) for (n, d) inputs, else [..., n_q, n_k] following q's leading dims.
     """
     layout.check_gpu()
-    q4, lead = as_bhnd(q, "Q", layout.seq_len, layout.head_dim)
-    k4, _ = as_bhnd(k, "K", layout.seq_len, layout.head_dim)
+    q4, lead = as_bhnd(q, "Q", layout.seq_len, layout.head_dim, stage=True)
+    k4, _ = as_bhnd(k, "K", layout.seq_len, layout.head_dim, stage=True)
+    check_finite("Q / K", q4, k4)
     s = antidiagonal_scores(q4, k4, layout, stride)
     return s.reshape(lead + (layout.n_q, layout.n_k))

@@ -16,7 +16,7 @@ from fractions import Fraction
 import torch
 
 from . import _lib
-from ._tensors import require_cuda, stream_handle
+from ._tensors import require_cuda, stream_handle, to_device
 from .errors import ValidationError
 from .layout import BlockLayout, LevelThresholds, QuantileCutpoints
 
@@ -110,7 +110,7 @@ def plan_from_mask(mask: torch.Tensor, layout: BlockLayout, causal: bool,
 
 
 def _check_scores(scores) -> tuple:
-    require_cuda(scores, "importance scores")
+    scores = to_device(scores, "importance scores")
     if scores.ndim < 2 or scores.numel() == 0:
         raise ValidationError("importance scores must be a non-empty matrix")
     s = scores.to(torch.float64)
@@ -148,8 +148,8 @@ def assign_quantile(scores, cutpoints: QuantileCutpoints) -> torch.Tensor:
 
 def combine_mask(mask, caps) -> torch.Tensor:
     """min(M, caps[j]) with zeros kept (mask.py:237-247). Elementwise on the device."""
-    require_cuda(mask, "mask")
-    require_cuda(caps, "caps")
+    mask = to_device(mask, "mask")
+    caps = to_device(caps, "caps")
     m = mask.to(torch.int64)
     c = caps.to(torch.int64)
     if m.ndim < 2 or c.ndim < 1 or m.shape[-1] != c.shape[-1]:
@@ -161,7 +161,7 @@ def combine_mask(mask, caps) -> torch.Tensor:
 
 def causal_premask(mask, layout: BlockLayout) -> torch.Tensor:
     """Causal pre-pass (mask.py:324-349): future -> 0, straddling -> 1, visible -> keep."""
-    require_cuda(mask, "mask")
+    mask = to_device(mask, "mask")
     m = mask.to(torch.int64)
     if tuple(m.shape[-2:]) != (layout.n_q, layout.n_k):
         raise ValidationError(f"mask shape {tuple(m.shape)} does not match layout "
@@ -212,7 +212,7 @@ def report_from_counts(level_counts, total: int) -> SparsityReport:
 
 def sparsity_report(mask, levels: int | None = None) -> SparsityReport:
     """Budget, sparsity and coverage of a level map (mask.py:303-321)."""
-    m = mask.to(torch.int64) if isinstance(mask, torch.Tensor) else torch.as_tensor(mask)
+    m = (to_device(mask, "mask") if torch.cuda.is_available() else torch.as_tensor(mask)).to(torch.int64)
     if m.ndim < 2 or m.numel() == 0:
         raise ValidationError("mask must be a non-empty 2D integer array")
     if bool((m < 0).any()):

@@ -129,6 +129,7 @@ class PSAResult:
     skipped: torch.Tensor        # device int32 counter of rows with no key
     scores: torch.Tensor | None  # fp64 importance (kept when requested)
     pyramid: PyramidKV | None
+    nonfinite: torch.Tensor | None = None  # device int32 [1]: Q/K/V held NaN/Inf (check_finite)
 
     @property
     def level_map(self) -> torch.Tensor:
@@ -167,7 +168,7 @@ def _mask_rule(cfg: RunConfig, levels: int):
 
 def psa_forward_4d(q4, k4, v4, cfg: RunConfig, keep_scores: bool = False,
                    out: torch.Tensor | None = None, lse: torch.Tensor | None = None,
-                   qblocks=None) -> PSAResult:
+                   qblocks=None, check_finite: bool = False) -> PSAResult:
     """Fused PSA forward on contiguous bf16 [B, H, N, d] device tensors (``out``/``lse``:
     optional preallocated device outputs). ``qblocks``: run only these query blocks of every
     head (a (b, h, q-block set) work unit of parallel.py); importance rows, level map, plan, O
@@ -178,15 +179,20 @@ def psa_forward_4d(q4, k4, v4, cfg: RunConfig, keep_scores: bool = False,
     if blk is not None and cfg.grid is not None:
         raise ValidationError("query-block subsets are not supported with grid permutations")
     perm = order = None
+    bad = None
+    if check_finite:  # linalg.py:15-24 (as_matrix): device flag, raised by the caller after a sync
+        bad = (~torch.isfinite(q4)).any().to(torch.int32).reshape(1)
     if cfg.grid is not None:  # pipeline.py:257-263: curve order applied to Q, K and V
         perm = _stage("permutation", hilbert_order, cfg.grid)
         order, _ = perm.on(q4.device)
         q4 = gather_rows(q4, order)
         # K/V: the gather is fused into the pyramid kernel's loads (level 1 = permuted K/V)
+        if bad is not None:
+            bad |= ((~torch.isfinite(k4)).any() | (~torch.isfinite(v4)).any()).to(torch.int32)
         pyr = _stage("pyramid", build_pyramid_gather, k4, v4, lay, order)
         k4, v4 = pyr.k_raw, pyr.v_raw
     else:
-        pyr = _stage("pyramid", build_pyramid, k4, v4, lay)
+        pyr = _stage("pyramid", build_pyramid, k4, v4, lay, flag=bad)
     mode, rule = _mask_rule(cfg, lay.levels)
     B, Hq = q4.shape[:2]
     Hkv = k4.shape[1]
@@ -208,7 +214,7 @@ def psa_forward_4d(q4, k4, v4, cfg: RunConfig, keep_scores: bool = False,
     out, lse, skipped = _stage("executor", attention_forward, q4, pyr, plan, cfg.causal, out, lse,
                                None, scatter, blk)
     return PSAResult(out=out, lse=lse, plan=plan, skipped=skipped,
-                     scores=scores if keep_scores else None, pyramid=pyr)
+                     scores=scores if keep_scores else None, pyramid=pyr, nonfinite=bad)
 
 
 def resolve_config(cfg: RunConfig | None, n: int, d: int, overrides: dict) -> RunConfig:
@@ -225,7 +231,7 @@ def resolve_config(cfg: RunConfig | None, n: int, d: int, overrides: dict) -> Ru
 
 
 def psa_attention(q, k, v, cfg: RunConfig | None = None, *, keep_scores: bool = False,
-                  qblocks=None, **overrides) -> PSAResult:
+                  qblocks=None, check_finite: bool = True, **overrides) -> PSAResult:
     """Pyramid sparse attention forward.
 
     ``q``: (n, d), (Hq, n, d) or (B, Hq, n, d); ``k``/``v``: same with Hkv heads (Hq % Hkv == 0).
@@ -237,12 +243,19 @@ def psa_attention(q, k, v, cfg: RunConfig | None = None, *, keep_scores: bool = 
     three overlapped streams, and the result lives in host memory (the reference's
     arrays-in/arrays-out contract); the compute is the same sm_100a path, never a CPU one.
     ``qblocks``: only these query blocks of every head (a work unit of parallel.partition); the
-    outputs then hold those blocks' rows (compact).
+    outputs then hold those blocks' rows (compact). ``check_finite``: NaN/Inf in Q, K or V
+    raise ValidationError like the reference's as_matrix (linalg.py:15-24); the K/V test rides in
+    the pyramid kernel's loads, the Q test is one reduction, both read after the forward (one
+    host sync per call).
     """
+    if not isinstance(q, torch.Tensor):  # array-likes (as_matrix, linalg.py:15-24): host tensors
+        import numpy as np
+        q, k, v = (torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.float32)))
+                   for x in (q, k, v))
     if isinstance(q, torch.Tensor) and not q.is_cuda:
         from .staging import psa_attention_staged  # host tensors: pipelined staging onto the GPU
         return psa_attention_staged(q, k, v, cfg, keep_scores=keep_scores, qblocks=qblocks,
-                                    **overrides)
+                                    check_finite=check_finite, **overrides)
     q4, lead = as_bhnd(q, "Q")
     k4, _ = as_bhnd(k, "K", q4.shape[2], q4.shape[3])
     v4, _ = as_bhnd(v, "V", q4.shape[2], q4.shape[3])
@@ -250,7 +263,10 @@ def psa_attention(q, k, v, cfg: RunConfig | None = None, *, keep_scores: bool = 
         raise ValidationError(f"Q/K/V shapes differ: {tuple(q4.shape)}/{tuple(k4.shape)}/"
                               f"{tuple(v4.shape)}")
     cfg = resolve_config(cfg, q4.shape[2], q4.shape[3], overrides)
-    res = psa_forward_4d(q4, k4, v4, cfg, keep_scores=keep_scores, qblocks=qblocks)
+    res = psa_forward_4d(q4, k4, v4, cfg, keep_scores=keep_scores, qblocks=qblocks,
+                         check_finite=check_finite)
+    if res.nonfinite is not None and int(res.nonfinite.item()):
+        raise ValidationError("[stage: input] Q, K or V contains NaN or Inf entries")
     rows = res.out.shape[2]
     res.out = res.out.reshape(lead + (rows, q4.shape[3]))
     res.lse = res.lse.reshape(lead + (rows,))

@@ -71,7 +71,7 @@ class PyramidKV:
 
 
 def build_pyramid(k: torch.Tensor, v: torch.Tensor, layout: BlockLayout,
-                  check_finite: bool = False) -> PyramidKV:
+                  check_finite: bool = False, flag: torch.Tensor | None = None) -> PyramidKV:
     """Split K/V into KV blocks and pool each ``layout.levels`` deep (blocks.py:93-109).
 
     Levels are fp64 dyadic means of the bf16 inputs rounded once to bf16, i.e. exactly
@@ -79,8 +79,8 @@ def build_pyramid(k: torch.Tensor, v: torch.Tensor, layout: BlockLayout,
     raises ValidationError like the reference's as_matrix (costs one host sync).
     """
     layout.check_gpu()
-    k4, _ = as_bhnd(k, "K", layout.seq_len, layout.head_dim)
-    v4, _ = as_bhnd(v, "V", layout.seq_len, layout.head_dim)
+    k4, _ = as_bhnd(k, "K", layout.seq_len, layout.head_dim, stage=True)
+    v4, _ = as_bhnd(v, "V", layout.seq_len, layout.head_dim, stage=True)
     if k4.shape != v4.shape:
         raise ValidationError(f"K/V shapes {tuple(k4.shape)}/{tuple(v4.shape)} differ")
     B, H, n, d = k4.shape
@@ -90,7 +90,9 @@ def build_pyramid(k: torch.Tensor, v: torch.Tensor, layout: BlockLayout,
     total = pyramid_elems(B * H, n, d, layout.levels)
     kp = torch.empty(total, dtype=torch.bfloat16, device=dev)
     vp = torch.empty(total, dtype=torch.bfloat16, device=dev)
-    flag = torch.zeros(1, dtype=torch.int32, device=dev) if check_finite else None
+    # ``flag`` (device int32 [1]): set when K or V holds NaN/Inf, without a host sync
+    if check_finite and flag is None:
+        flag = torch.zeros(1, dtype=torch.int32, device=dev)
     lib = _lib.load()
     rc = lib.psa_pyramid_build(k4.data_ptr(), v4.data_ptr(), B * H, n, d, layout.k_block,
                                layout.levels, kp.data_ptr(), vp.data_ptr(), _lib.ptr(flag),
@@ -154,7 +156,7 @@ def level_cap_from_similarity(source, sim_thresholds: SimThresholds,
     else:
         if layout is None:
             raise ValidationError("raw key input requires an explicit layout")
-        k4, lead = as_bhnd(source, "K", layout.seq_len, layout.head_dim)
+        k4, lead = as_bhnd(source, "K", layout.seq_len, layout.head_dim, stage=True)
     layout.check_gpu()
     caps = similarity_caps(k4, layout, sim_thresholds)
     return caps.to(torch.int64).reshape(lead + (layout.n_k,))

@@ -72,7 +72,7 @@ def _group_sizes(n: int) -> list:
 def psa_attention_staged(q, k, v, cfg=None, *, device=None, kv_heads_per_group: int | None = None,
                          out: torch.Tensor | None = None, lse: torch.Tensor | None = None,
                          keep_level_map: bool = False, keep_scores: bool = False,
-                         qblocks=None, **overrides) -> StagedResult:
+                         qblocks=None, check_finite: bool = True, **overrides) -> StagedResult:
     """PSA forward of host tensors on ``device`` (default: the current CUDA device).
 
     ``out`` / ``lse``: optional preallocated (ideally pinned) host outputs of shapes
@@ -143,6 +143,7 @@ def psa_attention_staged(q, k, v, cfg=None, *, device=None, kv_heads_per_group: 
             })
         counts = torch.zeros(lay.levels + 1, dtype=torch.int64, device=dev)
         skipped = torch.zeros(1, dtype=torch.int64, device=dev)
+        bad = torch.zeros(1, dtype=torch.int64, device=dev)
         for gi, (b, h0, h1) in enumerate(groups):
             sl = slots[gi % len(slots)]
             nk, nq = h1 - h0, (h1 - h0) * group
@@ -159,9 +160,12 @@ def psa_attention_staged(q, k, v, cfg=None, *, device=None, kv_heads_per_group: 
             s_cmp.wait_event(ready)
             if sl["free_out"] is not None:
                 s_cmp.wait_event(sl["free_out"])
-            res = psa_forward_4d(qs, ks, vs, cfg, out=os_, lse=ls, qblocks=qblocks)
+            res = psa_forward_4d(qs, ks, vs, cfg, out=os_, lse=ls, qblocks=qblocks,
+                                 check_finite=check_finite)
             counts += res.plan.level_counts
             skipped += res.skipped
+            if res.nonfinite is not None:
+                bad += res.nonfinite
             done = torch.cuda.Event()
             done.record(s_cmp)
             sl["free_in"] = done
@@ -177,7 +181,10 @@ def psa_attention_staged(q, k, v, cfg=None, *, device=None, kv_heads_per_group: 
                 sl["free_out"] = freed
         cur.wait_stream(s_out)
         s_out.synchronize()
-        tail = torch.cat([counts, skipped]).cpu().tolist()
+        tail = torch.cat([counts, skipped, bad]).cpu().tolist()
+    if tail[-1]:
+        raise ValidationError("[stage: input] Q, K or V contains NaN or Inf entries")
+    tail = tail[:-1]
     return StagedResult(out=out4.reshape(lead + (rows, d)),
                         lse=lse3.reshape(lead + (rows,)), level_counts=[int(c) for c in tail[:-1]],
                         skipped=int(tail[-1]), level_map=lmap)
