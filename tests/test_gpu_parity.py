@@ -249,8 +249,11 @@ def test_mask_validation():
         psa.psa_streaming(q, pyr, torch.full((4, 4), 3, device="cuda"))
     with pytest.raises(psa.ValidationError):  # pooled level on a straddling pair
         psa.psa_streaming(q, pyr, torch.full((4, 4), 2, device="cuda"), causal=True)
-    with pytest.raises(psa.ValidationError):
-        psa.psa_streaming(q.cpu(), pyr, torch.ones(4, 4, device="cuda"))
+    # host Q is staged onto the device like any array-like (linalg.py:15-24), same result
+    m1 = torch.ones(4, 4, device="cuda", dtype=torch.int64)
+    assert torch.equal(psa.psa_streaming(q.cpu(), pyr, m1).out, psa.psa_streaming(q, pyr, m1).out)
+    with pytest.raises(psa.ValidationError):  # non-numeric input
+        psa.psa_streaming([["a"] * 64] * 256, pyr, m1)
 
 
 # ------------------------------------------------------------------ fused pipeline
