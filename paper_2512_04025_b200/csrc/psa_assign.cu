@@ -263,7 +263,50 @@ __global__ void __launch_bounds__(128) assign_levels_kernel(
     for (int t = threadIdx.x; t < p.n_k; t += blockDim.x)
       keys[t] = tot > 0.0 ? __ddiv_rn(keys[t], tot) : uni;
     __syncthreads();
-    if (threadIdx.x == 0) {
+    // Fast path: fp64 prefix sums in parallel (blocked: thread t owns positions [t*IPT, t*IPT +
+    // IPT)); they differ from the reference's sequential Neumaier sums by ~1e-15 at most (n_k <=
+    // 4096 non-negative terms summing to 1), so the comparisons cum <= tau agree whenever no sum
+    // lies within 1e-12 of a threshold. Otherwise (probability ~1e-8 per row) the row falls back
+    // to the exact sequential recurrence below.
+    {
+      double loc[IPT];
+      double run = 0.0;
+#pragma unroll
+      for (int e = 0; e < IPT; ++e) {
+        const int t = threadIdx.x * IPT + e;
+        run = __dadd_rn(run, t < p.n_k ? keys[t] : 0.0);
+        loc[e] = run;
+      }
+      double excl = run;  // inclusive scan of the thread totals, then shifted
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, excl, o);
+        if (lane >= o) excl = __dadd_rn(excl, y);
+      }
+      __shared__ double warp_sum[4];
+      if (lane == 31) warp_sum[warp] = excl;
+      __syncthreads();
+      double wbase = 0.0;
+      for (int w = 0; w < warp; ++w) wbase = __dadd_rn(wbase, warp_sum[w]);
+      excl = __dadd_rn(__dsub_rn(excl, run), wbase);
+      bool fragile = false;
+#pragma unroll
+      for (int e = 0; e < IPT; ++e) {
+        const int t = threadIdx.x * IPT + e;
+        loc[e] = fmin(__dadd_rn(excl, loc[e]), 1.0);
+        if (t < p.n_k)
+          for (int c = 0; c < p.rule.n_cuts; ++c)
+            fragile |= fabs(loc[e] - p.rule.taus[c]) <= 1e-12;
+      }
+      fragile = __syncthreads_or(fragile) != 0;
+      if (!fragile) {
+#pragma unroll
+        for (int e = 0; e < IPT; ++e) {
+          const int t = threadIdx.x * IPT + e;
+          if (t < p.n_k) keys[t] = loc[e];
+        }
+      } else if (threadIdx.x == 0) {
       // The recurrence is inherently sequential; keep only it on one thread and store
       // cum_t in place of e_t (read just before it is overwritten).
       // t = 0: total = 0 < x (the else branch of Neumaier's |total| >= |x| test); for t >= 1 the
@@ -278,6 +321,7 @@ __global__ void __launch_bounds__(128) assign_levels_kernel(
         comp = __dadd_rn(comp, __dadd_rn(__dsub_rn(total, tt), x));
         total = tt;
         keys[t] = fmin(__dadd_rn(total, comp), 1.0);
+      }
       }
     }
     __syncthreads();

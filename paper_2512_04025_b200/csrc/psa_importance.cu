@@ -230,6 +230,11 @@ __global__ void __launch_bounds__(kImpThreads, 2)
 
 // S_ij = max_a exp(fl(M_aj / sqrt(d)) - m_a) / l_a, M_aj = raw block-max dot
 // (or mean: sum_a M_aj / (s_q*s_k))
+// MAX: the candidates are ranked by y_a = M_aj / sqrt(d) - (m_a + ln l_a) (one multiply and one
+// subtraction each; |error| << 1e-12); only those within 1e-9 of the best are evaluated exactly
+// as fl(fl(exp(fl(fl(M_aj / sqrt(d)) - m_a))) / l_a), the reference's arithmetic (softmax,
+// linalg.py:38-43, then the block max), so S is the same value as evaluating every candidate
+// (exp and division are monotone) with ~1 exp and 2 divisions per (i, j) instead of s_q.
 template <bool MEAN>
 __global__ void __launch_bounds__(128) importance_finalize_kernel(
     const double* __restrict__ M, const double* __restrict__ mstat,
@@ -237,6 +242,33 @@ __global__ void __launch_bounds__(128) importance_finalize_kernel(
     double* __restrict__ S) {
   const int i = blockIdx.x;
   const int64_t bhq = blockIdx.y;
+  constexpr int kMaxSq = 64;
+  __shared__ double nl[kMaxSq];
+  if (!MEAN && s_q <= kMaxSq) {
+    for (int t = threadIdx.x; t < s_q; t += blockDim.x) {
+      const int64_t a = bhq * R + static_cast<int64_t>(i) * s_q + t;
+      nl[t] = mstat[a] + log(lstat[a]);
+    }
+    __syncthreads();
+    const double inv = 1.0 / sqrt_d;
+    for (int j = threadIdx.x; j < n_k; j += blockDim.x) {
+      double ybest = -INFINITY;
+      for (int t = 0; t < s_q; ++t) {
+        const int64_t a = bhq * R + static_cast<int64_t>(i) * s_q + t;
+        ybest = fmax(ybest, M[a * n_k + j] * inv - nl[t]);
+      }
+      double acc = -INFINITY;
+      for (int t = 0; t < s_q; ++t) {
+        const int64_t a = bhq * R + static_cast<int64_t>(i) * s_q + t;
+        const double mv = M[a * n_k + j];
+        if (!(mv * inv - nl[t] >= ybest - 1e-9)) continue;
+        const double logit = __ddiv_rn(mv, sqrt_d);  // importance.py:80
+        acc = fmax(acc, __ddiv_rn(exp(__dsub_rn(logit, mstat[a])), lstat[a]));
+      }
+      S[(bhq * n_q + i) * n_k + j] = acc;
+    }
+    return;
+  }
   for (int j = threadIdx.x; j < n_k; j += blockDim.x) {
     double acc = MEAN ? 0.0 : -INFINITY;
     for (int t = 0; t < s_q; ++t) {
