@@ -747,6 +747,8 @@ def main_sweep(args, cfg, rank, world, device, red_dev):
         return psa.RunConfig.from_dict(d)
 
     rows = []
+    clk = ClockSampler(device.index)
+    clk.__enter__()
     for beta in (0.1, 0.2, 0.3, 0.4, 0.5):
         entry = {"budget": beta}
         for name, rc in (("psa", base_cfg(mask="quantile",
@@ -767,7 +769,15 @@ def main_sweep(args, cfg, rank, world, device, red_dev):
         rows.append(entry)
     dense_flops = 4.0 * cfg["N"] * cfg["N"] * cfg["d"] * cfg["B"] * cfg["Hq"]
     full_ms = timed(lambda: psa.full_attention(q, k, v))
-    sdpa_ms = timed(lambda: torch.nn.functional.scaled_dot_product_attention(q, k, v))
+    from torch.nn.attention import SDPBackend, sdpa_kernel
+    sdpa_backend = "default"
+    try:
+        with sdpa_kernel([SDPBackend.CUDNN_ATTENTION]):
+            sdpa_ms = timed(lambda: torch.nn.functional.scaled_dot_product_attention(q, k, v))
+        sdpa_backend = "cudnn"
+    except Exception:  # noqa: BLE001
+        sdpa_ms = timed(lambda: torch.nn.functional.scaled_dot_product_attention(q, k, v))
+    clk.__exit__(None, None, None)
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -787,8 +797,9 @@ def main_sweep(args, cfg, rank, world, device, red_dev):
         "dense": {"tflop": dense_flops / 1e12,
                   "psa_kernel_all_level1_ms": round(full_ms, 4),
                   "psa_kernel_all_level1_tflops": round(dense_flops / (full_ms * 1e-3) / 1e12, 2),
-                  "torch_sdpa_ms": round(sdpa_ms, 4),
+                  "torch_sdpa_ms": round(sdpa_ms, 4), "torch_sdpa_backend": sdpa_backend,
                   "torch_sdpa_tflops": round(dense_flops / (sdpa_ms * 1e-3) / 1e12, 2)},
+        "clocks": clk.summary(),
         "gpu_launches": None,
     }
     print(json.dumps(line), flush=True)
