@@ -73,13 +73,21 @@ def main(tag: str) -> None:
         rows = list(csv.reader(io.StringIO(body)))
         hdr = rows[0]
         ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+        mi = hdr.index("Metric Name")
         agg = collections.OrderedDict()
+        byt = collections.defaultdict(float)
         for r in rows[1:]:
             name = r[ki].split("(")[0].replace("void ", "")
-            agg.setdefault(name, []).append(float(r[vi].replace(",", "")) * SCALE.get(r[ui], 1e-9))
+            val = float(r[vi].replace(",", "")) * SCALE.get(r[ui], 1e-9)
+            if r[mi] == "gpu__time_duration.sum":
+                agg.setdefault(name, []).append(val)
+            elif r[mi].startswith("dram__bytes"):
+                byt[name] += float(r[vi].replace(",", "")) * SCALE.get(r[ui], 1)
         total = sum(sum(v) for v in agg.values())
         summ = {k: {"launches": len(v), "mean_ms": 1e3 * sum(v) / len(v),
-                    "share_of_listed": sum(v) / total} for k, v in agg.items()}
+                    "share_of_listed": sum(v) / total,
+                    "dram_gb_per_launch": byt[k] / len(v) / 1e9 if byt else None}
+                for k, v in agg.items()}
         (PROF / f"{tag}_launch_summary.json").write_text(json.dumps(summ, indent=1) + "\n")
         print(json.dumps(summ, indent=1))
     for rep in sorted(OUT.glob("*_full.ncu-rep")):
