@@ -251,20 +251,28 @@ __global__ void __launch_bounds__(128) importance_finalize_kernel(
     }
     __syncthreads();
     const double inv = 1.0 / sqrt_d;
+    const double* Mi = M + (bhq * R + static_cast<int64_t>(i) * s_q) * n_k;
     for (int j = threadIdx.x; j < n_k; j += blockDim.x) {
+      constexpr int kReg = 8;  // the s_q <= 8 candidates in registers (all loads in flight)
+      double mv[kReg];
+#pragma unroll
+      for (int t = 0; t < kReg; ++t) mv[t] = t < s_q ? Mi[static_cast<int64_t>(t) * n_k + j] : 0.0;
       double ybest = -INFINITY;
-      for (int t = 0; t < s_q; ++t) {
-        const int64_t a = bhq * R + static_cast<int64_t>(i) * s_q + t;
-        ybest = fmax(ybest, M[a * n_k + j] * inv - nl[t]);
-      }
+#pragma unroll
+      for (int t = 0; t < kReg; ++t)
+        if (t < s_q) ybest = fmax(ybest, mv[t] * inv - nl[t]);
+      for (int t = kReg; t < s_q; ++t) ybest = fmax(ybest, Mi[static_cast<int64_t>(t) * n_k + j] * inv - nl[t]);
       double acc = -INFINITY;
-      for (int t = 0; t < s_q; ++t) {
+      auto cand = [&](int t, double m_) {
+        if (!(m_ * inv - nl[t] >= ybest - 1e-9)) return;
         const int64_t a = bhq * R + static_cast<int64_t>(i) * s_q + t;
-        const double mv = M[a * n_k + j];
-        if (!(mv * inv - nl[t] >= ybest - 1e-9)) continue;
-        const double logit = __ddiv_rn(mv, sqrt_d);  // importance.py:80
+        const double logit = __ddiv_rn(m_, sqrt_d);  // importance.py:80
         acc = fmax(acc, __ddiv_rn(exp(__dsub_rn(logit, mstat[a])), lstat[a]));
-      }
+      };
+#pragma unroll
+      for (int t = 0; t < kReg; ++t)
+        if (t < s_q) cand(t, mv[t]);
+      for (int t = kReg; t < s_q; ++t) cand(t, Mi[static_cast<int64_t>(t) * n_k + j]);
       S[(bhq * n_q + i) * n_k + j] = acc;
     }
     return;

@@ -329,8 +329,10 @@ PSA_DEV double exp_nonpos_slow(double t, const double* tab) {
   const int ea = e >> 1;
   return __dmul_rn(__dmul_rn(__fma_rn(tj, q, tj), pow2(ea)), pow2(e - ea));
 }
-// exp(m_old - m_new) for the running-sum rescale; 0 before the first tile (m_old = -inf)
+// exp(m_old - m_new) for the running-sum rescale; 0 before the first tile (m_old = -inf), and
+// exactly 1 without the exp when the max did not move (most tiles after the first few)
 PSA_DEV double rescale(double m_old, double m_new, const double* tab) {
+  if (m_old == m_new) return 1.0;
   return m_old == -INFINITY ? 0.0 : exp_nonpos_slow(__dsub_rn(m_old, m_new), tab);
 }
 // value of x on row grid E (the part the int8 slices carry exactly)
