@@ -122,10 +122,6 @@ struct PlanCursor {
 // softmax warpgroups 216 (128*64 + 256*216 <= 384*168, else the increase never completes).
 constexpr int kPPThreads = 384;
 
-template <uint32_t N>
-PSA_DEV void regs_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N)); }
-template <uint32_t N>
-PSA_DEV void regs_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N)); }
 
 template <int D>
 struct PP2Cfg {

@@ -50,7 +50,19 @@ constexpr int kXlHalf = 16;         // keys per epilogue group and tile (half an
 constexpr int kXlGroups = 4;        // epilogue warpgroups: (accumulator buffer, half) pairs
 constexpr int kXlEpiThreads = kXlGroups * 128;
 constexpr int kXlThreads = 128 + kXlEpiThreads;
-constexpr int kXlGridShift = 27;  // X = x * 2^(27 - E), |X| < 2^28
+constexpr int kXlGridShift = 27;
+
+#ifndef PSA_XL_REGS_EPI
+#define PSA_XL_REGS_EPI 112
+#endif
+// setmaxnreg redistributes the CTA's own pool (640 threads x 96 at launch): the increase only
+// completes if 128 x producer + 512 x epilogue fits in it
+#ifndef PSA_XL_REGS_PROD
+#define PSA_XL_REGS_PROD 32
+#endif
+constexpr int kXlRegsProducer = PSA_XL_REGS_PROD, kXlRegsEpilogue = PSA_XL_REGS_EPI;
+static_assert(128 * kXlRegsProducer + kXlEpiThreads * kXlRegsEpilogue <= (128 + kXlEpiThreads) * 96,
+              "register pool");  // X = x * 2^(27 - E), |X| < 2^28
 
 struct XlMeta {
   int32_t e;      // row exponent E (0 for an all-zero row)
@@ -270,9 +282,37 @@ PSA_DEV double i32_to_f64(int x) {
   return __dsub_rn(__hiloint2double(0x43380000, x ^ static_cast<int>(0x80000000u)),
                    6755401588539392.0);  // 1.5 * 2^52 + 2^31
 }
-// exact int64 -> fp64 for |v| < 2^51
-PSA_DEV double i64_to_f64_exact(long long v) {
-  return __dsub_rn(__longlong_as_double(v + 0x4338000000000000LL), 6755399441055744.0);
+// 64-bit a * b + c with a sign-extended 32-bit a
+PSA_DEV long long mad_wide(int a, int b, long long c) {
+  long long d;
+  asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
+  return d;
+}
+// The exact dot from the 7 class sums c_k (weight 2^(7k), |c_k| < 2^23), rounded once.
+//   lo = c0 + c1 2^7 + c2 2^14 + c3 2^21  (|lo| < 2^45),  hi = c4 + c5 2^7 + c6 2^14  (< 2^38)
+// Default: four exact int32 -> fp64 conversions and three fmas (the partial sums below 2^53 are
+// exact, the last fma rounds). kWide: lo and hi are built with integer
+// multiply-adds directly as the bit patterns of 1.5 * 2^52 + lo / hi (doubles with ulp 1), and
+// fma(hi - 1.5 * 2^24, 2^28, 1.5 * 2^52 + lo) = hi * 2^28 + lo (2 FP64 ops instead of 7, more
+// integer work: A/B at cfg4 17.2 vs 17.75 ms, at cfg3 5.90 vs 5.77 ms, so only the antidiagonal
+// estimator uses it).
+template <bool kWide>
+PSA_DEV double class_dot(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t c4,
+                         uint32_t c5, uint32_t c6) {
+  const int a = static_cast<int>(c0) + (static_cast<int>(c1) << 7);
+  const int b = static_cast<int>(c2) + (static_cast<int>(c3) << 7);
+  const int h = static_cast<int>(c4) + (static_cast<int>(c5) << 7);
+  if constexpr (kWide) {
+    constexpr long long kMagic = 0x4338000000000000LL;  // 1.5 * 2^52
+    const long long lo_bits = mad_wide(b, 16384, mad_wide(a, 1, kMagic));
+    const long long hi_bits = mad_wide(static_cast<int>(c6), 16384, mad_wide(h, 1, kMagic));
+    const double hi_off = __dsub_rn(__longlong_as_double(hi_bits), 6755399466221568.0);  // 1.5*(2^52+2^24)
+    return __fma_rn(hi_off, 268435456.0, __longlong_as_double(lo_bits));
+  } else {
+    const double lo = __fma_rn(i32_to_f64(b), 16384.0, i32_to_f64(a));
+    const double hi = __fma_rn(i32_to_f64(static_cast<int>(c6)), 16384.0, i32_to_f64(h));
+    return __fma_rn(hi, 268435456.0, lo);
+  }
 }
 // 2^(j/64), j = 0..63, correctly rounded (host-computed)
 __constant__ double kExp2Tab[64] = {1.0, 1.0108892860517005, 1.0218971486541166, 1.0330248790212284, 1.0442737824274138, 1.0556451783605572, 1.0671404006768237, 1.0787607977571199, 1.0905077326652577, 1.102382583307841, 1.1143867425958924, 1.1265216186082418, 1.1387886347566916, 1.1511892299529827, 1.1637248587775775, 1.1763969916502812, 1.189207115002721, 1.202156731452703, 1.215247359980469, 1.22848053610687, 1.241857812073484, 1.255380757024691, 1.2690509571917332, 1.2828700160787783, 1.2968395546510096, 1.3109612115247644, 1.3252366431597413, 1.339667524053303, 1.3542555469368927, 1.3690024229745905, 1.383909881963832, 1.3989796725383112, 1.4142135623730951, 1.42961333839197, 1.4451808069770467, 1.460917794180647, 1.4768261459394993, 1.4929077282912648, 1.5091644275934228, 1.5255981507445384, 1.5422108254079407, 1.559004400237837, 1.5759808451078865, 1.593142151342267, 1.6104903319492543, 1.6280274218573478, 1.645755478153965, 1.6636765803267364, 1.681792830507429, 1.7001063537185235, 1.718619298122478, 1.7373338352737062, 1.7562521603732995, 1.7753764925265212, 1.7947090750031072, 1.8142521755003989, 1.8340080864093424, 1.8539791250833855, 1.8741676341103, 1.8945759815869656, 1.9152065613971474, 1.9360617934922943, 1.9571441241754002, 1.978456026387951};
@@ -422,6 +462,10 @@ __global__ void __launch_bounds__(kXlThreads, 1)
   __syncthreads();
   tc_fence_after();
 
+  if (warp < 4) {
+    // producer warpgroup (TMA, MMA, TMEM allocator, idle): few registers, so the epilogue
+    // warpgroups get 112 (128 x 32 + 512 x 112 = 640 x 96) instead of the launch's 96
+    if constexpr (kXlRegsEpilogue > 96) regs_dec<kXlRegsProducer>();
   if (warp == 0) {
     if (lane == 0) {
       const int qset = (bhq * p.classes + cls) * kXlSlices;
@@ -469,7 +513,9 @@ __global__ void __launch_bounds__(kXlThreads, 1)
       }
       __syncwarp();
     }
-  } else if (warp >= 4) {
+  }
+  } else {
+    if constexpr (kXlRegsEpilogue > 96) regs_inc<kXlRegsEpilogue>();
     // ---- epilogue: group g takes accumulator buffer g >> 1 (tiles t = g >> 1 mod 2) and
     // the 16-key half (g & 1) of each of those tiles; half index hx = 2 t + half holds the
     // whole KV blocks [hx * bpt, hx * bpt + bpt) (keys packed 16 per half by the slicer)
@@ -516,17 +562,9 @@ __global__ void __launch_bounds__(kXlThreads, 1)
         for (int c = 0; c < kXlClasses; ++c) tmem_ld8(t_acc + c * kXlKeys + c8 * 8, cv[c]);
         tmem_wait_ld();
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          // classes (weights 2^(7c)): exact int32 pairs (|.| < 2^31), each converted exactly to
-          // fp64; the partial sums below 2^53 are exact, the last fma rounds the exact dot once
-          const int lo32 = static_cast<int>(cv[0][e]) + (static_cast<int>(cv[1][e]) << 7);
-          const int mid32 = static_cast<int>(cv[2][e]) + (static_cast<int>(cv[3][e]) << 7);
-          const int hi32 = static_cast<int>(cv[4][e]) + (static_cast<int>(cv[5][e]) << 7);
-          const double lo = __fma_rn(i32_to_f64(mid32), 16384.0, i32_to_f64(lo32));
-          const double hi = __fma_rn(i32_to_f64(static_cast<int>(cv[6][e])), 16384.0,
-                                     i32_to_f64(hi32));
-          dv[c8 * 8 + e] = __fma_rn(hi, 268435456.0, lo);  // exact dot(X, Y) rounded once
-        }
+        for (int e = 0; e < 8; ++e)  // exact dot(X, Y) rounded once
+          dv[c8 * 8 + e] = class_dot<MODE == kXlAntidiag>(cv[0][e], cv[1][e], cv[2][e], cv[3][e], cv[4][e], cv[5][e],
+                                     cv[6][e]);
       }
 #pragma unroll
       for (int c = kXlSlices; c < kXlClasses; ++c) tmem_zero16(t_acc + c * kXlKeys);
@@ -534,13 +572,13 @@ __global__ void __launch_bounds__(kXlThreads, 1)
       tc_fence_before();
       mbar_arrive(&sm.acc_empty[buf]);
       if (nb == 0) continue;  // odd half count: this half of the last tile holds no block
+      // exact corrections for tiny elements (rare: skipped unless some lane needs one)
+      const uint32_t key_tiny = __ballot_sync(0xffffffffu, kinfo & 1) & valid_mask;
 #pragma unroll
       for (int j = 0; j < kXlHalf; ++j) {
         const int kj = __shfl_sync(0xffffffffu, kinfo, j);
         dv[j] = __dmul_rn(dv[j], pow2((kj >> 1) + qm.e - 2 * kXlGridShift));
       }
-      // exact corrections for tiny elements (rare: skipped unless some lane needs one)
-      const uint32_t key_tiny = __ballot_sync(0xffffffffu, kinfo & 1) & valid_mask;
       if (__any_sync(0xffffffffu, q_tiny && row_ok) || key_tiny != 0u) {
 #pragma unroll 1
         for (int j = 0; j < nvalid; ++j)
@@ -600,6 +638,7 @@ __global__ void __launch_bounds__(kXlThreads, 1)
           l_run = __dadd_rn(__dmul_rn(l_run, rescale(m_run, m_new, sm.exp_tab)), part);
           m_run = m_new;
         } else {
+          auto xsc = [&](int j) { return __dmul_rn(dv[j], p.scale); };  // importance.py:128
           double cmax = -INFINITY;
 #pragma unroll
           for (int j = 0; j < kXlHalf; ++j)
@@ -612,13 +651,11 @@ __global__ void __launch_bounds__(kXlThreads, 1)
             int slow = 0;
 #pragma unroll
             for (int u = 0; u < kP; ++u)
-              ev[u] = exp_nonpos(__dsub_rn(__dmul_rn(dv[bb * kP + u], p.scale), m_new), sm.exp_tab,
-                                 &slow);
+              ev[u] = exp_nonpos(__dsub_rn(xsc(bb * kP + u), m_new), sm.exp_tab, &slow);
             if (slow) {
 #pragma unroll
               for (int u = 0; u < kP; ++u)
-                ev[u] = exp_nonpos_slow(__dsub_rn(__dmul_rn(dv[bb * kP + u], p.scale), m_new),
-                                        sm.exp_tab);
+                ev[u] = exp_nonpos_slow(__dsub_rn(xsc(bb * kP + u), m_new), sm.exp_tab);
             }
             // numpy pairwise order for PER elements (np_pairwise_sum, common.cuh)
             double e;
