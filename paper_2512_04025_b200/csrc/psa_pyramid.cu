@@ -128,33 +128,38 @@ __global__ void __launch_bounds__(128) simcap_kernel(const uint16_t* __restrict_
     reinterpret_cast<uint4*>(blk)[i] = __ldg(reinterpret_cast<const uint4*>(src) + i);
   if (threadIdx.x == 0) cap_s = 1;
   __syncthreads();
-  for (int r = threadIdx.x; r < b_k; r += blockDim.x) {
-    double s = 0.0;
-    for (int c = 0; c < d; ++c) {
-      double x = bf16_bits_to_dbl(blk[r * d + c]);
-      s = __fma_rn(x, x, s);
-    }
-    norms[r] = __dsqrt_rn(s);
+  // one warp per row (pair): lanes take columns lane, lane + 32, ... (conflict-free shared
+  // loads), then a shuffle reduction; the sums are exact, so the order does not matter
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  auto row_dot = [&](int ra, int rb) {
+    double acc = 0.0;
+    for (int c = lane; c < d; c += 32)
+      acc = __fma_rn(bf16_bits_to_dbl(blk[ra * d + c]), bf16_bits_to_dbl(blk[rb * d + c]), acc);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+    return acc;
+  };
+  for (int r = warp; r < b_k; r += nwarps) {
+    const double s = row_dot(r, r);
+    if (lane == 0) norms[r] = __dsqrt_rn(s);
   }
   __syncthreads();
   for (int h = 2; h <= levels; ++h) {
     const int stride = 1 << (h - 1);
     const int np_ = b_k - stride;
     if (np_ <= 0) break;  // uniform across the CTA
-    for (int r = threadIdx.x; r < np_; r += blockDim.x) {
+    for (int r = warp; r < np_; r += nwarps) {
       const double na = norms[r], nb = norms[r + stride];
-      const bool ok = (na > 0.0) && (nb > 0.0);
+      const bool ok = (na > 0.0) && (nb > 0.0);  // warp-uniform
       double c = 0.0;
       if (ok) {
-        double dot = 0.0;
-        for (int cc = 0; cc < d; ++cc)
-          dot = __fma_rn(bf16_bits_to_dbl(blk[r * d + cc]),
-                         bf16_bits_to_dbl(blk[(r + stride) * d + cc]), dot);
-        c = __ddiv_rn(dot, __dmul_rn(na, nb));
+        c = __ddiv_rn(row_dot(r, r + stride), __dmul_rn(na, nb));
         c = fmin(fmax(c, -1.0), 1.0);
       }
-      cosv[r] = c;
-      okf[r] = ok ? 1 : 0;
+      if (lane == 0) {
+        cosv[r] = c;
+        okf[r] = ok ? 1 : 0;
+      }
     }
     __syncthreads();
     if (threadIdx.x == 0) {

@@ -96,35 +96,45 @@ __global__ void __launch_bounds__(256) xl_slice_kernel(const uint16_t* __restric
   const int64_t set = (bh * classes + cls);
   int8_t* dst = slices + set * kXlSlices * static_cast<int64_t>(pk.pad_rows) * kXlRowBytes;
 
-  double v[4] = {0.0, 0.0, 0.0, 0.0};
-  if (valid) {
-    const uint16_t* row = src + (bh * n + rows(idx)) * D;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int c = lane * 4 + e;
-      if (c < D) v[e] = static_cast<double>(__uint_as_float(static_cast<uint32_t>(row[c]) << 16));
-    }
-  }
-  double amax = 0.0;
-  bool finite = true;
+  // Integer decomposition of the bf16 elements |x| = sig * 2^eb (sig < 256): the row exponent
+  // E = floor(log2 max|x|) is the max of the elements' eb + floor(log2 sig), and
+  // X = trunc(x * 2^(27 - E)) is a shift of sig (a right shift drops bits only for "tiny" x).
+  uint2 raw = make_uint2(0u, 0u);
+  if (valid && lane * 4 < D)
+    raw = *reinterpret_cast<const uint2*>(src + (bh * n + rows(idx)) * D + lane * 4);
+  const uint32_t u[4] = {raw.x & 0xFFFFu, raw.x >> 16, raw.y & 0xFFFFu, raw.y >> 16};
+  int sig[4], eb[4];
+  bool fin = true;
+  int emax = -100000;
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
-    amax = fmax(amax, fabs(v[e]));
-    finite = finite && isfinite(v[e]);
+    const int ex = static_cast<int>((u[e] >> 7) & 0xFFu), man = static_cast<int>(u[e] & 0x7Fu);
+    fin = fin && ex != 0xFF;
+    sig[e] = ex ? (128 | man) : man;
+    eb[e] = ex ? ex - 134 : -133;
+    if (sig[e]) emax = max(emax, eb[e] + 31 - __clz(sig[e]));
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-  finite = __all_sync(0xffffffffu, finite);
-  const int E = (amax > 0.0 && finite) ? ilogb(amax) : 0;
-  const double up = ldexp(1.0, kXlGridShift - E);
+  const bool finite = __all_sync(0xffffffffu, fin);
+  emax = __reduce_max_sync(0xffffffffu, emax);
+  const int E = (emax > -100000 && finite) ? emax : 0;
   uint32_t d[kXlSlices] = {0u, 0u, 0u, 0u};
   unsigned tiny_bits = 0;
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
-    const double xf = v[e] * up;
-    const double xt = trunc(xf);
-    if (finite && xt != xf) tiny_bits |= 1u << e;
-    const int X = finite ? static_cast<int>(xt) : 0;
+    const int sh = eb[e] + kXlGridShift - E;  // <= 20 (E >= the element's exponent)
+    uint32_t mag;
+    bool frac;
+    if (sh >= 0) {
+      mag = static_cast<uint32_t>(sig[e]) << sh;
+      frac = false;
+    } else {
+      const int r = -sh;
+      mag = r < 32 ? static_cast<uint32_t>(sig[e]) >> r : 0u;
+      frac = r < 32 ? (static_cast<uint32_t>(sig[e]) & ((1u << r) - 1u)) != 0u : sig[e] != 0;
+    }
+    if (!finite) mag = 0u, frac = false;
+    if (frac) tiny_bits |= 1u << e;
+    const int X = (u[e] & 0x8000u) ? -static_cast<int>(mag) : static_cast<int>(mag);
     d[0] |= static_cast<uint32_t>(X & 127) << (8 * e);
     d[1] |= static_cast<uint32_t>((X >> 7) & 127) << (8 * e);
     d[2] |= static_cast<uint32_t>((X >> 14) & 127) << (8 * e);
@@ -133,16 +143,16 @@ __global__ void __launch_bounds__(256) xl_slice_kernel(const uint16_t* __restric
 #pragma unroll
   for (int s = 0; s < kXlSlices; ++s)
     reinterpret_cast<uint32_t*>(dst + (static_cast<int64_t>(s) * pk.pad_rows + p) * kXlRowBytes)[lane] = d[s];
-  // tiny elements: at most kXlMaxTiny per row, else the head goes to the fp64 fallback
-  const int cnt = __popc(tiny_bits);
-  int before = cnt;
+  // tiny elements: at most kXlMaxTiny per row, else the head goes to the fp64 fallback; slots
+  // in element order (lane-major), counted with one ballot per element position
+  int before = 0, total = 0;
+  const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, before, o);
-    if (lane >= o) before += y;
+  for (int e = 0; e < 4; ++e) {
+    const uint32_t b = __ballot_sync(0xffffffffu, (tiny_bits >> e) & 1u);
+    before += __popc(b & lt);
+    total += __popc(b);
   }
-  const int total = __shfl_sync(0xffffffffu, before, 31);
-  before -= cnt;
   uint32_t dims = 0;
   int slot = before;
 #pragma unroll
@@ -151,8 +161,7 @@ __global__ void __launch_bounds__(256) xl_slice_kernel(const uint16_t* __restric
       if (slot < kXlMaxTiny) dims |= static_cast<uint32_t>(lane * 4 + e) << (7 * slot);
       ++slot;
     }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) dims |= __shfl_xor_sync(0xffffffffu, dims, o);
+  dims = __reduce_or_sync(0xffffffffu, dims);
   if (lane == 0) {
     XlMeta m;
     m.e = E;
