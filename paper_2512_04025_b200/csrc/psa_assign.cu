@@ -183,11 +183,14 @@ PSA_DEV void emit_plan_row(const int8_t* lvl, int n_k, int levels, int b_k, int6
 // of -s, mask.py:107-109). The fp64 bit patterns are monotone for non-negative values (-0.0 is
 // folded into +0.0 first, as the comparison-based sort treats them as equal). A CUB block radix
 // sort orders the rows by the top 32 of the 63 value bits with the column index as payload
-// (7 passes instead of 13); radix sort is stable, so equal keys keep ascending column order.
+// (8 passes of 4-bit digits instead of 16); radix sort is stable, so equal keys keep ascending column order.
 // Entries whose top 32 bits tie but whose low bits differ (rare) are then put in full order by
 // an insertion pass with the same (value desc, column asc) comparator. Padding keys (0) follow
 // every real score, zeros included.
-template <int IPT, int RB = 5>  // 5-bit digits
+#ifndef PSA_ASSIGN_RADIX_BITS
+#define PSA_ASSIGN_RADIX_BITS 4  // A/B at cfg3: 4 bits 0.81 ms, 5 bits 0.85, 6 bits 0.92
+#endif
+template <int IPT, int RB = PSA_ASSIGN_RADIX_BITS>  // digit bits per radix pass
 __global__ void __launch_bounds__(128) assign_levels_kernel(
     const double* __restrict__ S, const int8_t* __restrict__ caps, AssignParams p,
     int8_t* __restrict__ level_map, uint16_t* __restrict__ csr, int32_t* __restrict__ info,

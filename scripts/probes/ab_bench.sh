@@ -5,6 +5,6 @@ cd $GRAFT_REPO_ROOT 2>/dev/null || cd /root/repo
 for rep in 1 2; do
   for lib in scripts/probes/ab/libpsa_*.so; do
     PSA_LIB_PATH=$lib timeout 300 python bench.py --config ${CFG:-cfg3} --steps 20 --warmup 5 --no-cpu-baseline --no-e2e --no-yardsticks > /tmp/ab.json 2>/tmp/ab.log
-    python -c "import json; d=json.load(open('/tmp/ab.json')); print('$lib', 'attn', d['stage_ms']['attention'], 'imp', d['stage_ms']['importance'], 'step', d['ms_per_step'], 'sm_mhz', d['clocks']['sm_mhz'])" || tail -3 /tmp/ab.log
+    python -c "import json; d=json.load(open('/tmp/ab.json')); print('$lib', d['stage_ms'], 'step', d['ms_per_step'], 'sm_mhz', d['clocks']['sm_mhz'])" || tail -3 /tmp/ab.log
   done
 done
