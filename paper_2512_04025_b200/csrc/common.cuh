@@ -48,6 +48,19 @@ PSA_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Wait with an explicit suspend-time hint: the thread sleeps in try_wait until the phase
+// completes (or the hint elapses) instead of re-polling after the short system-dependent limit,
+// so a waiting warp leaves the issue slots to the other warps of its scheduler.
+PSA_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t hint_ns = 1000000u) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(hint_ns)
+      : "memory");
+}
+
 // Same wait with a nanosleep back-off: for roles that run far ahead (producers), so their
 // polling does not take issue slots from the compute warps of the same scheduler.
 PSA_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {

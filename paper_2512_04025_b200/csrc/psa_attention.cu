@@ -121,6 +121,24 @@ struct PlanCursor {
 // Register split via setmaxnreg within the CTA pool of 384 x 168: producer/MMA warpgroup 64,
 // softmax warpgroups 216 (128*64 + 256*216 <= 384*168, else the increase never completes).
 constexpr int kPPThreads = 384;
+// mbarrier waits of the forward kernel: spin (try_wait re-polled after the system-dependent
+// limit) or sleep (try_wait with a suspend-time hint)
+#ifndef PSA_ATTN_SLEEP_SOFT
+#define PSA_ATTN_SLEEP_SOFT 0
+#endif
+#ifndef PSA_ATTN_SLEEP_PROD
+#define PSA_ATTN_SLEEP_PROD 0
+#endif
+#if PSA_ATTN_SLEEP_SOFT
+#define PP_WAIT_SOFT(bar, par) mbar_wait_sleep(bar, par)
+#else
+#define PP_WAIT_SOFT(bar, par) mbar_wait(bar, par)
+#endif
+#if PSA_ATTN_SLEEP_PROD
+#define PP_WAIT_PROD(bar, par) mbar_wait_sleep(bar, par)
+#else
+#define PP_WAIT_PROD(bar, par) mbar_wait(bar, par)
+#endif
 
 
 template <int D>
@@ -248,7 +266,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         for (int t = 0; t < T; ++t) {
           const int ks = t % KST;
           const TileSeg sg = pc.next(p, bhkv, lane);
-          if (t >= KST) mbar_wait(&sm.k_empty[ks], ((t / KST) - 1) & 1);
+          if (t >= KST) PP_WAIT_PROD(&sm.k_empty[ks], ((t / KST) - 1) & 1);
           if (lane == 0) mbar_arrive_expect_tx(&sm.k_full[ks], static_cast<uint32_t>(sg.total) * D * 2);
           __syncwarp();
           if (sg.fits)
@@ -265,7 +283,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         for (int t = 0; t < T; ++t) {
           const int vs = t % VST;
           const TileSeg sg = pc.next(p, bhkv, lane);
-          if (t >= VST) mbar_wait(&sm.v_empty[vs], ((t / VST) - 1) & 1);
+          if (t >= VST) PP_WAIT_PROD(&sm.v_empty[vs], ((t / VST) - 1) & 1);
           if (lane == 0) mbar_arrive_expect_tx(&sm.v_full[vs], static_cast<uint32_t>(sg.total) * D * 2);
           __syncwarp();
           if (sg.fits)
@@ -283,7 +301,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         for (int t = 0; t < T; ++t) {
           const int as = t % AST;
           const TileSeg sg = pc.next(p, bhkv, lane);
-          if (t >= AST) mbar_wait(&sm.aug_empty[as], ((t / AST) - 1) & 1);  // S(t - AST) done
+          if (t >= AST) PP_WAIT_PROD(&sm.aug_empty[as], ((t / AST) - 1) & 1);  // S(t - AST) done
           {  // lane owns keys 4 lane .. 4 lane + 3 (one segment: slots are >= 8 rows, aligned)
             int g = 0;
             for (int q = 1; q < sg.nseg; ++q)
@@ -306,7 +324,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
             // per 8-key chunk: straddle flag, valid keys of the chunk (pad keys of a straddling
             // chunk are masked too, so a row with no visible key stays empty), first key position
             const int ms = t % kMetaRing;
-            if (t >= kMetaRing) mbar_wait(&sm.meta_empty[ms], ((t / kMetaRing) - 1) & 1);
+            if (t >= kMetaRing) PP_WAIT_PROD(&sm.meta_empty[ms], ((t / kMetaRing) - 1) & 1);
             if (sg.fits) {
               const bool straddle = static_cast<int64_t>(sg.j + 1) * p.b_k - 1 > q_lo;
               for (int c = 0; c < sg.sz / 8; ++c) {
@@ -330,9 +348,9 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         const uint64_t qa_desc = umma_desc_noswz(smem_u32(sm.qaug), 128, 0);
         auto issue_s = [&](int t) {
           const int ks = t % KST, as = t % AST, L = t & 1;
-          mbar_wait(&sm.k_full[ks], (t / KST) & 1);
-          if (t >= 2) mbar_wait(&sm.s_free[L], ((t >> 1) - 1) & 1);  // lane read S(t-2)
-          mbar_wait(&sm.aug_full[as], (t / AST) & 1);
+          PP_WAIT_PROD(&sm.k_full[ks], (t / KST) & 1);
+          if (t >= 2) PP_WAIT_PROD(&sm.s_free[L], ((t >> 1) - 1) & 1);  // lane read S(t-2)
+          PP_WAIT_PROD(&sm.aug_full[as], (t / AST) & 1);
           tc_fence_after();
           const uint64_t k_desc0 = umma_desc_sw128(smem_u32(sm.k[ks]), 16, 1024);
           const uint64_t ka_desc = umma_desc_noswz(smem_u32(sm.kaug[as]), 0, 128);
@@ -352,8 +370,8 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         };
         auto issue_pv = [&](int t) {
           const int vs = t % VST, L = t & 1;
-          mbar_wait(&sm.v_full[vs], (t / VST) & 1);
-          mbar_wait(&sm.p_full[L], (t >> 1) & 1);
+          PP_WAIT_PROD(&sm.v_full[vs], (t / VST) & 1);
+          PP_WAIT_PROD(&sm.p_full[L], (t >> 1) & 1);
           tc_fence_after();
           const uint64_t v_desc0 = umma_desc_sw128(smem_u32(sm.v[vs]), kTileRows * 128, 1024);
           const uint64_t p_desc0 = umma_desc_sw128(smem_u32(sm.p[L]), 16, 1024);
@@ -392,7 +410,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     float m_run = -INFINITY, l_run = 0.f;
     for (int t = L; t < T; t += 2) {
       const int ms = t % kMetaRing;
-      mbar_wait(&sm.s_full[L], (t >> 1) & 1);
+      PP_WAIT_SOFT(&sm.s_full[L], (t >> 1) & 1);
       tc_fence_after();
       uint32_t s[4][32];
 #pragma unroll
@@ -407,7 +425,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
 #pragma unroll
       for (int e = 0; e < 128; ++e) y[e] = __uint_as_float(s[e >> 5][e & 31]);
       if (p.causal) {  // token-level mask on straddling level-1 chunks (attention.py:88-108)
-        mbar_wait(&sm.meta_full[ms], (t / kMetaRing) & 1);
+        PP_WAIT_SOFT(&sm.meta_full[ms], (t / kMetaRing) & 1);
 #pragma unroll
         for (int c = 0; c < kChunks; ++c) {
           const uint32_t w = sm.meta[ms][c];
@@ -462,7 +480,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       l_run = l_run * alpha + (ls.x + ls.y);
       // PV(t-2) done: P_L is free and O_L is stable
       if (t >= 2) {
-        mbar_wait(&sm.o_done[L], ((t >> 1) - 1) & 1);
+        PP_WAIT_SOFT(&sm.o_done[L], ((t >> 1) - 1) & 1);
         tc_fence_after();
       }
       if (t >= 2 && __any_sync(0xffffffffu, resc)) {

@@ -51,6 +51,14 @@ constexpr int kXlGroups = 4;        // epilogue warpgroups: (accumulator buffer,
 constexpr int kXlEpiThreads = kXlGroups * 128;
 constexpr int kXlThreads = 128 + kXlEpiThreads;
 constexpr int kXlGridShift = 27;
+#ifndef PSA_XL_SLEEP_WAIT
+#define PSA_XL_SLEEP_WAIT 1
+#endif
+#if PSA_XL_SLEEP_WAIT
+#define XL_WAIT(bar, par) mbar_wait_sleep(bar, par)
+#else
+#define XL_WAIT(bar, par) mbar_wait(bar, par)
+#endif
 
 #ifndef PSA_XL_REGS_EPI
 #define PSA_XL_REGS_EPI 112
@@ -502,7 +510,7 @@ __global__ void __launch_bounds__(kXlThreads, 1)
     tc_fence_after();
     for (int t = 0; t < T; ++t) {
       const int s = t % kXlStages, ab = t % kXlAccBufs;
-      mbar_wait(&sm.k_full[s], (t / kXlStages) & 1);
+      XL_WAIT(&sm.k_full[s], (t / kXlStages) & 1);
       if (t >= kXlAccBufs) mbar_wait_backoff(&sm.acc_empty[ab], ((t / kXlAccBufs) - 1) & 1);
       tc_fence_after();
       if (elect_one()) {
@@ -561,7 +569,7 @@ __global__ void __launch_bounds__(kXlThreads, 1)
       const uint32_t valid_mask = (1u << nvalid) - 1u;
       const XlMeta kml = kmeta[t * kXlKeys + half * kXlHalf + (lane & (kXlHalf - 1))];
       const int kinfo = (kml.e << 1) | ((kml.tiny >> 28) != 0u ? 1 : 0);
-      mbar_wait(&sm.acc_full[buf], (tl >> 1) & 1);
+      XL_WAIT(&sm.acc_full[buf], (tl >> 1) & 1);
       tc_fence_after();
       double dv[kXlHalf];
 #pragma unroll
