@@ -282,6 +282,23 @@ PSA_DEV float2 fmul2(float2 a, float2 b) {
   return r;
 }
 
+// 2^x for a pair on the FMA pipe (FA4-style MUFU offload): round-to-nearest split x = n + f
+// with the 1.5*2^23 trick, f in [-0.5, 0.5], degree-3 polynomial with p(0) = 1 exactly
+// (max rel. error 1.0e-4, far below bf16's 2^-9), exponent added as integer bits. x is
+// clamped at -127, where the result is exactly +0 (so pad keys and -inf give 0 like MUFU).
+PSA_DEV float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -127.f);
+  x.y = fmaxf(x.y, -127.f);
+  const float2 j = fadd2(x, make_float2(12582912.f, 12582912.f));
+  const float2 n = fadd2(j, make_float2(-12582912.f, -12582912.f));
+  const float2 f = ffma2(n, make_float2(-1.f, -1.f), x);
+  float2 q = ffma2(f, make_float2(0.05500815063714981f, 0.05500815063714981f),
+                   make_float2(0.24220973253250122f, 0.24220973253250122f));
+  q = ffma2(q, f, make_float2(0.6932829022407532f, 0.6932829022407532f));
+  q = ffma2(q, f, make_float2(1.f, 1.f));
+  return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(j.x) << 23)),
+                     __int_as_float(__float_as_int(q.y) + (__float_as_int(j.y) << 23)));
+}
 PSA_DEV float fmax3(float a, float b, float c) {
   float r;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));

@@ -123,6 +123,15 @@ struct PlanCursor {
 constexpr int kPPThreads = 384;
 // mbarrier waits of the forward kernel: spin (try_wait re-polled after the system-dependent
 // limit) or sleep (try_wait with a suspend-time hint)
+// Pairs (e + 2, e + 3) of the softmax loop iterations e / 4 whose bit is set take the FMA-pipe
+// exp2 polynomial instead of MUFU.EX2 (FA4-style offload of the exp unit). A/B at cfg3 (round 2,
+// evenly interleaved): 0 / 8 / 16 / 24 polynomial pairs per row-tile: 24.7 / 25.0 / 25.5 / 26.1
+// ms. The MUFU pipe is 64% busy but the lanes are dependency-latency-bound, so every extra
+// instruction costs more than the exp-unit time it frees; all exps stay on MUFU.
+#ifndef PSA_ATTN_POLY_MASK
+#define PSA_ATTN_POLY_MASK 0x00000000u
+#endif
+constexpr uint32_t kPPPolyMask = PSA_ATTN_POLY_MASK;
 #ifndef PSA_ATTN_SLEEP_SOFT
 #define PSA_ATTN_SLEEP_SOFT 0
 #endif
@@ -465,12 +474,14 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       for (int e = 0; e < 128; e += 4) {
         float2 a = ffma2(make_float2(y[e], y[e + 1]), scale2, negm);
         float2 c = ffma2(make_float2(y[e + 2], y[e + 3]), scale2, negm);
-        // every exp on MUFU: an FMA-pipe polynomial for the last 16/32/48/64 columns measured
-        // 26.7/26.5/27.6/28.2 ms against 25.9 ms at cfg3 (the lanes are issue-bound, not MUFU-bound)
         a.x = ex2_approx(a.x);
         a.y = ex2_approx(a.y);
-        c.x = ex2_approx(c.x);
-        c.y = ex2_approx(c.y);
+        if ((kPPPolyMask >> (e >> 2)) & 1u) {  // spread evenly: MUFU and FMA pipes overlap
+          c = ex2_poly2(c);
+        } else {
+          c.x = ex2_approx(c.x);
+          c.y = ex2_approx(c.y);
+        }
         ls0 = fadd2(ls0, a);
         ls1 = fadd2(ls1, c);
         pk[e / 2] = pack_bf16x2(a.x, a.y);
