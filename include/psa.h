@@ -178,6 +178,10 @@ int psa_attn_fwd_scatter(const void* q, const void* k, const void* v, const void
  * [batch, hq, n_q, n_k]) and dO (dout, bf16 like O).  Outputs dq [batch, hq, n, d] and dk, dv
  * [batch, hkv, n, d] (bf16, gradients w.r.t. the RAW K/V: pooled levels are differentiated
  * through their means).  workspace: psa_attn_bwd_workspace_bytes(batch, hq, hkv, n, d) bytes.
+ * Limit: the dK/dV pass keeps the list of (query head, query block) entries of a KV head in
+ * shared memory, 6 bytes each next to ~194 KB of tiles, so (hq / hkv) * n_q must stay below
+ * about 5.6K entries per KV head (e.g. 8 query heads per KV head at n = 128K, b_q = 128 is
+ * over); beyond it the call returns PSA_EINVAL ("too many query blocks per KV head").
  */
 size_t psa_attn_bwd_workspace_bytes(int64_t batch, int hq, int hkv, int64_t n, int d);
 int psa_attn_bwd(const void* q, const void* k, const void* v, const void* k_pyr,

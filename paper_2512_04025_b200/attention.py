@@ -92,7 +92,9 @@ def attention_forward(q4: torch.Tensor, pyr: PyramidKV, plan: MaskPlan, causal: 
 def attention_backward(q4: torch.Tensor, pyr: PyramidKV, plan: MaskPlan, causal: bool,
                        out: torch.Tensor, lse: torch.Tensor, dout: torch.Tensor):
     """Gradients (dq, dk, dv) of attention_forward for the fixed mask ``plan`` (psa_attn_bwd):
-    dk/dv are w.r.t. the raw K/V of ``pyr`` (pooled levels differentiated through their means)."""
+    dk/dv are w.r.t. the raw K/V of ``pyr`` (pooled levels differentiated through their means).
+    Limit (include/psa.h): about 5.6K (query head, query block) entries per KV head, i.e.
+    (Hq / Hkv) * n_q; larger shapes raise the library's "too many query blocks per KV head"."""
     lay = pyr.layout
     B, Hq, n, d = q4.shape
     Hkv = pyr.k_raw.shape[1]
