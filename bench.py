@@ -607,6 +607,37 @@ def main():
                         "wall clock max over ranks, outside the timed region"}
         del full_o
 
+    # ---- the same step replayed from a CUDA graph (graph.py: the chain is sync-free, so its host
+    # work - argument checks, tensor maps, allocations, ctypes calls - is captured once)
+    graph = None
+    if world == 1:
+        try:
+            side = torch.cuda.Stream(device)
+            side.wait_stream(stream)
+            with torch.cuda.stream(side):
+                step()
+            stream.wait_stream(side)
+            cg = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(cg):
+                step()
+            for _ in range(3):
+                cg.replay()
+            torch.cuda.synchronize()
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record(stream)
+            for _ in range(args.steps):
+                cg.replay()
+            b_.record(stream)
+            torch.cuda.synchronize()
+            g_ms = a_.elapsed_time(b_) / args.steps
+            graph = {"ms_per_step": round(g_ms, 4),
+                     "value": round(flops_all / (g_ms * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
+                     "what": "the timed step's kernels captured once into a CUDA graph and "
+                             "replayed (no per-call host work); same inputs and outputs"}
+            del cg
+        except Exception as exc:  # noqa: BLE001 - supplementary; must not kill the line
+            graph = {"error": repr(exc)}
+
     # ---- end-to-end through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e:
@@ -684,6 +715,7 @@ def main():
                      "executed_frac_of_burst": round(exec_flops / (attn_ms_max * 1e-3) / 1e12 / peak_burst, 4)
                      if world == 1 else None},
         "e2e": e2e,
+        "graph": graph,
         "gather": gather,
         "yardsticks": yard,
         "gpu_launches": launches_per_step * args.steps,

@@ -20,6 +20,7 @@ from .pipeline import (PipelineResult, PSAResult, RunConfig, psa_attention, psa_
                        relative_error, report_to_json, run_pipeline)
 from .pyramid import PyramidKV, build_pyramid, build_pyramid_gather, level_cap_from_similarity
 from .autograd import psa_attention_differentiable
+from .graph import CapturedForward
 from .tensorfile import read_tensor, write_tensor
 from .schedule import (ExecutionTile, Segment, TileSchedule, UtilizationStats, build_schedule,
                        execute_schedule, plan_utilization, utilization)
@@ -27,7 +28,7 @@ from .schedule import (ExecutionTile, Segment, TileSchedule, UtilizationStats, b
 __version__ = "0.1.0"
 
 __all__ = [
-    "AttentionOutput", "BlockLayout", "LN2", "LevelThresholds", "MaskPlan", "NumericError",
+    "AttentionOutput", "CapturedForward", "BlockLayout", "LN2", "LevelThresholds", "MaskPlan", "NumericError",
     "Permutation", "apply_permutation", "hilbert_order", "invert_permutation",
     "ExecutionTile", "Segment", "TileSchedule", "UtilizationStats", "build_schedule",
     "execute_schedule", "plan_utilization", "utilization", "psa_reference",

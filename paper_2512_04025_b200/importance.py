@@ -53,12 +53,16 @@ def query_blocks(qblocks, layout: BlockLayout, device) -> torch.Tensor | None:
     return it as a device int32 tensor, or None for every block."""
     if qblocks is None:
         return None
+    if getattr(qblocks, "_psa_n_q", None) == layout.n_q and qblocks.device == torch.device(device):
+        return qblocks  # validated already (no host round trip: capturable in a CUDA graph)
     blk = torch.as_tensor(qblocks, dtype=torch.int64).reshape(-1).cpu()
     if blk.numel() == 0 or int(blk.min()) < 0 or int(blk.max()) >= layout.n_q:
         raise ValidationError(f"query blocks must be a non-empty subset of 0..{layout.n_q - 1}")
     if torch.unique(blk).numel() != blk.numel():
         raise ValidationError("query blocks must be distinct")
-    return blk.to(torch.int32).to(device)
+    out = blk.to(torch.int32).to(device)
+    out._psa_n_q = layout.n_q
+    return out
 
 
 def importance_scores(q4: torch.Tensor, k4: torch.Tensor, layout: BlockLayout,
