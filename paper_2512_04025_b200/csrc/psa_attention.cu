@@ -184,6 +184,24 @@ struct PP2Smem {
   uint32_t tmem_base;
 };
 
+// Optional clock64 trace (-DPSA_TRACE; scripts/probes/pp2_trace3.py): 8 CTAs spaced through the
+// grid record per KV tile t < 256: 0 lane (t&1) starts waiting for S(t), 1 S(t) ready, 2 tile
+// max done, 3 exp loop done, 4 P(t) stored and released, 5 S(t) issued, 6 PV(t) issued, 7 the MMA
+// warp starts waiting for P(t), 8 K(t) TMA issued, 9 V(t) TMA issued, 10 segments (TMA boxes / 2)
+// of K tile t (a count), 11 the MMA warp sees K(t) full, 12 ... s_free, 13 ... aug_full (the
+// lanes' first warps, the MMA warp and the producers' lane 0).
+#ifdef PSA_TRACE
+__device__ long long g_pp2_trace[8][14][256];
+#define PP2_TRACE(ev, t)                                                              \
+  do {                                                                                \
+    if (tslot >= 0 && (t) < 256) g_pp2_trace[tslot][ev][t] = clock64();               \
+  } while (0)
+#else
+#define PP2_TRACE(ev, t) \
+  do {                   \
+  } while (0)
+#endif
+
 template <int D>
 __global__ void __launch_bounds__(kPPThreads, 1)
     psa_attn_pp2_kernel(const __grid_constant__ AttnMaps maps, const AttnParams p,
@@ -198,6 +216,10 @@ __global__ void __launch_bounds__(kPPThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t unit = blockIdx.x;
+#ifdef PSA_TRACE
+  const int tstep = static_cast<int>(gridDim.x) / 8;
+  const int tslot = (static_cast<int>(blockIdx.x) % tstep == tstep / 2) ? static_cast<int>(blockIdx.x) / tstep : -1;
+#endif
   const int bhq = static_cast<int>(unit / p.n_qs);
   const int il = static_cast<int>(unit % p.n_qs);
   const int i = p.qblk != nullptr ? p.qblk[il] : il;
@@ -277,6 +299,10 @@ __global__ void __launch_bounds__(kPPThreads, 1)
           const TileSeg sg = pc.next(p, bhkv, lane);
           if (t >= KST) PP_WAIT_PROD(&sm.k_empty[ks], ((t / KST) - 1) & 1);
           if (lane == 0) mbar_arrive_expect_tx(&sm.k_full[ks], static_cast<uint32_t>(sg.total) * D * 2);
+          if (lane == 0) PP2_TRACE(8, t);
+#ifdef PSA_TRACE
+          if (lane == 0 && tslot >= 0 && t < 256) g_pp2_trace[tslot][10][t] = sg.nseg;
+#endif
           __syncwarp();
           if (sg.fits)
             for (int c = 0; c < D / 64; ++c)
@@ -294,6 +320,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
           const TileSeg sg = pc.next(p, bhkv, lane);
           if (t >= VST) PP_WAIT_PROD(&sm.v_empty[vs], ((t / VST) - 1) & 1);
           if (lane == 0) mbar_arrive_expect_tx(&sm.v_full[vs], static_cast<uint32_t>(sg.total) * D * 2);
+          if (lane == 0) PP2_TRACE(9, t);
           __syncwarp();
           if (sg.fits)
             for (int c = 0; c < D / 64; ++c)
@@ -358,8 +385,11 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         auto issue_s = [&](int t) {
           const int ks = t % KST, as = t % AST, L = t & 1;
           PP_WAIT_PROD(&sm.k_full[ks], (t / KST) & 1);
+          if (lane == 0) PP2_TRACE(11, t);
           if (t >= 2) PP_WAIT_PROD(&sm.s_free[L], ((t >> 1) - 1) & 1);  // lane read S(t-2)
+          if (lane == 0) PP2_TRACE(12, t);
           PP_WAIT_PROD(&sm.aug_full[as], (t / AST) & 1);
+          if (lane == 0) PP2_TRACE(13, t);
           tc_fence_after();
           const uint64_t k_desc0 = umma_desc_sw128(smem_u32(sm.k[ks]), 16, 1024);
           const uint64_t ka_desc = umma_desc_noswz(smem_u32(sm.kaug[as]), 0, 128);
@@ -371,6 +401,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
                           kk > 0 ? 1u : 0u);
             }
             mma_bf16_ss(tmem + L * 128, qa_desc, ka_desc, idesc_s, 1u);  // + level bias
+            PP2_TRACE(5, t);
             mma_commit(&sm.k_empty[ks]);
             mma_commit(&sm.aug_empty[as]);
             mma_commit(&sm.s_full[L]);
@@ -380,6 +411,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         auto issue_pv = [&](int t) {
           const int vs = t % VST, L = t & 1;
           PP_WAIT_PROD(&sm.v_full[vs], (t / VST) & 1);
+          if (lane == 0) PP2_TRACE(7, t);
           PP_WAIT_PROD(&sm.p_full[L], (t >> 1) & 1);
           tc_fence_after();
           const uint64_t v_desc0 = umma_desc_sw128(smem_u32(sm.v[vs]), kTileRows * 128, 1024);
@@ -391,6 +423,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
               mma_bf16_ss(tmem + kO0 + L * D, p_desc0 + poff, v_desc0 + ((kk * 16 * 128) >> 4),
                           idesc_o, (t >= 2 || kk > 0) ? 1u : 0u);
             }
+            PP2_TRACE(6, t);
             mma_commit(&sm.v_empty[vs]);
             mma_commit(&sm.o_done[L]);
           }
@@ -419,7 +452,10 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     float m_run = -INFINITY, l_run = 0.f;
     for (int t = L; t < T; t += 2) {
       const int ms = t % kMetaRing;
+      const bool tr = wq == 0 && lane == 0;
+      if (tr) PP2_TRACE(0, t);
       PP_WAIT_SOFT(&sm.s_full[L], (t >> 1) & 1);
+      if (tr) PP2_TRACE(1, t);
       tc_fence_after();
       uint32_t s[4][32];
 #pragma unroll
@@ -470,6 +506,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       const float2 negm = make_float2(-m_use, -m_use);
       float2 ls0 = make_float2(0.f, 0.f), ls1 = make_float2(0.f, 0.f);
       uint32_t pk[64];
+      if (tr) PP2_TRACE(2, t);
 #pragma unroll
       for (int e = 0; e < 128; e += 4) {
         float2 a = ffma2(make_float2(y[e], y[e + 1]), scale2, negm);
@@ -487,6 +524,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         pk[e / 2] = pack_bf16x2(a.x, a.y);
         pk[e / 2 + 1] = pack_bf16x2(c.x, c.y);
       }
+      if (tr) PP2_TRACE(3, t);
       const float2 ls = fadd2(ls0, ls1);
       l_run = l_run * alpha + (ls.x + ls.y);
       // PV(t-2) done: P_L is free and O_L is stable
@@ -521,6 +559,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.p_full[L]);
+      if (tr) PP2_TRACE(4, t);
     }
 
     // ---------------------------------------------------------------- merge + epilogue
@@ -1602,3 +1641,10 @@ extern "C" int psa_attn_fwd(const void* q, const void* k, const void* v, const v
   return psa_attn_fwd_scatter(q, k, v, k_pyr, v_pyr, batch, hq, hkv, n, d, b_q, b_k, levels,
                               plan_csr, plan_info, causal, out, lse, skipped_rows, nullptr, stream);
 }
+
+#ifdef PSA_TRACE
+// Copies the forward kernel's clock64 trace (8 x 14 x 256 int64) to host memory.
+extern "C" int psa_debug_pp2_trace(long long* host) {
+  return cudaMemcpyFromSymbol(host, psa::g_pp2_trace, sizeof(psa::g_pp2_trace)) == cudaSuccess ? 0 : 1;
+}
+#endif
