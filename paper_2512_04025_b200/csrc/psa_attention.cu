@@ -150,9 +150,16 @@ constexpr uint32_t kPPPolyMask = PSA_ATTN_POLY_MASK;
 #endif
 
 
+// PSA_ATTN_SHARED_P: one P buffer for both lanes (a lane stores P(t) once the other lane's
+// PV(t-1) has read P(t-1)); the freed 32 KB give K a third stage at D = 128.
+#ifndef PSA_ATTN_SHARED_P
+#define PSA_ATTN_SHARED_P 0
+#endif
+constexpr bool kPPSharedP = PSA_ATTN_SHARED_P;
+constexpr int kPPBufsP = kPPSharedP ? 1 : 2;
 template <int D>
 struct PP2Cfg {
-  static constexpr int kKStages = D == 128 ? 2 : 3;
+  static constexpr int kKStages = D == 128 ? (kPPSharedP ? 3 : 2) : 3;
   static constexpr int kVStages = D == 128 ? 2 : 3;
   static constexpr int kAugStages = D == 128 ? 1 : 2;  // one 2 KB stage is all that fits at D=128
   static constexpr int kTileBytes = kTileRows * D * 2;
@@ -171,7 +178,7 @@ struct PP2Smem {
   uint8_t q[kTileRows * D * 2];
   uint8_t k[C::kKStages][C::kTileBytes];
   uint8_t v[C::kVStages][C::kTileBytes];
-  uint8_t p[2][kTileRows * kTileRows * 2];
+  uint8_t p[kPPBufsP][kTileRows * kTileRows * 2];
   uint8_t kaug[C::kAugStages][kTileRows * 16];
   uint8_t qaug[256];
   uint32_t meta[kMetaRing][kChunks];
@@ -415,7 +422,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
           PP_WAIT_PROD(&sm.p_full[L], (t >> 1) & 1);
           tc_fence_after();
           const uint64_t v_desc0 = umma_desc_sw128(smem_u32(sm.v[vs]), kTileRows * 128, 1024);
-          const uint64_t p_desc0 = umma_desc_sw128(smem_u32(sm.p[L]), 16, 1024);
+          const uint64_t p_desc0 = umma_desc_sw128(smem_u32(sm.p[kPPSharedP ? 0 : L]), 16, 1024);
           if (elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < kTileRows / 16; ++kk) {
@@ -543,8 +550,12 @@ __global__ void __launch_bounds__(kPPThreads, 1)
           tmem_st32(t_lane + kO0 + L * D + c4 * 32, o);
         }
       }
+      if (kPPSharedP && t >= 1) {  // the shared P buffer: the other lane's PV(t-1) has read it
+        PP_WAIT_SOFT(&sm.o_done[L ^ 1], ((t - 1) >> 1) & 1);
+        tc_fence_after();
+      }
       {  // P (bf16) -> shared memory, UMMA K-major 128B-swizzled: [key half][row][128 B]
-        uint8_t* prow = sm.p[L] + row * 128;
+        uint8_t* prow = sm.p[kPPSharedP ? 0 : L] + row * 128;
         const int sw = row & 7;
 #pragma unroll
         for (int c = 0; c < 2; ++c)
@@ -565,13 +576,19 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     // ---------------------------------------------------------------- merge + epilogue
     const int cnt0 = (T + 1) >> 1, cnt1 = T >> 1;  // tiles of lane 0 / lane 1
     const int cnt_me = L == 0 ? cnt0 : cnt1;
-    if (cnt_me > 0) mbar_wait(&sm.o_done[L], (cnt_me - 1) & 1);  // P_L no longer read
-    float* red = reinterpret_cast<float*>(sm.p[L]);
+    if (kPPSharedP) {  // every PV has read the shared P buffer
+      if (cnt0 > 0) mbar_wait(&sm.o_done[0], (cnt0 - 1) & 1);
+      if (cnt1 > 0) mbar_wait(&sm.o_done[1], (cnt1 - 1) & 1);
+    } else if (cnt_me > 0) {
+      mbar_wait(&sm.o_done[L], (cnt_me - 1) & 1);  // P_L no longer read
+    }
+    constexpr int kRedStride = kPPSharedP ? 2 * kTileRows : kTileRows * kTileRows / 2;  // floats
+    float* red = reinterpret_cast<float*>(sm.p[0]) + L * kRedStride;
     red[row] = m_run;
     red[kTileRows + row] = l_run;
     named_bar_sync(1, 2 * kTileRows);
     const float* red0 = reinterpret_cast<const float*>(sm.p[0]);
-    const float* red1 = reinterpret_cast<const float*>(sm.p[1]);
+    const float* red1 = reinterpret_cast<const float*>(sm.p[0]) + kRedStride;
     const float m0 = red0[row], m1 = red1[row];
     const float l0 = red0[kTileRows + row], l1 = red1[kTileRows + row];
     const float m = fmaxf(m0, m1);
