@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import json
 import math
+import os
 from dataclasses import dataclass, fields
 
 import torch
@@ -142,11 +143,21 @@ class PSAResult:
         return int(self.skipped.item())
 
 
+_NVTX = os.environ.get("PSA_NVTX", "0") not in ("", "0")
+
+
 def _stage(name: str, fn, *args, **kw):
+    """One stage of the fused call: errors tagged like pipeline.py:247-253; with PSA_NVTX=1 the
+    stage is an NVTX range (``psa:<stage>``) for nsys / ncu --nvtx timelines."""
+    if _NVTX:
+        torch.cuda.nvtx.range_push(f"psa:{name}")
     try:
         return fn(*args, **kw)
     except (ValidationError, NumericError) as exc:  # same tagging as pipeline.py:247-253
         raise type(exc)(f"[stage: {name}] {exc}") from exc
+    finally:
+        if _NVTX:
+            torch.cuda.nvtx.range_pop()
 
 
 def _mask_rule(cfg: RunConfig, levels: int):
