@@ -39,7 +39,7 @@ lib = _lib.load()
 lib.psa_debug_pp2_trace.argtypes = [ctypes.c_void_p]
 assert lib.psa_debug_pp2_trace(buf.ctypes.data) == 0
 os.makedirs("gpurun_out", exist_ok=True)
-np.save("gpurun_out/pp2_trace3.npy", buf)
+np.save(os.environ.get("TRACE_OUT", "gpurun_out/pp2_trace3.npy"), buf)
 
 ph = {k_: [] for k_ in ("S wait", "ldtm+max", "exp", "store+release", "S issue->ready",
                         "P ready->PV issue", "MMA waits P", "lane period (2 tiles)",
@@ -85,7 +85,15 @@ for k_, v_ in ph.items():
               f"p90 {np.percentile(v_, 90):9.1f}")
 tr = buf[3]
 t0 = tr[5, 0]
-print("\ntimeline CTA slot 3 (cycles from S(0) issue): t | Kiss Siss Sready maxdone expdone Prel PVwait PViss")
+print("\ntimeline CTA slot 3 (cycles from S(0) issue): t | Kiss Kfull Siss Sready maxdone expdone Prel Viss PVwait PViss")
 for t in range(8, 20):
     e = tr[:, t] - t0
-    print(f"{t:3d} L{t & 1} | {e[8]:8d} {e[5]:8d} {e[1]:8d} {e[2]:8d} {e[3]:8d} {e[4]:8d} {e[7]:8d} {e[6]:8d}")
+    print(f"{t:3d} L{t & 1} | {e[8]:8d} {e[11]:8d} {e[5]:8d} {e[1]:8d} {e[2]:8d} {e[3]:8d} {e[4]:8d} {e[9]:8d} {e[7]:8d} {e[6]:8d}")
+vk = []
+for s in range(8):
+    tr_ = buf[s]
+    T = int((tr_[1] > 0).sum())
+    for t in range(4, T - 4):
+        vk.append((tr_[9, t], tr_[7, t], tr_[8, t + 1]))
+vk = np.array(vk)
+print("V(t) issue -> MMA reaches PV(t) (median):", np.median(vk[:, 1] - vk[:, 0]))
