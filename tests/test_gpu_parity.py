@@ -499,3 +499,55 @@ def test_plan_utilization_counts_executed_tiles():
     counts = res.plan.level_counts.cpu().tolist()
     assert u.useful_rows == sum(c * (b >> (h - 1)) for h, c in enumerate(counts) if h)
     assert 0.5 < u.utilization <= 1.0
+
+
+# ------------------------------------------------------------------ more layouts (round 2)
+# b_q != b_k for the sampled estimator, a b_q that is not a power of two, deep pyramids (6 and
+# 8 levels: level-8 blocks pool to one row), d = 64 with the antidiagonal estimator under causal
+# GQA, and batch 2 -- each against the oracle's stage order (level map ==, O within the bar).
+EXTRA = {
+    "bq128_bk64_sampled": dict(n=4096, d=128, b_q=128, b_k=64, levels=4, hq=2, hkv=2,
+                               kw=dict(estimator="sampled-max", s_q=8, s_k=8, seed=1,
+                                       mask="threshold", thresholds=TAUS_CFG1)),
+    "bq90_bk64": dict(n=5760, d=128, b_q=90, b_k=64, levels=4, hq=2, hkv=1,
+                      kw=dict(estimator="sampled-max", s_q=8, s_k=8, seed=2, mask="threshold",
+                              thresholds=TAUS_CFG1)),
+    "levels6_b96_d64": dict(n=3072, d=64, b_q=96, b_k=96, levels=6, hq=2, hkv=2,
+                            kw=dict(estimator="sampled-max", s_q=8, s_k=8, seed=3, mask="threshold",
+                                    thresholds=(0.12, 0.2, 0.28, 0.36, 0.45, 0.95))),
+    "levels8_b128": dict(n=4096, d=128, b_q=128, b_k=128, levels=8, hq=2, hkv=2,
+                         kw=dict(estimator="sampled-max", s_q=8, s_k=8, seed=4, mask="threshold",
+                                 thresholds=(0.1, 0.16, 0.22, 0.28, 0.34, 0.4, 0.5, 0.95))),
+    "antidiag_d64_causal_gqa": dict(n=4096, d=64, b_q=64, b_k=32, levels=4, hq=6, hkv=2,
+                                    kw=dict(estimator="antidiagonal", stride=4, mask="threshold",
+                                            thresholds=TAUS_CFG1, causal=True)),
+    "batch2_causal": dict(n=2048, d=128, b_q=64, b_k=64, levels=4, hq=2, hkv=2, batch=2,
+                          kw=dict(estimator="sampled-max", s_q=8, s_k=8, seed=5, mask="threshold",
+                                  thresholds=TAUS_CFG1, causal=True)),
+}
+
+
+@pytest.mark.parametrize("case", sorted(EXTRA))
+def test_pipeline_more_layouts(case):
+    psa = _psa()
+    c = EXTRA[case]
+    n, d, hq, hkv, batch = c["n"], c["d"], c["hq"], c["hkv"], c.get("batch", 1)
+    qs, ks, vs = zip(*(gaussian_qkv(41 + bi, hq, n, d, hkv) for bi in range(batch)))
+    q4, k4, v4 = (torch.stack([to_dev(x) for x in xs]) for xs in (qs, ks, vs))
+    res = psa.psa_attention(q4, k4, v4, b_q=c["b_q"], b_k=c["b_k"], levels=c["levels"],
+                            tile_len=128, **c["kw"])
+    lm = res.level_map.cpu().numpy()
+    out = res.out.float().cpu().numpy()
+    lay = orc.Layout(n, d, c["b_q"], c["b_k"], c["levels"])
+    okw = {x: c["kw"].get(x) for x in ("estimator", "s_q", "s_k", "seed", "mask", "thresholds",
+                                       "stride", "causal")}
+    okw["causal"] = bool(okw["causal"])
+    mism = 0
+    for bi in range(batch):
+        for h in range(hq):
+            hk = h // (hq // hkv)
+            r = orc.run_head(qs[bi][h], ks[bi][hk], vs[bi][hk], lay, executor="materialized",
+                             **okw)
+            mism += int((lm[bi, h] != r["mask"]).sum())
+            assert rel_l2(out[bi, h], r["out"]) <= 5e-3, (bi, h)
+    assert mism == 0
