@@ -340,9 +340,14 @@ class HeadWorkers:
 
     def close(self):
         for c in self.conns:
-            c.send(None)
+            try:
+                c.send(None)
+            except (BrokenPipeError, EOFError, OSError):  # a worker that already died
+                pass
         for p_ in self.procs:
             p_.join(timeout=30)
+            if p_.is_alive():
+                p_.terminate()
 
 
 def cpu_baseline(cfg, q, k, v, gpu=None, blocks_per_head=None, max_workers=None):
