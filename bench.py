@@ -638,7 +638,9 @@ def main():
             graph = {"ms_per_step": round(g_ms, 4),
                      "value": round(flops_all / (g_ms * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
                      "what": "the timed step's kernels captured once into a CUDA graph and "
-                             "replayed (no per-call host work); same inputs and outputs"}
+                             "replayed (no per-call host work); same inputs and outputs; timed "
+                             "right after the eager region, so on a hotter, possibly more "
+                             "power-capped GPU (it matters for launch-bound shapes, not cfg3)"}
             del cg
         except Exception as exc:  # noqa: BLE001 - supplementary; must not kill the line
             graph = {"error": repr(exc)}
